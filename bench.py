@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""SGMV benchmark -- BASELINE.json metric "SGMV us/layer & HBM GB/s vs batch across
+Distinct/Uniform/Skewed/Identical", headline workload configs[1]:
+
+    Llama-2-7B  h=4096, r=16, batch 64 decode rows, Distinct popularity, 1x B200
+
+A *step* is one decode step's LoRA work: 7 projection sites x 32 layers = 224
+fused SGMV launches (one shrink+expand pair each -- the paper's "LoRA operator",
+PAPER.md:516), every launch on its own (site, layer) weights and its own x / y
+buffers, replayed from a CUDA graph.  ``value`` is microseconds per LoRA site
+(= "us/layer" in the reference's sense, cost_model.cpp:53-61), lower is better.
+Weights rotate over a 3.7 GB pool and x/y over 235 MB per step, so every launch
+reads HBM, not L2 (config.l2 says so).
+
+Algorithmic bytes per launch (cost_model.cpp:59):
+    2 * (s_n * (h + r) + n * h * r) * 2 B  = 17,829,888 B at the headline config.
+
+--impl reference times the reference's own CPU SGMV (oracle/_ref, compiled from
+/root/reference/proj/core/src/sgmv.cpp; else the oracle/ restatement) on all
+host cores for the same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+POPS = {"distinct": 0, "uniform": 1, "skewed": 2, "identical": 3}
+SITES_PER_LAYER, LAYERS = 7, 32
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--rank", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--popularity", choices=list(POPS), default="distinct")
+    ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
+    ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--sites", type=int, default=SITES_PER_LAYER * LAYERS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also print per-(popularity,batch) lines to stderr")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no graph, no extras)")
+    return ap.parse_args()
+
+
+def alg_bytes(rows, nseg, h, r, e=2):
+    return 2 * (rows * (h + r) + nseg * h * r) * e  # cost_model.cpp:59
+
+
+def alg_flop(rows, h, r):
+    return 4 * rows * h * r  # cost_model.cpp:58
+
+
+def segments(pop: str, batch: int, seed: int = 11):
+    """assign_models grouped by ascending id (experiments.cpp:56-76), via the workload port."""
+    from paper_2310_18547_b200.workload import assign_models
+    ids = assign_models(batch, POPS[pop], 1.5, seed)
+    uniq = sorted(set(ids))
+    bounds = [0]
+    for u in uniq:
+        bounds.append(bounds[-1] + sum(1 for i in ids if i == u))
+    return bounds
+
+
+def workload_name(a):
+    return f"llama2-7b-lora h={a.hidden} r={a.rank} batch={a.batch} decode {a.popularity} ({a.dtype})"
+
+
+# ----------------------------------------------------------------------------------
+# clocks (NVML, sampled every 10 ms during the timed region)
+# ----------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------
+# CPU baselines
+# ----------------------------------------------------------------------------------
+def _cpu_problem(a, seed=5):
+    from oracle.oracle import Oracle
+    o = Oracle()
+    bounds = np.array(segments(a.popularity, a.batch), dtype=np.uint64)
+    g = o.rng(seed)
+    n = len(bounds) - 1
+    h, r = a.hidden, a.rank
+    x = g.fill_pm1(a.batch * h).reshape(a.batch, h)
+    A = g.fill_pm1(n * h * r).reshape(n, h, r)
+    B = g.fill_pm1(n * r * h).reshape(n, r, h)
+    # the CPU gets the dequantised 16-bit values, like the GPU
+    q = np.float16 if a.dtype == "fp16" else np.float32
+    return [np.asarray(t.astype(q), dtype=np.float64) for t in (x, A, B)] + [bounds]
+
+
+def cpu_impl():
+    from oracle.oracle import Oracle, Reference, reference_available
+    if reference_available():
+        return Reference(), "reference"
+    return Oracle(), "port"
+
+
+def cpu_baseline(a, budget_s=10.0):
+    """Reference SGMV (fp64, 1 thread, as shipped) on a bounded sample of the workload."""
+    impl, kind = cpu_impl()
+    x, A, B, bounds = _cpu_problem(a)
+    impl.lora_addon(x, bounds, A, B)  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        impl.lora_addon(x, bounds, A, B)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 2000:
+            break
+    return {"value": el / n * 1e6, "unit": "us/layer", "cores": 1, "kind": kind,
+            "sample": f"{n} x lora_addon(batch={a.batch}, {a.popularity}, h={a.hidden}, r={a.rank}) fp64 "
+                      f"on dequantised {a.dtype} inputs, {el:.1f} s, 1 thread ({'oracle/_ref' if kind == 'reference' else 'oracle port'})"}
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    impl, kind = cpu_impl()
+    threads = os.cpu_count() or 1
+    problems = [_cpu_problem(a, seed=5 + t) for t in range(threads)]
+
+    def one_step():
+        ths = [threading.Thread(target=impl.lora_addon, args=(p[0], p[3], p[1], p[2])) for p in problems]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+
+    for _ in range(a.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        one_step()
+    el = time.perf_counter() - t0
+    sites = a.steps * threads
+    us = el / sites * 1e6
+    line = {"metric": "SGMV us/layer (LoRA shrink+expand per projection site)", "value": us, "unit": "us/layer",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": workload_name(a), "hidden": a.hidden, "rank": a.rank, "batch": a.batch,
+                       "popularity": a.popularity, "step": f"{threads} concurrent lora_addon calls (one per host thread)"},
+            "cpu_baseline": {"value": us, "unit": "us/layer", "cores": threads, "kind": kind,
+                             "sample": f"{sites} lora_addon calls over {threads} threads, {el:.1f} s"},
+            "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_18547_b200 as lsg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = torch.float16 if a.dtype == "fp16" else torch.bfloat16
+    lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
+    h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
+    bounds = segments(a.popularity, batch)
+    nseg = len(bounds) - 1
+    # Request-partitioned weak scaling: every rank owns its own batch of `batch` rows
+    # and its own replica of the adapter pool -- no collective on the data path.
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    pool = lsg.AdapterPool(nseg, sites, h, h, r, dtype)
+    pool.a.uniform_(-1, 1, generator=gen)
+    pool.b.uniform_(-1, 1, generator=gen)
+    xs = torch.empty(sites, batch, h, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen)
+    ys = torch.zeros(sites, batch, h, dtype=dtype, device="cuda")
+    seg_starts = torch.tensor(bounds, dtype=torch.int32, device="cuda")
+    seg_slot = torch.arange(nseg, dtype=torch.int32, device="cuda")
+    bytes_per_launch = alg_bytes(batch, nseg, h, r)
+    info = lsg.query_launch(pool, nseg, batch)
+
+    def step():
+        for s in range(sites):
+            lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
+
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    if a.profile:
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, a.warmup)):
+                step()
+        torch.cuda.synchronize()
+        return
+    with torch.cuda.stream(stream):
+        step()  # eager warm-up (sets function attributes before capture)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    for _ in range(max(3, a.warmup)):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(k):
+                fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    with ClockSampler(local) as clk:
+        ms = timed(graph.replay, a.steps)
+    ms_step = ms / a.steps
+    us_site = ms_step * 1e3 / sites  # per-rank device time per launch
+    value = ms * 1e3 / (a.steps * sites * world)  # whole job: max-over-ranks time / all sites
+
+    extra = {}
+    # isolated single-launch latency (no PDL overlap), L2 flushed between launches
+    lsg.set_option(lsg.LSG_OPT_PDL, 0)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    lat = []
+    for i in range(20):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            lsg.sgmv(ys[i], xs[i], pool, seg_starts, seg_slot, i)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        lat.append(e0.elapsed_time(e1) * 1e3)
+    extra["isolated_launch_us_median"] = statistics.median(lat)
+    graph_nopdl = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_nopdl, stream=stream):
+        step()
+    graph_nopdl.replay()
+    ms_nopdl = timed(graph_nopdl.replay, max(3, a.steps // 2)) / max(3, a.steps // 2)
+    extra["us_per_launch_no_pdl"] = ms_nopdl * 1e3 / sites
+    lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
+    del flush
+
+    # e2e through the public API: pinned host x in, host y out, every launch, every step
+    e2e = None
+    if not a.no_e2e:
+        hx = torch.empty(sites, batch, h, dtype=dtype, pin_memory=True)
+        hx.copy_(xs.cpu())
+        hy = torch.empty(sites, batch, h, dtype=dtype, pin_memory=True)
+
+        def e2e_step():
+            for s in range(sites):
+                xs[s].copy_(hx[s], non_blocking=True)
+                lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
+                hy[s].copy_(ys[s], non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            e2e_step()
+        torch.cuda.synchronize()
+        ke = max(2, min(a.steps, 10))
+        t0 = time.perf_counter()
+        ms_e2e = timed(e2e_step, ke)
+        _ = time.perf_counter() - t0
+        e2e = {"value": ms_e2e * 1e3 / (ke * sites * world), "unit": "us/layer",
+               "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
+               "d2h_bytes_per_step": int(hy.numel() * hy.element_size())}
+
+    if a.sweep and rank == 0:
+        sweep(a, lsg, torch, dtype, stream)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md 6.65 TB/s)"
+    peak = peak or 6650.0
+    achieved = bytes_per_launch / (us_site * 1e-6) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        key = f"h{h}_r{r}_b{batch}_{a.popularity}_{a.dtype}"
+        traffic = prof.get(key)
+    except Exception:
+        pass
+    line = {
+        "metric": "SGMV us/layer (LoRA shrink+expand per projection site)",
+        "value": value, "unit": "us/layer", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": a.dtype + " (fp32 accumulate)", "data": "synthetic (U[-1,1) adapters/activations, random init)",
+        "config": {"workload": workload_name(a), "model": "Llama-2-7B LoRA sites (h x h)", "hidden": h, "rank": r,
+                   "batch_per_gpu": batch, "global_batch": batch * world, "segments": nseg,
+                   "popularity": a.popularity, "step": f"{sites} fused SGMV launches (7 sites x 32 layers), CUDA graph",
+                   "parallelism": f"request-partitioned x{world} (no collective)",
+                   "l2": "inputs larger than L2: weights rotate over a "
+                         f"{pool.a.numel() * 2 * 2 / 2**30:.2f} GiB pool, x/y over {2 * xs.numel() * 2 / 2**20:.0f} MiB per step",
+                   "pdl": bool(a.pdl), "launch": info},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": bytes_per_launch, "flop_per_launch": alg_flop(batch, h, r)},
+        "gpu_launches": a.steps * sites,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        **extra,
+    }
+    if not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(a)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sweep(a, lsg, torch, dtype, stream):
+    """Batch x popularity sweep at the configured shape (reported on stderr)."""
+    h, r = a.hidden, a.rank
+    for pop in ("distinct", "uniform", "skewed", "identical"):
+        for batch in (1, 2, 4, 8, 16, 32, 64):
+            bounds = segments(pop, batch)
+            nseg = len(bounds) - 1
+            L = 224
+            pool = lsg.AdapterPool(nseg, L, h, h, r, dtype)
+            pool.a.uniform_(-1, 1)
+            pool.b.uniform_(-1, 1)
+            xs = torch.empty(L, batch, h, dtype=dtype, device="cuda").uniform_(-1, 1)
+            ys = torch.zeros(L, batch, h, dtype=dtype, device="cuda")
+            ss = torch.tensor(bounds, dtype=torch.int32, device="cuda")
+            sl = torch.arange(nseg, dtype=torch.int32, device="cuda")
+            with torch.cuda.stream(stream):
+                for s in range(L):
+                    lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for s in range(L):
+                    lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / (10 * L)
+            b = alg_bytes(batch, nseg, h, r)
+            sys.stderr.write(json.dumps({"sweep": True, "popularity": pop, "batch": batch, "segments": nseg,
+                                         "us_per_launch": us, "alg_bytes": b, "gbs": b / us / 1e3,
+                                         "launch": lsg.query_launch(pool, nseg, batch)}) + "\n")
+            del pool, xs, ys
+
+
+if __name__ == "__main__":
+    main()

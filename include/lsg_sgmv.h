@@ -1,0 +1,169 @@
+/*
+ * lsg_sgmv.h -- C-ABI of the B200-native SGMV library (libsgmv_b200.so).
+ *
+ * This is the thin C layer the north star asks for underneath the reference's
+ * C++ operator API.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   lsg_sgmv           <- lorasim::lora_addon(const Batch&)        core/include/lorasim/sgmv.hpp:72-73,
+ *                         core/src/sgmv.cpp:138-141 (fused, accumulates into y)
+ *   lsg_sgmv_shrink    <- lorasim::sgmv_shrink(const Batch&)       sgmv.hpp:64-66, sgmv.cpp:105-119
+ *   lsg_sgmv_expand    <- lorasim::sgmv_expand(v, segs, models)    sgmv.hpp:68-70, sgmv.cpp:121-136
+ *   lsg_bgmv           <- lorasim::gather_bmm_oracle(const Batch&) sgmv.hpp:81-83, sgmv.cpp:186-217
+ *                         (the per-row gather formulation, one adapter slot per row)
+ *   lsg_build_segments <- lorasim::plan_batch grouping             core/src/simulator.cpp:267-309,
+ *                         and the per-row gather loop              sgmv.cpp:195-203
+ *
+ * Mapping from the reference's value types:
+ *   Segments::boundaries() (sgmv.hpp:28, size_t)  -> seg_starts[n+1] int32, device memory
+ *   models[s] (LoraModel, sgmv.hpp:38-48)          -> seg_slot[s]: pool slot index, device memory
+ *   LoraModel::a  [h_in, rank] row-major            -> a_ptr[slot] + layer * a_layer_stride
+ *   LoraModel::b  [rank, h_out] row-major           -> b_ptr[slot] + layer * b_layer_stride
+ *   Matrix x / y (matrix.hpp:12-41, fp64)           -> fp16 / bf16 row-major with row stride ldx / ldy
+ *
+ * Semantics
+ *   * y += x . A_slot(s) . B_slot(s) for every row of segment s (fp32 accumulate,
+ *     the shrink result v kept in fp32, one rounding to the storage type per y
+ *     element).  lsg_sgmv_shrink overwrites v (fp32); lsg_sgmv_expand accumulates
+ *     into y.  The C++ drop-in (lorasim::lora_addon) zero-fills y first, which
+ *     gives the reference's overwrite semantics.
+ *   * A slot < 0 (or >= num_slots) means "no adapter": the rows are left untouched.
+ *   * Every call is asynchronous on `stream`, allocates nothing, never
+ *     synchronises the host, and is deterministic: each output element is
+ *     produced by a fixed-order fp32 reduction that does not depend on the batch
+ *     composition, the segment order, or the launch configuration (so a row's
+ *     result is bitwise identical whether it is computed by lsg_sgmv, by
+ *     lsg_sgmv_shrink + lsg_sgmv_expand, or by lsg_bgmv, and on any GPU of a
+ *     request-partitioned job).
+ *   * Programmatic dependent launch (opt-in, lsg_set_option(LSG_OPT_PDL, 1)):
+ *     a launch may then start while the preceding kernel on the stream is still
+ *     running; it reads the segment metadata, the weight table and streams the
+ *     adapter weights immediately, and waits for the preceding kernel only
+ *     before touching x, v or y.  With PDL on, metadata, table and weights must
+ *     not be written by the immediately preceding KERNEL on the same stream
+ *     (copies and earlier kernels are fine) -- the serving pattern, where one
+ *     segment plan is reused by the 7*L launches of a decode step.
+ *
+ * Errors: host-side validation returns a negative lsg_status and never throws;
+ * lsg_last_error() returns a thread-local message for the last failure.
+ *
+ * Device-side invariants the caller guarantees (the pool allocators in this
+ * repo do): a_ptr[s] / b_ptr[s] are 16-byte aligned device pointers, seg_starts
+ * is non-decreasing with seg_starts[0] = 0 and seg_starts[n] = total_rows.
+ */
+#ifndef LSG_SGMV_H_
+#define LSG_SGMV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* lsg_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum { LSG_F16 = 0, LSG_BF16 = 1 } lsg_dtype;
+
+typedef enum {
+  LSG_OK = 0,
+  LSG_EINVAL = -1,       /* bad argument (shape, pointer, layer, segment count) */
+  LSG_EUNSUPPORTED = -2, /* well-formed but not supported (e.g. rank > 256) */
+  LSG_ECUDA = -3,        /* a CUDA runtime call failed; see lsg_last_error() */
+  LSG_ENODEVICE = -4     /* no usable sm_100 device */
+} lsg_status;
+
+/* Adapter pool for one projection site (e.g. q_proj), all layers.
+ * Plain host struct; the two pointer arrays live in DEVICE memory. */
+typedef struct lsg_weight_table {
+  const void* const* a_ptr;   /* device [num_slots]: slot base of A, layout [layers][h_in][rank] */
+  const void* const* b_ptr;   /* device [num_slots]: slot base of B, layout [layers][rank][h_out] */
+  int64_t a_layer_stride;     /* elements between layers of A (>= h_in * rank) */
+  int64_t b_layer_stride;     /* elements between layers of B (>= rank * h_out) */
+  int32_t num_slots;
+  int32_t num_layers;
+  int32_t h_in;
+  int32_t h_out;
+  int32_t rank;
+  int32_t dtype;              /* lsg_dtype: storage type of A, B, x and y */
+} lsg_weight_table;
+
+/* Fused shrink+expand: y[s_n, h_out] += x[s_n, h_in] . A . B per segment. */
+int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+             const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+             int32_t total_rows, int32_t layer, lsg_stream_t stream);
+
+/* Shrink only: v[s_n, rank] (fp32, row stride rank) = x . A per segment (overwrite). */
+int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                    const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                    int32_t total_rows, int32_t layer, lsg_stream_t stream);
+
+/* Expand only: y[s_n, h_out] += v[s_n, rank] (fp32) . B per segment. */
+int lsg_sgmv_expand(void* y, int64_t ldy, const float* v, const lsg_weight_table* tbl,
+                    const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                    int32_t total_rows, int32_t layer, lsg_stream_t stream);
+
+/* Decode-specialised BGMV: one adapter slot per row (row_slot[s_n], device;
+ * negative = no adapter).  y += x . A_row_slot . B_row_slot. */
+int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+             const int32_t* row_slot, int32_t total_rows, int32_t layer, lsg_stream_t stream);
+
+/* On-device segment builder (replaces the CPU grouping of plan_batch,
+ * simulator.cpp:267-309, and the per-row gather loop, sgmv.cpp:195-203).
+ * Input (device): row_slot[s_n], the pool slot of every token row (negative or
+ * >= num_slots = no adapter).  Output (device): a STABLE grouping of the rows --
+ * rows of one slot keep their original order; groups in ascending slot order,
+ * except that lead_slot (>= 0; the slot of the step's prefill request, or -1)
+ * is placed first, and the no-adapter rows form a final group with slot -1.
+ * This is plan_batch's order whenever slots are assigned in ascending LoraId.
+ *   row_perm[s_n]          gathered row -> original row
+ *   seg_starts[s_n + 1]    n+1 boundaries, then padded with s_n
+ *   seg_slot[s_n]          n slots, then padded with -1
+ *   num_segments[1]        n
+ * Because of the padding, lsg_sgmv may be launched with ANY host-side
+ * num_segments in [n, s_n] (e.g. the host's count of distinct adapters) without
+ * reading n back.  One CTA; total_rows <= 16384. */
+size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots);
+int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_slots,
+                       int32_t lead_slot, int32_t* row_perm, int32_t* seg_starts,
+                       int32_t* seg_slot, int32_t* num_segments, void* workspace,
+                       size_t workspace_bytes, lsg_stream_t stream);
+
+/* Row gather / scatter helpers for the builder's permutation (16-bit rows). */
+int lsg_gather_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
+                    const int32_t* row_perm, int32_t rows, int32_t cols, lsg_stream_t stream);
+int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
+                     const int32_t* row_perm, int32_t rows, int32_t cols, lsg_stream_t stream);
+
+/* Tuning / test hooks. */
+typedef enum {
+  LSG_OPT_PDL = 0,            /* 0 (default) / 1: programmatic dependent launch */
+  LSG_OPT_FORCE_CLUSTER = 1,  /* 0 (default): auto; else split-K cluster size 1..16 */
+  LSG_OPT_FORCE_GENERIC = 2,  /* 1: use the generic (any-shape) kernels */
+  LSG_OPT_FORCE_TILE_ROWS = 3 /* 0 (default): auto; else rows per tile (1 or 8) */
+} lsg_option;
+int lsg_set_option(int32_t option, int32_t value);
+int lsg_get_option(int32_t option);
+
+/* Launch configuration the next call with these scalars would use (for
+ * tests and the benchmark's roofline bookkeeping).  path: 0 fast, 1 generic. */
+typedef struct lsg_launch_info {
+  int32_t path;
+  int32_t cluster;
+  int32_t tile_rows;
+  int32_t row_splits;
+  int32_t grid_ctas;
+  int32_t smem_bytes;
+} lsg_launch_info;
+int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t total_rows,
+                     int32_t kernel /* 0 fused, 1 shrink, 2 expand, 3 bgmv */,
+                     lsg_launch_info* info);
+
+const char* lsg_status_string(int status);
+const char* lsg_last_error(void);
+int lsg_version(void); /* major*10000 + minor*100 + patch */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSG_SGMV_H_ */

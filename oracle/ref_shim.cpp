@@ -1,0 +1,289 @@
+// ref_shim.cpp -- extern "C" shim over the UNMODIFIED reference sources.
+// TEST INFRASTRUCTURE ONLY.
+//
+// oracle/Makefile compiles this file together with the reference's own
+// /root/reference/proj/core/src/*.cpp (read in place, never copied) into
+// oracle/_ref/libref.so.  The shim only marshals plain arrays into
+// lorasim::Matrix / Segments / LoraModel / Batch and calls the reference's
+// functions; it contains no SGMV arithmetic of its own.  It is used to
+//   * generate the golden fixtures in tests/golden/ (make_golden.py),
+//   * pin the C restatement in oracle/sgmv_oracle.c live (tests/test_oracle.py),
+//   * serve as bench.py's CPU baseline ("kind": "reference").
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lorasim/cost_model.hpp"
+#include "lorasim/experiments.hpp"
+#include "lorasim/sgmv.hpp"
+#include "lorasim/simulator.hpp"
+#include "lorasim/workload.hpp"
+
+using namespace lorasim;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+Matrix to_matrix(const double* p, std::size_t r, std::size_t c) {
+  Matrix m(r, c);
+  if (r * c) std::memcpy(m.data().data(), p, sizeof(double) * r * c);
+  return m;
+}
+
+void from_matrix(const Matrix& m, double* out) {
+  if (!m.data().empty()) std::memcpy(out, m.data().data(), sizeof(double) * m.data().size());
+}
+
+Batch make_batch(const double* x, std::size_t h_in, const std::size_t* bounds, std::size_t nseg,
+                 const double* A, const double* B, std::size_t rank, std::size_t h_out) {
+  std::vector<std::size_t> b(bounds, bounds + nseg + 1);
+  Segments segs(b);
+  std::vector<LoraModel> models;
+  for (std::size_t s = 0; s < nseg; ++s)
+    models.emplace_back(static_cast<LoraId>(s), to_matrix(A + s * h_in * rank, h_in, rank),
+                        to_matrix(B + s * rank * h_out, rank, h_out));
+  const std::size_t rows = segs.total_rows();  // read before segs is moved from
+  Matrix xm = to_matrix(x, rows, h_in);
+  return Batch(std::move(xm), std::move(segs), std::move(models));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return -1;
+  }
+}
+
+Popularity pop_of(int p) {
+  switch (p) {
+    case 0: return Popularity::Distinct;
+    case 1: return Popularity::Uniform;
+    case 2: return Popularity::Skewed;
+    default: return Popularity::Identical;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_last_error.c_str(); }
+
+// ---- workload ---------------------------------------------------------------
+void* ref_rng_new(uint64_t seed) { return new Rng(seed); }
+void ref_rng_free(void* g) { delete static_cast<Rng*>(g); }
+uint64_t ref_rng_next(void* g) { return static_cast<Rng*>(g)->next(); }
+double ref_rng_uniform01(void* g) { return static_cast<Rng*>(g)->uniform01(); }
+uint64_t ref_rng_uniform_index(void* g, uint64_t n) { return static_cast<Rng*>(g)->uniform_index(n); }
+int ref_rng_uniform_int(void* g, int lo, int hi) { return static_cast<Rng*>(g)->uniform_int(lo, hi); }
+size_t ref_rng_discrete(void* g, const double* cumulative, size_t n, double total) {
+  std::vector<double> c(cumulative, cumulative + n);
+  return static_cast<Rng*>(g)->discrete(c, total);
+}
+void ref_rng_shuffle_i64(void* g, int64_t* v, size_t n) {
+  std::vector<int64_t> w(v, v + n);
+  static_cast<Rng*>(g)->shuffle(w);
+  std::memcpy(v, w.data(), sizeof(int64_t) * n);
+}
+uint64_t ref_derive_seed(uint64_t seed, uint64_t stream) { return derive_seed(seed, stream); }
+int ref_model_count_for(int n, int pop) { return model_count_for(n, pop_of(pop)); }
+int ref_assign_models(int n, int pop, double alpha, uint64_t seed, int64_t* out) {
+  return guarded([&] {
+    const auto v = assign_models(n, pop_of(pop), alpha, seed);
+    if (!v.empty()) std::memcpy(out, v.data(), sizeof(int64_t) * v.size());
+  });
+}
+
+// ---- SGMV operators (sgmv.hpp:66-83) ---------------------------------------
+int ref_sgmv_shrink(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
+                    const double* A, const double* B, size_t rank, size_t h_out, double* v) {
+  return guarded([&] { from_matrix(sgmv_shrink(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)), v); });
+}
+int ref_sgmv_expand(const double* v, size_t rows, const size_t* bounds, size_t nseg,
+                    const double* A, const double* B, size_t h_in, size_t rank, size_t h_out,
+                    double* y) {
+  return guarded([&] {
+    std::vector<double> x(rows * h_in, 0.0);
+    Batch b = make_batch(x.data(), h_in, bounds, nseg, A, B, rank, h_out);
+    from_matrix(sgmv_expand(to_matrix(v, rows, rank), b.segments, b.models), y);
+  });
+}
+int ref_lora_addon(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
+                   const double* A, const double* B, size_t rank, size_t h_out, double* y) {
+  return guarded([&] { from_matrix(lora_addon(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)), y); });
+}
+int ref_dense_projection(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
+                         const double* A, const double* B, size_t rank, size_t h_out,
+                         const double* w, double* y) {
+  return guarded([&] {
+    from_matrix(dense_projection(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out),
+                                 to_matrix(w, h_in, h_out)),
+                y);
+  });
+}
+int ref_lora_loop_oracle(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
+                         const double* A, const double* B, size_t rank, size_t h_out, double* y) {
+  return guarded([&] { from_matrix(lora_loop_oracle(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)), y); });
+}
+int ref_gather_bmm_oracle(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
+                          const double* A, const double* B, size_t rank, size_t h_out, double* y) {
+  return guarded([&] { from_matrix(gather_bmm_oracle(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)), y); });
+}
+
+// ---- verify_sgmv (experiments.cpp:35-102) ------------------------------------
+int ref_verify_sgmv(int trials, uint64_t seed, int inject, int* failures, double* worst,
+                    double* first_fail_dev, size_t* first_fail_shape /* h_in,h_out,rank,rows,models */) {
+  return guarded([&] {
+    const VerifyReport r = verify_sgmv(trials, seed, inject != 0);
+    *failures = r.failures;
+    *worst = r.worst_deviation;
+    *first_fail_dev = r.failed_cases.empty() ? 0.0 : r.failed_cases[0].deviation;
+    if (!r.failed_cases.empty()) {
+      const auto& c = r.failed_cases[0];
+      first_fail_shape[0] = c.h_in;
+      first_fail_shape[1] = c.h_out;
+      first_fail_shape[2] = c.rank;
+      first_fail_shape[3] = c.rows;
+      first_fail_shape[4] = c.models;
+    }
+  });
+}
+
+// The same draw sequence as experiments.cpp:43-76, written with the reference's
+// own Rng / assign_models / LoraModel / Batch and the same emplace_back call
+// shape, so this compiler's argument evaluation order is what gets recorded.
+int ref_verify_next_trial(void* gp, int trial, size_t* h_in_out, size_t* h_out_out,
+                          size_t* rank_out, size_t* rows_out, size_t* nseg_out, size_t* bounds_out,
+                          int64_t* seg_ids, double* x_out, double* A_out, double* B_out) {
+  return guarded([&] {
+    Rng& rng = *static_cast<Rng*>(gp);
+    auto random_matrix = [](Rng& g, std::size_t rows, std::size_t cols) {
+      Matrix m(rows, cols);
+      for (double& v : m.data()) v = g.uniform01() * 2.0 - 1.0;
+      return m;
+    };
+    static const std::size_t dims[] = {8, 64, 128};
+    static const std::size_t ranks[] = {8, 16, 32, 64};
+    const Popularity pop = pop_of(trial % 4);
+    const std::size_t h_in = dims[rng.uniform_index(3)];
+    const std::size_t h_out = dims[rng.uniform_index(3)];
+    std::vector<std::size_t> fitting;
+    for (std::size_t r : ranks)
+      if (r <= std::min(h_in, h_out)) fitting.push_back(r);
+    const std::size_t rank = fitting[rng.uniform_index(fitting.size())];
+    const std::size_t max_rows = pop == Popularity::Distinct ? 8 : 64;
+    const int rows = rng.uniform_int(1, static_cast<int>(max_rows));
+    const auto assignment = assign_models(rows, pop, 1.5, rng.next());
+    std::map<LoraId, std::vector<int>> groups;
+    for (int i = 0; i < rows; ++i) groups[assignment[static_cast<std::size_t>(i)]].push_back(i);
+    std::vector<std::size_t> boundaries{0};
+    std::vector<LoraModel> models;
+    Matrix x(static_cast<std::size_t>(rows), h_in);
+    std::size_t row_cursor = 0;
+    for (const auto& [lora, members] : groups) {
+      models.emplace_back(lora, random_matrix(rng, h_in, rank), random_matrix(rng, rank, h_out));
+      for (std::size_t i = 0; i < members.size(); ++i) {
+        for (std::size_t c = 0; c < h_in; ++c) x(row_cursor, c) = rng.uniform01() * 2.0 - 1.0;
+        ++row_cursor;
+      }
+      boundaries.push_back(row_cursor);
+    }
+    *h_in_out = h_in;
+    *h_out_out = h_out;
+    *rank_out = rank;
+    *rows_out = static_cast<std::size_t>(rows);
+    *nseg_out = models.size();
+    for (std::size_t i = 0; i < boundaries.size(); ++i) bounds_out[i] = boundaries[i];
+    for (std::size_t s = 0; s < models.size(); ++s) {
+      seg_ids[s] = models[s].id;
+      from_matrix(models[s].a, A_out + s * h_in * rank);
+      from_matrix(models[s].b, B_out + s * rank * h_out);
+    }
+    from_matrix(x, x_out);
+  });
+}
+
+// ---- cost model (cost_model.cpp:8-40) ----------------------------------------
+double ref_sgmv_flop(int64_t n, int64_t rows, int64_t h_in, int64_t h_out) {
+  return sgmv_flop(SgmvShape{n, rows, h_in, h_out});
+}
+double ref_sgmv_io_bytes(int64_t n, int64_t rows, int64_t h_in, int64_t h_out, int e) {
+  return sgmv_io_bytes(SgmvShape{n, rows, h_in, h_out}, e);
+}
+double ref_arithmetic_intensity(int64_t n, int64_t rows, int64_t h_in, int64_t h_out, int e) {
+  try {
+    return arithmetic_intensity(SgmvShape{n, rows, h_in, h_out}, e);
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return -1.0;
+  }
+}
+double ref_sgmv_latency(int64_t n, int64_t rows, int64_t h_in, int64_t h_out, double peak,
+                        double bw, double floor_s, int e) {
+  CostParams p;
+  p.peak_flops = peak;
+  p.mem_bw = bw;
+  p.kernel_overhead = floor_s;
+  p.elem_bytes = e;
+  return sgmv_latency(SgmvShape{n, rows, h_in, h_out}, p);
+}
+double ref_gather_bmm_extra_elements(int64_t n, int64_t rows, int64_t h_in, int64_t h_out) {
+  return gather_bmm_extra_elements(SgmvShape{n, rows, h_in, h_out});
+}
+
+// roofline_sweep + roofline_csv with default CostParams (experiments.cpp:141-174)
+size_t ref_roofline_csv(int max_batch, char* out, size_t cap) {
+  const std::string s = roofline_csv(roofline_sweep(CostParams{}, max_batch));
+  if (out && cap) {
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(out, s.data(), n);
+    out[n] = '\0';
+  }
+  return s.size();
+}
+
+// ---- plan_batch (simulator.cpp:239-311), MultiLora mode -----------------------
+// Requests are placed in one GpuState in id order with every adapter loaded.
+int ref_plan_batch(size_t nreq, const int64_t* req_lora, const uint8_t* prefill_done,
+                   const int32_t* prompt, int64_t* prefill, int64_t* decodes, size_t* n_decodes,
+                   size_t* bounds, int64_t* seg_loras, size_t* nseg) {
+  return guarded([&] {
+    ExperimentConfig cfg;
+    KvPageConfig kcfg = cfg.kv_page_config();
+    ClusterState c;
+    c.gpus.emplace_back(0, kcfg);
+    GpuState& g = c.gpus[0];
+    for (size_t i = 0; i < nreq; ++i) {
+      Request r;
+      r.id = static_cast<RequestId>(i);
+      r.lora_id = req_lora[i];
+      r.prompt_len = prompt[i];
+      r.restart_prompt_len = prompt[i];
+      r.target_output_len = 4;
+      r.state = RequestState::Running;
+      r.gpu = 0;
+      r.prefill_done = prefill_done[i] != 0;
+      if (r.prefill_done) r.generated = 1;
+      c.requests.push_back(r);
+      g.working_set.push_back(r.id);
+      g.adapter_ready_time[r.lora_id] = 0.0;
+    }
+    const BatchPlan plan = plan_batch(c, 0, 1.0, BatchMode::MultiLora);
+    *prefill = plan.prefill ? static_cast<int64_t>(*plan.prefill) : -1;
+    *n_decodes = plan.decodes.size();
+    for (size_t i = 0; i < plan.decodes.size(); ++i) decodes[i] = plan.decodes[i];
+    *nseg = plan.segment_loras.size();
+    for (size_t i = 0; i < plan.segment_boundaries.size(); ++i) bounds[i] = plan.segment_boundaries[i];
+    for (size_t i = 0; i < plan.segment_loras.size(); ++i) seg_loras[i] = plan.segment_loras[i];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// launch.cuh -- cudaLaunchKernelEx plumbing (cluster dims, programmatic
+// dependent launch) and the per-mode template dispatch.  The instantiations are
+// spread over inst_*.cu so the sm_100a compile parallelises.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/lsg_sgmv.h"
+#include "sgmv_kernels.cuh"
+
+namespace lsg {
+
+constexpr int kSmemBudget = 225 * 1024;
+constexpr int kMaxCluster = 16;
+
+struct Plan {
+  int path = 0;  // 0 fast, 1 generic
+  int mt = 1;
+  int cluster = 1;
+  int row_splits = 1;
+  int clusters = 0;
+  int nqc_max = 0;
+  int ncv_max = 0;
+  int smem = 0;
+  int mode = kFused;
+};
+
+// Set by the API layer; read at launch.
+bool pdl_enabled();
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+// Per-mode entry points, defined in inst_fused.cu / inst_shrink.cu / inst_expand.cu.
+int launch_fast_fused(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
+int launch_fast_shrink(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
+int launch_fast_expand(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
+int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st);
+
+template <typename K>
+cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cudaStream_t st,
+                      const void* params_ptr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (cluster > 0) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  void* args[] = {const_cast<void*>(params_ptr)};
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kernel), args);
+}
+
+template <typename T, int R, int MT, int MODE>
+int launch_fast_inst(const FastParams& p, const Plan& pl, cudaStream_t st) {
+  auto kern = sgmv_fast_kernel<T, R, MT, MODE>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(max dynamic smem)");
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(non-portable cluster)");
+    configured = true;
+  }
+  const dim3 grid(static_cast<unsigned>(pl.cluster), static_cast<unsigned>(pl.clusters), 1);
+  cudaError_t e = launch_ex(kern, grid, dim3(kThreads), pl.smem, pl.cluster, st, &p);
+  if (e != cudaSuccess) return cuda_fail(e, "sgmv_fast_kernel launch");
+  return LSG_OK;
+}
+
+template <typename T, int MODE>
+int dispatch_rank_mt(const FastParams& p, const Plan& pl, int rank, cudaStream_t st) {
+#define LSG_CASE(R)                                                            \
+  case R:                                                                      \
+    return pl.mt == 1 ? launch_fast_inst<T, R, 1, MODE>(p, pl, st)             \
+                      : launch_fast_inst<T, R, 8, MODE>(p, pl, st);
+  switch (rank) {
+    LSG_CASE(8)
+    LSG_CASE(16)
+    LSG_CASE(32)
+    LSG_CASE(64)
+  }
+#undef LSG_CASE
+  return fail(LSG_EUNSUPPORTED, "lsg: rank not supported by the fast path");
+}
+
+template <typename T, int MODE>
+int launch_generic_inst(const GenericParams& g, int rows, int smem, cudaStream_t st) {
+  auto kern = sgmv_generic_kernel<T, MODE>;
+  cudaError_t e = launch_ex(kern, dim3(static_cast<unsigned>(rows)), dim3(kThreads), smem, 0, st, &g);
+  if (e != cudaSuccess) return cuda_fail(e, "sgmv_generic_kernel launch");
+  return LSG_OK;
+}
+
+template <typename T>
+int dispatch_generic(const GenericParams& g, int mode, int rows, int smem, cudaStream_t st) {
+  switch (mode) {
+    case kFused: return launch_generic_inst<T, kFused>(g, rows, smem, st);
+    case kShrink: return launch_generic_inst<T, kShrink>(g, rows, smem, st);
+    default: return launch_generic_inst<T, kExpand>(g, rows, smem, st);
+  }
+}
+
+
+}  // namespace lsg
+
+#define LSG_DEFINE_FAST_ENTRY(NAME, MODE)                                                     \
+  namespace lsg {                                                                             \
+  int NAME(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st) {       \
+    return dtype == LSG_F16 ? dispatch_rank_mt<__half, MODE>(p, pl, rank, st)                \
+                            : dispatch_rank_mt<__nv_bfloat16, MODE>(p, pl, rank, st);         \
+  }                                                                                           \
+  }

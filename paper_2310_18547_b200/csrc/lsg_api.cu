@@ -1,0 +1,380 @@
+// lsg_api.cu -- the extern "C" boundary (include/lsg_sgmv.h): host-side
+// validation, launch planning and dispatch onto the sm_100a kernels.
+//
+// Planning is pure host integer arithmetic on the scalars of the call
+// (num_segments, total_rows, shapes) -- no device metadata is read back and the
+// host never synchronises.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lsg_sgmv.h"
+#include "segment_builder.cuh"
+#include "launch.cuh"
+
+namespace lsg {
+
+thread_local std::string g_err;
+
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return LSG_ECUDA;
+}
+
+namespace {
+
+std::atomic<int> g_opt_pdl{0};
+std::atomic<int> g_opt_force_cluster{0};
+std::atomic<int> g_opt_force_generic{0};
+std::atomic<int> g_opt_force_tile_rows{0};
+
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+enum Kernel { kKFused = 0, kKShrink = 1, kKExpand = 2, kKBgmv = 3 };
+
+
+int validate_table(const lsg_weight_table* t) {
+  if (t == nullptr) return fail(LSG_EINVAL, "lsg: weight table is NULL");
+  if (t->a_ptr == nullptr || t->b_ptr == nullptr) return fail(LSG_EINVAL, "lsg: weight table pointer arrays are NULL");
+  if (t->num_slots < 0 || t->num_layers < 1) return fail(LSG_EINVAL, "lsg: weight table slot/layer counts invalid");
+  if (t->h_in < 1 || t->h_out < 1) return fail(LSG_EINVAL, "lsg: weight table dims must be >= 1");
+  // Same invariant as LoraModel (sgmv.cpp:45-56): 1 <= rank <= min(h_in, h_out).
+  if (t->rank < 1 || t->rank > t->h_in || t->rank > t->h_out)
+    return fail(LSG_EINVAL, "lsg: rank must satisfy 1 <= rank <= min(h_in, h_out)");
+  if (t->rank > 1024) return fail(LSG_EUNSUPPORTED, "lsg: rank > 1024 is not supported");
+  if (t->a_layer_stride < static_cast<int64_t>(t->h_in) * t->rank ||
+      t->b_layer_stride < static_cast<int64_t>(t->rank) * t->h_out)
+    return fail(LSG_EINVAL, "lsg: layer strides smaller than one layer");
+  if (t->dtype != LSG_F16 && t->dtype != LSG_BF16) return fail(LSG_EINVAL, "lsg: unknown dtype");
+  return LSG_OK;
+}
+
+bool fast_shape_ok(const lsg_weight_table* t) {
+  const int r = t->rank;
+  return (r == 8 || r == 16 || r == 32 || r == 64) && t->h_in % KW == 0 && t->h_out % 8 == 0 &&
+         t->a_layer_stride % 8 == 0 && t->b_layer_stride % 8 == 0;
+}
+
+// Choose tile rows, row splits and the split-K cluster size for a launch.
+Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast) {
+  Plan pl;
+  pl.mode = kernel == kKShrink ? kShrink : kernel == kKExpand ? kExpand : kFused;
+  if (!fast || g_opt_force_generic.load()) {
+    pl.path = 1;
+    pl.clusters = s_n;
+    pl.smem = t->rank * 4;
+    return pl;
+  }
+  const int forced_mt = g_opt_force_tile_rows.load();
+  if (kernel == kKBgmv)
+    pl.mt = 1;
+  else if (forced_mt == 1 || forced_mt == 8)
+    pl.mt = forced_mt;
+  else
+    pl.mt = s_n <= n_seg ? 1 : 8;
+  if (kernel == kKBgmv) {
+    pl.row_splits = 1;
+    pl.clusters = s_n;
+  } else {
+    const int tiles_per_seg = (s_n + pl.mt * n_seg - 1) / (pl.mt * n_seg);
+    pl.row_splits = std::max(1, tiles_per_seg);
+    pl.clusters = n_seg * pl.row_splits;
+  }
+  const int nq = t->h_in / KW, ncvt = t->h_out / 8;
+  auto smem_for = [&](int c) {
+    const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
+    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nqc, ncv).total);
+  };
+  int c_fit = 1;
+  while (c_fit < kMaxCluster && smem_for(c_fit) > kSmemBudget) ++c_fit;
+  const int sms = num_sms();
+  int c_fill = std::max(1, std::min(kMaxCluster, sms / std::max(1, pl.clusters)));
+  int c = std::max(c_fit, c_fill);
+  const int span = pl.mode == kExpand ? ncvt : std::min(nq, pl.mode == kShrink ? nq : ncvt);
+  c = std::max(c_fit, std::min(c, std::max(1, span)));
+  const int forced = g_opt_force_cluster.load();
+  if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
+  pl.cluster = c;
+  pl.nqc_max = (nq + c - 1) / c;
+  pl.ncv_max = (ncvt + c - 1) / c;
+  pl.smem = smem_for(c);
+  return pl;
+}
+
+// Shared entry for all four SGMV kernels.
+int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_out, const float* v_in,
+        const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
+        const int32_t* row_slot, int32_t n_seg, int32_t s_n, int32_t layer, lsg_stream_t stream) {
+  int st = validate_table(tbl);
+  if (st != LSG_OK) return st;
+  if (s_n < 0) return fail(LSG_EINVAL, "lsg: total_rows must be >= 0");
+  if (kernel != kKBgmv && n_seg < 0) return fail(LSG_EINVAL, "lsg: num_segments must be >= 0");
+  if (layer < 0 || layer >= tbl->num_layers) return fail(LSG_EINVAL, "lsg: layer index out of range");
+  if (s_n == 0 || (kernel != kKBgmv && n_seg == 0)) return LSG_OK;  // empty batch: nothing to do
+  if (kernel == kKBgmv ? row_slot == nullptr : (seg_starts == nullptr || seg_slot == nullptr))
+    return fail(LSG_EINVAL, "lsg: segment metadata pointers are NULL");
+  const bool need_x = kernel != kKExpand, need_y = kernel != kKShrink;
+  if (need_x && (x == nullptr || ldx < tbl->h_in)) return fail(LSG_EINVAL, "lsg: x is NULL or ldx < h_in");
+  if (need_y && (y == nullptr || ldy < tbl->h_out)) return fail(LSG_EINVAL, "lsg: y is NULL or ldy < h_out");
+  if (kernel == kKShrink && v_out == nullptr) return fail(LSG_EINVAL, "lsg: v is NULL");
+  if (kernel == kKExpand && v_in == nullptr) return fail(LSG_EINVAL, "lsg: v is NULL");
+
+  bool fast = fast_shape_ok(tbl);
+  if (need_x) fast = fast && aligned16(x) && ldx % 8 == 0;
+  if (need_y) fast = fast && aligned16(y) && ldy % 8 == 0;
+  const Plan pl = make_plan(tbl, kernel, n_seg, s_n, fast);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+
+  if (pl.path == 1) {
+    GenericParams g{};
+    g.y = y;
+    g.x = x;
+    g.v_out = v_out;
+    g.v_in = v_in;
+    g.a_ptr = tbl->a_ptr;
+    g.b_ptr = tbl->b_ptr;
+    g.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+    g.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+    g.ldx = ldx;
+    g.ldy = ldy;
+    g.seg_starts = seg_starts;
+    g.seg_slot = seg_slot;
+    g.row_slot = kernel == kKBgmv ? row_slot : nullptr;
+    g.n_seg = n_seg;
+    g.s_n = s_n;
+    g.num_slots = tbl->num_slots;
+    g.h_in = tbl->h_in;
+    g.h_out = tbl->h_out;
+    g.rank = tbl->rank;
+    return launch_generic(tbl->dtype, pl.mode, g, s_n, pl.smem, cs);
+  }
+
+  FastParams p{};
+  p.y = y;
+  p.x = x;
+  p.v_out = v_out;
+  p.v_in = v_in;
+  p.a_ptr = tbl->a_ptr;
+  p.b_ptr = tbl->b_ptr;
+  p.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+  p.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.seg_starts = seg_starts;
+  p.seg_slot = seg_slot;
+  p.row_slot = kernel == kKBgmv ? row_slot : nullptr;
+  p.n_seg = n_seg;
+  p.s_n = s_n;
+  p.row_splits = pl.row_splits;
+  p.num_slots = tbl->num_slots;
+  p.h_in = tbl->h_in;
+  p.h_out = tbl->h_out;
+  p.nq = tbl->h_in / KW;
+  p.ncvt = tbl->h_out / 8;
+  p.nqc_max = pl.nqc_max;
+  p.ncv_max = pl.ncv_max;
+  switch (pl.mode) {
+    case kFused: return launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs);
+    case kShrink: return launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs);
+    default: return launch_fast_expand(tbl->dtype, tbl->rank, p, pl, cs);
+  }
+}
+
+}  // namespace
+
+bool pdl_enabled() { return g_opt_pdl.load() != 0; }
+
+int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st) {
+  return dtype == LSG_F16 ? dispatch_generic<__half>(g, mode, rows, smem, st)
+                          : dispatch_generic<__nv_bfloat16>(g, mode, rows, smem, st);
+}
+
+}  // namespace lsg
+
+using namespace lsg;
+
+extern "C" {
+
+int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+             const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+             int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
+             num_segments, total_rows, layer, stream);
+}
+
+int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                    const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                    int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  return run(kKShrink, nullptr, 0, x, ldx, v, nullptr, tbl, seg_starts, seg_slot, nullptr,
+             num_segments, total_rows, layer, stream);
+}
+
+int lsg_sgmv_expand(void* y, int64_t ldy, const float* v, const lsg_weight_table* tbl,
+                    const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                    int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  return run(kKExpand, y, ldy, nullptr, 0, nullptr, v, tbl, seg_starts, seg_slot, nullptr,
+             num_segments, total_rows, layer, stream);
+}
+
+int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+             const int32_t* row_slot, int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  return run(kKBgmv, y, ldy, x, ldx, nullptr, nullptr, tbl, nullptr, nullptr, row_slot, 0,
+             total_rows, layer, stream);
+}
+
+int lsg_set_option(int32_t option, int32_t value) {
+  switch (option) {
+    case LSG_OPT_PDL: g_opt_pdl = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_FORCE_CLUSTER:
+      if (value < 0 || value > kMaxCluster) return fail(LSG_EINVAL, "lsg: cluster size must be 0..16");
+      g_opt_force_cluster = value;
+      return LSG_OK;
+    case LSG_OPT_FORCE_GENERIC: g_opt_force_generic = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_FORCE_TILE_ROWS:
+      if (value != 0 && value != 1 && value != 8) return fail(LSG_EINVAL, "lsg: tile rows must be 0, 1 or 8");
+      g_opt_force_tile_rows = value;
+      return LSG_OK;
+  }
+  return fail(LSG_EINVAL, "lsg: unknown option");
+}
+
+int lsg_get_option(int32_t option) {
+  switch (option) {
+    case LSG_OPT_PDL: return g_opt_pdl.load();
+    case LSG_OPT_FORCE_CLUSTER: return g_opt_force_cluster.load();
+    case LSG_OPT_FORCE_GENERIC: return g_opt_force_generic.load();
+    case LSG_OPT_FORCE_TILE_ROWS: return g_opt_force_tile_rows.load();
+  }
+  return fail(LSG_EINVAL, "lsg: unknown option");
+}
+
+int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t total_rows,
+                     int32_t kernel, lsg_launch_info* info) {
+  int st = validate_table(tbl);
+  if (st != LSG_OK) return st;
+  if (info == nullptr || kernel < 0 || kernel > 3) return fail(LSG_EINVAL, "lsg_query_launch: bad arguments");
+  if (total_rows <= 0 || (kernel != kKBgmv && num_segments <= 0)) {
+    *info = lsg_launch_info{};
+    return LSG_OK;
+  }
+  const Plan pl = make_plan(tbl, kernel, num_segments, total_rows, fast_shape_ok(tbl));
+  info->path = pl.path;
+  info->cluster = pl.path ? 1 : pl.cluster;
+  info->tile_rows = pl.path ? 1 : pl.mt;
+  info->row_splits = pl.row_splits;
+  info->grid_ctas = pl.path ? total_rows : pl.cluster * pl.clusters;
+  info->smem_bytes = pl.smem;
+  return LSG_OK;
+}
+
+size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots) {
+  (void)total_rows;
+  (void)num_slots;
+  return 0;  // the single-CTA builder keeps everything in shared memory
+}
+
+int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_slots,
+                       int32_t lead_slot, int32_t* row_perm, int32_t* seg_starts,
+                       int32_t* seg_slot, int32_t* num_segments, void* workspace,
+                       size_t workspace_bytes, lsg_stream_t stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (total_rows < 0 || num_slots < 0) return fail(LSG_EINVAL, "lsg_build_segments: negative sizes");
+  if (total_rows > kBuilderMaxRows) return fail(LSG_EUNSUPPORTED, "lsg_build_segments: total_rows > 16384");
+  if (seg_starts == nullptr || num_segments == nullptr || (total_rows > 0 && (row_slot == nullptr ||
+      row_perm == nullptr || seg_slot == nullptr)))
+    return fail(LSG_EINVAL, "lsg_build_segments: NULL output");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (total_rows == 0) {
+    cudaError_t e = cudaMemsetAsync(seg_starts, 0, sizeof(int32_t), cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(num_segments, 0, sizeof(int32_t), cs);
+    return e == cudaSuccess ? LSG_OK : cuda_fail(e, "lsg_build_segments memset");
+  }
+  int n_pow2 = 1;
+  while (n_pow2 < total_rows) n_pow2 <<= 1;
+  const int smem = n_pow2 * static_cast<int>(sizeof(uint64_t));
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(build_segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kBuilderMaxRows * 8);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(builder smem)");
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kBuilderThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = cs;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = g_opt_pdl.load() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, build_segments_kernel, row_slot, total_rows, num_slots, lead_slot,
+                                     n_pow2, row_perm, seg_starts, seg_slot, num_segments);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "build_segments_kernel launch");
+}
+
+static int permute_rows(bool gather, void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
+                        const int32_t* perm, int32_t rows, int32_t cols, lsg_stream_t stream) {
+  if (rows < 0 || cols < 0) return fail(LSG_EINVAL, "lsg permute rows: negative sizes");
+  if (rows == 0 || cols == 0) return LSG_OK;
+  if (dst == nullptr || src == nullptr || perm == nullptr || ld_dst < cols || ld_src < cols)
+    return fail(LSG_EINVAL, "lsg permute rows: bad pointers or strides");
+  const bool vec = aligned16(dst) && aligned16(src) && cols % 8 == 0 && ld_dst % 8 == 0 && ld_src % 8 == 0;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (gather)
+    permute_rows_kernel<true><<<rows, 128, 0, cs>>>(static_cast<uint16_t*>(dst), ld_dst,
+                                                   static_cast<const uint16_t*>(src), ld_src, perm, cols, vec);
+  else
+    permute_rows_kernel<false><<<rows, 128, 0, cs>>>(static_cast<uint16_t*>(dst), ld_dst,
+                                                    static_cast<const uint16_t*>(src), ld_src, perm, cols, vec);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "permute_rows_kernel launch");
+}
+
+int lsg_gather_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, const int32_t* row_perm,
+                    int32_t rows, int32_t cols, lsg_stream_t stream) {
+  return permute_rows(true, dst, ld_dst, src, ld_src, row_perm, rows, cols, stream);
+}
+
+int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, const int32_t* row_perm,
+                     int32_t rows, int32_t cols, lsg_stream_t stream) {
+  return permute_rows(false, dst, ld_dst, src, ld_src, row_perm, rows, cols, stream);
+}
+
+const char* lsg_status_string(int status) {
+  switch (status) {
+    case LSG_OK: return "LSG_OK";
+    case LSG_EINVAL: return "LSG_EINVAL: invalid argument";
+    case LSG_EUNSUPPORTED: return "LSG_EUNSUPPORTED: unsupported configuration";
+    case LSG_ECUDA: return "LSG_ECUDA: CUDA runtime error";
+    case LSG_ENODEVICE: return "LSG_ENODEVICE: no usable sm_100 device";
+  }
+  return "LSG: unknown status";
+}
+
+const char* lsg_last_error(void) { return g_err.c_str(); }
+
+int lsg_version(void) { return 100; }
+
+}  // extern "C"

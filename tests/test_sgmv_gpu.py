@@ -1,0 +1,350 @@
+"""GPU parity tests: the sm_100a kernels (through the C-ABI) against the CPU oracle.
+
+Mirrors the reference's SGMV tests (proj/tests/unit/test_sgmv.cpp,
+test_experiments.cpp) plus the kernel-level invariants the B200 design adds
+(cluster-size / tile-size / kernel-variant independence, bitwise).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from tests._util import (DISTINCT, IDENTICAL, NORTH_STAR_TOL, SKEWED, TOL, UNIFORM, oracle, random_problem,
+                         row_norm_err, segments_for)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+DTYPES = [torch.float16, torch.bfloat16]
+
+
+@pytest.fixture(scope="module")
+def lsg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2310_18547_b200 as m
+    m.set_option(m.LSG_OPT_PDL, 0)
+    return m
+
+
+@pytest.fixture(autouse=True)
+def _reset_options(lsg):
+    yield
+    for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL):
+        lsg.set_option(opt, 0)
+
+
+class Problem:
+    """One segmented batch, quantised for the GPU, dequantised for the oracle."""
+
+    def __init__(self, lsg, x, A, B, bounds, dtype, slots=None, num_slots=None, layers=1, layer=0, y0=None):
+        self.lsg, self.dtype = lsg, dtype
+        nseg = len(bounds) - 1
+        self.rank, self.h_in, self.h_out = B.shape[1], x.shape[1], B.shape[2]
+        self.slots = list(range(nseg)) if slots is None else list(slots)
+        ns = num_slots if num_slots is not None else max(self.slots + [nseg - 1]) + 1
+        self.pool = lsg.AdapterPool(ns, layers, self.h_in, self.h_out, self.rank, dtype)
+        self.x = torch.tensor(x, dtype=torch.float64).to(dtype).cuda()
+        Aq = torch.tensor(A, dtype=torch.float64).to(dtype)
+        Bq = torch.tensor(B, dtype=torch.float64).to(dtype)
+        for s, slot in enumerate(self.slots):
+            if slot >= 0:
+                self.pool.a[slot, layer].copy_(Aq[s])
+                self.pool.b[slot, layer].copy_(Bq[s])
+        self.layer = layer
+        self.bounds = np.asarray(bounds, dtype=np.uint64)
+        self.seg_starts = torch.tensor(self.bounds.astype(np.int64), dtype=torch.int32, device="cuda")
+        self.seg_slot = torch.tensor(self.slots, dtype=torch.int32, device="cuda")
+        self.xd, self.Ad, self.Bd = self.x.double().cpu().numpy(), Aq.double().numpy(), Bq.double().numpy()
+        rows = int(self.bounds[-1]) if nseg else 0
+        self.y0 = (torch.zeros(rows, self.h_out, dtype=dtype, device="cuda") if y0 is None
+                   else torch.tensor(y0, dtype=torch.float64).to(dtype).cuda())
+
+    def run(self, kind="fused"):
+        lsg = self.lsg
+        y = self.y0.clone()
+        if kind == "fused":
+            lsg.sgmv(y, self.x, self.pool, self.seg_starts, self.seg_slot, self.layer)
+        elif kind == "two_launch":
+            v = torch.empty(self.x.shape[0], self.rank, dtype=torch.float32, device="cuda")
+            lsg.sgmv_shrink(v, self.x, self.pool, self.seg_starts, self.seg_slot, self.layer)
+            lsg.sgmv_expand(y, v, self.pool, self.seg_starts, self.seg_slot, self.layer)
+        elif kind == "bgmv":
+            row_slot = np.zeros(self.x.shape[0], dtype=np.int32)
+            for s in range(len(self.bounds) - 1):
+                row_slot[int(self.bounds[s]):int(self.bounds[s + 1])] = self.slots[s]
+            lsg.bgmv(y, self.x, self.pool, torch.tensor(row_slot, device="cuda"), self.layer)
+        torch.cuda.synchronize()
+        return y
+
+    def reference(self):
+        valid = [s >= 0 for s in self.slots]
+        y = self.y0.double().cpu().numpy().copy()
+        if len(self.bounds) > 1:
+            add = oracle().lora_addon(self.xd, self.bounds, self.Ad, self.Bd)
+            for s, ok in enumerate(valid):
+                a, b = int(self.bounds[s]), int(self.bounds[s + 1])
+                if ok:
+                    y[a:b] += add[a:b]
+        return y
+
+
+def tol(dtype):
+    return TOL[str(dtype).split(".")[-1]]
+
+
+# ---------------------------------------------------------------------------------
+# Known-answer tests (test_sgmv.cpp:83-122; values produced by the reference)
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_hand_checked_two_segment_exact(lsg, dtype):
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["two_segment"]
+    p = Problem(lsg, np.array(kat["x"]), np.array(kat["A"]), np.array(kat["B"]), kat["bounds"], dtype)
+    for kind in ("fused", "two_launch", "bgmv"):
+        y = p.run(kind).double().cpu().numpy()
+        assert np.array_equal(y, np.array(kat["lora_addon"])), kind  # [[5,1],[11,3],[16,54]]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_rank1_and_zero_weights_exact(lsg, dtype):
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["rank1"]
+    p = Problem(lsg, np.array(kat["x"]), np.array(kat["A"]), np.array(kat["B"]), kat["bounds"], dtype)
+    assert np.array_equal(p.run().double().cpu().numpy(), np.array(kat["lora_addon"]))  # [[3, 3]]
+    x, _, _ = random_problem(8, 8, 2, [0, 4], 11)
+    pz = Problem(lsg, x, np.zeros((1, 8, 2)), np.zeros((1, 2, 8)), [0, 4], dtype)
+    assert torch.count_nonzero(pz.run()).item() == 0
+
+
+def test_empty_batch_is_noop(lsg):
+    pool = lsg.AdapterPool(1, 1, 128, 128, 16, torch.float16)
+    x = torch.empty(0, 128, dtype=torch.float16, device="cuda")
+    y = torch.empty(0, 128, dtype=torch.float16, device="cuda")
+    z = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lsg.sgmv(y, x, pool, z, z[:0], 0)
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------------
+# Randomised parity: verify_sgmv's shape distribution (experiments.cpp:35-102)
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_verify_sgmv_trials_match_oracle(lsg, dtype):
+    o = oracle()
+    g = o.rng(o.derive_seed(42, 17))
+    worst = 0.0
+    for t in range(200):
+        tr = g.verify_next_trial(t)
+        p = Problem(lsg, tr["x"], tr["A"], tr["B"], tr["bounds"], dtype)
+        yref = p.reference()
+        for kind in ("fused", "two_launch", "bgmv"):
+            err = row_norm_err(p.run(kind).double().cpu().numpy(), yref)
+            worst = max(worst, err)
+            assert err <= tol(dtype), (t, kind, err)
+    assert worst <= NORTH_STAR_TOL
+
+
+SHAPES = [  # (h_in, h_out, rank) at the BASELINE configs and rank sweep
+    (4096, 4096, 16), (4096, 4096, 8), (4096, 4096, 32), (4096, 4096, 64), (5120, 5120, 64), (8192, 8192, 16)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("pop", [DISTINCT, UNIFORM, SKEWED, IDENTICAL])
+def test_baseline_shapes_match_oracle(lsg, dtype, shape, pop):
+    h_in, h_out, r = shape
+    bounds, _, _ = segments_for(pop, 64, 1234 + pop)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 77 + pop)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    y = p.run()
+    assert lsg.query_launch(p.pool, len(bounds) - 1, 64)["path"] == 0  # the fast (cluster) path
+    err = row_norm_err(y.double().cpu().numpy(), p.reference())
+    assert err <= tol(dtype), err
+
+
+@pytest.mark.parametrize("dtype", [torch.float16])
+@pytest.mark.parametrize("batch", [1, 2, 7, 32])
+def test_small_batches_and_accumulate(lsg, dtype, batch):
+    bounds, _, _ = segments_for(UNIFORM, batch, 5)
+    x, A, B = random_problem(4096, 4096, 16, bounds, batch)
+    y0 = oracle().rng(99).fill_pm1(batch * 4096).reshape(batch, 4096)
+    p = Problem(lsg, x, A, B, bounds, dtype, y0=y0)
+    err = row_norm_err(p.run().double().cpu().numpy(), p.reference())
+    assert err <= tol(dtype), err
+
+
+@pytest.mark.parametrize("prefill", [128, 512])
+def test_mixed_prefill_plus_decodes(lsg, prefill):
+    bounds = np.array([0, prefill] + [prefill + i + 1 for i in range(31)], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, prefill)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    err = row_norm_err(p.run().double().cpu().numpy(), p.reference())
+    assert err <= tol(torch.float16), err
+
+
+# ---------------------------------------------------------------------------------
+# Determinism / invariance (bitwise)
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_kernel_variants_and_cluster_sizes_bitwise_identical(lsg, dtype):
+    bounds, _, _ = segments_for(SKEWED, 64, 3)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 4)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    base = p.run("fused")
+    for kind in ("two_launch", "bgmv"):
+        assert torch.equal(p.run(kind), base), kind
+    for c in (1, 2, 3, 4, 8, 16):
+        lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
+        for mt in (1, 8):
+            lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, mt)
+            assert torch.equal(p.run("fused"), base), (c, mt)
+            assert torch.equal(p.run("two_launch"), base), (c, mt)
+    lsg.set_option(lsg.LSG_OPT_PDL, 1)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, 0)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 0)
+    assert torch.equal(p.run("fused"), base)
+
+
+def test_segment_permutation_permutes_rows_bitwise(lsg):
+    """test_sgmv.cpp:171-197 on the GPU: swapping segments moves rows, bit for bit."""
+    bounds, _, _ = segments_for(UNIFORM, 40, 8)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 9)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    base = p.run().cpu().numpy()
+    nseg = len(bounds) - 1
+    order = list(reversed(range(nseg)))
+    xs, nb, src_rows = [], [0], []
+    for s in order:
+        a, b = int(bounds[s]), int(bounds[s + 1])
+        xs.append(x[a:b])
+        nb.append(nb[-1] + b - a)
+        src_rows.extend(range(a, b))
+    q = Problem(lsg, np.concatenate(xs), A[order], B[order], nb, torch.float16)
+    got = q.run().cpu().numpy()
+    assert np.array_equal(got.view(np.uint16), base[src_rows].view(np.uint16))
+
+
+def test_no_adapter_rows_untouched_and_slot_indirection(lsg):
+    bounds = np.array([0, 3, 5, 9], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 21)
+    y0 = oracle().rng(22).fill_pm1(9 * 4096).reshape(9, 4096)
+    p = Problem(lsg, x, A, B, bounds, torch.float16, slots=[5, -1, 2], num_slots=7, layers=3, layer=2, y0=y0)
+    y = p.run()
+    assert torch.equal(y[3:5], p.y0[3:5])
+    assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(torch.float16)
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 1), (64, 48, 8), (136, 1000, 16), (4096, 4096, 12), (96, 40, 40)])
+def test_generic_path_odd_shapes(lsg, shape):
+    h_in, h_out, r = shape
+    bounds, _, _ = segments_for(SKEWED, 20, 1)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 2)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    err = row_norm_err(p.run().double().cpu().numpy(), p.reference())
+    assert err <= tol(torch.float16), err
+
+
+def test_generic_and_unaligned_rows(lsg):
+    bounds, _, _ = segments_for(DISTINCT, 8, 1)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 2)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    yref = p.reference()
+    lsg.set_option(lsg.LSG_OPT_FORCE_GENERIC, 1)
+    assert row_norm_err(p.run().double().cpu().numpy(), yref) <= tol(torch.float16)
+    lsg.set_option(lsg.LSG_OPT_FORCE_GENERIC, 0)
+    # x viewed with an odd row stride -> not 16-byte aligned -> generic path, same tolerance
+    xb = torch.zeros(8, 4096 + 3, dtype=torch.float16, device="cuda")
+    xb[:, 1:4097] = p.x
+    y = torch.zeros(8, 4096, dtype=torch.float16, device="cuda")
+    lsg.sgmv(y, xb[:, 1:4097], p.pool, p.seg_starts, p.seg_slot, 0)
+    torch.cuda.synchronize()
+    assert row_norm_err(y.double().cpu().numpy(), yref) <= tol(torch.float16)
+
+
+def test_invalid_arguments_raise(lsg):
+    from paper_2310_18547_b200._lib import LsgError
+    pool = lsg.AdapterPool(2, 1, 128, 128, 16, torch.float16)
+    x = torch.zeros(4, 128, dtype=torch.float16, device="cuda")
+    y = torch.zeros(4, 128, dtype=torch.float16, device="cuda")
+    ss = torch.tensor([0, 4], dtype=torch.int32, device="cuda")
+    sl = torch.tensor([0], dtype=torch.int32, device="cuda")
+    with pytest.raises(LsgError, match="layer"):
+        lsg.sgmv(y, x, pool, ss, sl, 3)
+    with pytest.raises(ValueError):
+        lsg.sgmv(y.float(), x, pool, ss, sl, 0)
+
+
+# ---------------------------------------------------------------------------------
+# K6: on-device segment builder
+# ---------------------------------------------------------------------------------
+def _host_grouping(row_slot, num_slots, lead):
+    key = [(0 if s == lead else s + 1) if 0 <= s < num_slots else 1 << 31 for s in row_slot]
+    perm = sorted(range(len(row_slot)), key=lambda i: (key[i], i))
+    starts, slots = [], []
+    for i, r in enumerate(perm):
+        if i == 0 or key[r] != key[perm[i - 1]]:
+            starts.append(i)
+            s = row_slot[r]
+            slots.append(s if 0 <= s < num_slots else -1)
+    return perm, starts + [len(row_slot)], slots
+
+
+@pytest.mark.parametrize("n,num_slots", [(1, 4), (9, 3), (64, 64), (64, 8), (333, 40), (2079, 1000), (16384, 7)])
+def test_build_segments_matches_host_grouping(lsg, n, num_slots):
+    rs = np.random.default_rng(n).integers(-1, num_slots + 1, n).astype(np.int32)
+    lead = int(rs[n // 2])
+    perm, starts, slots = _host_grouping(rs.tolist(), num_slots, lead)
+    row_perm, seg_starts, seg_slot, nseg = lsg.build_segments(torch.tensor(rs, device="cuda"), num_slots, lead)
+    k = int(nseg.item())
+    assert k == len(slots)
+    assert row_perm.cpu().tolist() == perm
+    assert seg_starts.cpu().tolist()[: k + 1] == starts
+    assert seg_slot.cpu().tolist()[:k] == slots
+    assert all(v == n for v in seg_starts.cpu().tolist()[k + 1:])
+
+
+def test_build_segments_reproduces_plan_batch_golden(lsg):
+    """plan_batch layouts (simulator.cpp:239-311) from the reference, slots = LoraId rank."""
+    for case in json.load(open(os.path.join(GOLDEN, "plan_batch.json"))):
+        lora, done, prompt = case["lora"], case["done"], case["prompt"]
+        plan = case["plan"]
+        uniq = sorted(set(lora))
+        slot_of = {l: i for i, l in enumerate(uniq)}
+        # token rows in request order: a prefill contributes prompt rows, a decode one row;
+        # only the first pending prefill is scheduled (simulator.cpp:267-276)
+        rows = []
+        for i, (l, d) in enumerate(zip(lora, done)):
+            if d:
+                rows.append(slot_of[l])
+            elif i == plan["prefill"]:
+                rows.extend([slot_of[l]] * prompt[i])
+        lead = slot_of[lora[plan["prefill"]]] if plan["prefill"] >= 0 else -1
+        _, seg_starts, seg_slot, nseg = lsg.build_segments(torch.tensor(rows, dtype=torch.int32, device="cuda"),
+                                                           len(uniq), lead)
+        k = int(nseg.item())
+        assert seg_starts.cpu().tolist()[: k + 1] == plan["bounds"]
+        assert [uniq[s] for s in seg_slot.cpu().tolist()[:k]] == plan["loras"]
+
+
+def test_builder_feeds_sgmv_without_host_readback(lsg):
+    n, ns = 64, 10
+    rs = torch.tensor(np.random.default_rng(3).integers(0, ns, n).astype(np.int32), device="cuda")
+    pool = lsg.AdapterPool(ns, 1, 4096, 4096, 16, torch.float16)
+    torch.manual_seed(0)
+    pool.a.uniform_(-1, 1)
+    pool.b.uniform_(-1, 1)
+    x = torch.empty(n, 4096, dtype=torch.float16, device="cuda").uniform_(-1, 1)
+    row_perm, seg_starts, seg_slot, _ = lsg.build_segments(rs, ns)
+    xg = torch.empty_like(x)
+    lsg.gather_rows(xg, x, row_perm)
+    yg = torch.zeros_like(x)
+    lsg.sgmv(yg, xg, pool, seg_starts, seg_slot, 0, num_segments=ns)  # host bound, not the true count
+    y = torch.zeros_like(x)
+    lsg.scatter_rows(y, yg, row_perm)
+    yb = torch.zeros_like(x)
+    lsg.bgmv(yb, x, pool, rs, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(y, yb)
