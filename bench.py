@@ -296,7 +296,7 @@ def main():
     extra = {}
     # isolated single-launch latency (no PDL overlap), L2 flushed between launches
     lsg.set_option(lsg.LSG_OPT_PDL, 0)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2; hides launch latency
     lat = []
     for i in range(20):
         flush.zero_()

@@ -24,9 +24,13 @@
 // Generic path (sgmv_generic_kernel): any shape / alignment, one CTA per row.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "sgmv_device.cuh"
 
 namespace lsg {
+
+namespace cg = cooperative_groups;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -95,6 +99,34 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
 // Balanced split of n items over c owners: owner i holds [i*n/c, (i+1)*n/c).
 __device__ __forceinline__ int split_lo(int i, int n, int c) { return (i * n) / c; }
 __device__ __forceinline__ int split_owner(int q, int n, int c) { return ((q + 1) * c - 1) / n; }
+
+// Largest rows*R*nq handled by the one-barrier (every-CTA-reduces-everything) form.
+constexpr int kRedundantReduceMax = 8192;
+
+// v[o] = sum over chunks q ascending of P_q[o], reading each chunk partial from
+// the shared memory of the CTA that owns it.  Owners hold contiguous ascending
+// chunk ranges, so walking owners in rank order walks q in order; loads are
+// issued in independent batches of 8 and summed strictly in sequence.
+template <int MT, int R>
+__device__ __forceinline__ float reduce_chunks(const float* P_sm, int o, int nq, int C) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int m = o / R, k = o - m * R;
+  float s = 0.f;
+  for (int r = 0; r < C; ++r) {
+    const int n = split_lo(r + 1, nq, C) - split_lo(r, nq, C);
+    const float* base = cluster.map_shared_rank(P_sm, r) + m * R + k;
+    int ql = 0;
+    for (; ql + 8 <= n; ql += 8) {
+      float t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = base[(ql + u) * MT * R];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += t[u];
+    }
+    for (; ql < n; ++ql) s += base[ql * MT * R];
+  }
+  return s;
+}
 
 template <typename T, int R, int MT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
@@ -262,28 +294,33 @@ __global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_con
       // ---- cluster reduction over chunks, ascending q --------------------------
       cluster_sync();  // B1: every CTA's P_sm is visible cluster-wide
       const int no = rows * R;
-      const int o0 = split_lo(crank, no, C), o1 = split_lo(crank + 1, no, C);
-      for (int o = o0 + tid; o < o1; o += kThreads) {
-        const int m = o / R, k = o - m * R;
-        float s = 0.f;
-        for (int q = 0; q < p.nq; ++q) {
-          const int owner = split_owner(q, p.nq, C);
-          const int ql = q - split_lo(owner, p.nq, C);
-          s += ld_dsmem_f32(P_sm + (ql * MT + m) * R + k, static_cast<uint32_t>(owner));
-        }
-        if constexpr (MODE == kShrink)
-          p.v_out[static_cast<int64_t>(r0 + m) * R + k] = s;
-        else
-          Vpart_sm[o - o0] = s;
-      }
-      cluster_sync();  // B2: shares visible (shrink: P_sm reads done)
-      if constexpr (MODE == kFused) {
-        for (int o = tid; o < no; o += kThreads) {
-          const int owner = split_owner(o, no, C);
-          V_sm[o] = ld_dsmem_f32(Vpart_sm + (o - split_lo(owner, no, C)), static_cast<uint32_t>(owner));
-        }
-        cluster_arrive();  // B3 (arrive): this CTA is done reading remote shared memory
+      if (MODE == kFused && no * p.nq <= kRedundantReduceMax) {
+        // Small reductions (decode): every CTA sums all rows*R outputs itself --
+        // one cluster barrier fewer than the distributed form, same order.
+        for (int o = tid; o < no; o += kThreads) V_sm[o] = reduce_chunks<MT, R>(P_sm, o, p.nq, C);
+        cluster_arrive();  // B3 (arrive): done reading remote shared memory
         __syncthreads();
+      } else {
+        const int o0 = split_lo(crank, no, C), o1 = split_lo(crank + 1, no, C);
+        for (int o = o0 + tid; o < o1; o += kThreads) {
+          const float s = reduce_chunks<MT, R>(P_sm, o, p.nq, C);
+          if constexpr (MODE == kShrink) {
+            const int m = o / R;
+            p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
+          } else {
+            Vpart_sm[o - o0] = s;
+          }
+        }
+        cluster_sync();  // B2: shares visible (shrink: remote P_sm reads done)
+        if constexpr (MODE == kFused) {
+          cg::cluster_group cluster = cg::this_cluster();
+          for (int o = tid; o < no; o += kThreads) {
+            const int owner = split_owner(o, no, C);
+            V_sm[o] = cluster.map_shared_rank(Vpart_sm, owner)[o - split_lo(owner, no, C)];
+          }
+          cluster_arrive();  // B3 (arrive)
+          __syncthreads();
+        }
       }
     }
 

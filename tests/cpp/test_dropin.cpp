@@ -1,0 +1,330 @@
+// test_dropin.cpp -- the reference's SGMV unit tests (proj/tests/unit/test_sgmv.cpp,
+// test_experiments.cpp:11-29) run against the B200 drop-in library
+// (liblorasim_b200.so), with the CPU oracle (oracle/liboracle.so) as the checker.
+//
+// Where the reference compares fp64 results with 1e-10, the GPU result is fp16
+// (or bf16) with fp32 accumulation; those checks compare against the oracle on
+// the DEQUANTISED inputs with the per-row normalised tolerance stated below.
+// Checks that are exact in 16-bit (small-integer known answers, zero weights,
+// bitwise permutation, the three GPU formulations agreeing) stay exact.
+//
+// Usage: test_dropin [cpu]   ("cpu": only the validation cases, no GPU needed)
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lorasim/b200.hpp"
+#include "lorasim/experiments.hpp"
+#include "lorasim/sgmv.hpp"
+#include "lorasim/workload.hpp"
+#include "lsg_sgmv.h"
+#include "sgmv_oracle.h"
+
+using namespace lorasim;
+
+namespace {
+
+int g_checks = 0, g_failures = 0;
+std::string g_case;
+
+#define CHECK(cond)                                                                       \
+  do {                                                                                    \
+    ++g_checks;                                                                           \
+    if (!(cond)) {                                                                        \
+      ++g_failures;                                                                       \
+      std::printf("FAIL [%s] %s:%d: %s\n", g_case.c_str(), __FILE__, __LINE__, #cond);   \
+    }                                                                                     \
+  } while (0)
+
+template <typename F>
+void check_throws_msg(F&& f, const std::string& fragment, int line) {
+  ++g_checks;
+  try {
+    f();
+  } catch (const std::invalid_argument& e) {
+    if (std::string(e.what()).find(fragment) != std::string::npos) return;
+    std::printf("FAIL [%s] line %d: message '%s' lacks '%s'\n", g_case.c_str(), line, e.what(), fragment.c_str());
+    ++g_failures;
+    return;
+  } catch (const std::exception& e) {
+    std::printf("FAIL [%s] line %d: wrong exception type: %s\n", g_case.c_str(), line, e.what());
+    ++g_failures;
+    return;
+  }
+  std::printf("FAIL [%s] line %d: no exception (expected '%s')\n", g_case.c_str(), line, fragment.c_str());
+  ++g_failures;
+}
+#define CHECK_THROWS_MSG(expr, frag) check_throws_msg([&] { (void)(expr); }, frag, __LINE__)
+
+Matrix from_rows(std::vector<std::vector<double>> rows) {
+  Matrix m(rows.size(), rows.empty() ? 0 : rows[0].size());
+  for (std::size_t i = 0; i < rows.size(); ++i)
+    for (std::size_t j = 0; j < rows[i].size(); ++j) m(i, j) = rows[i][j];
+  return m;
+}
+
+Matrix random_matrix(Rng& rng, std::size_t r, std::size_t c) {
+  Matrix m(r, c);
+  for (double& v : m.data()) v = rng.uniform01() * 2.0 - 1.0;
+  return m;
+}
+
+Batch random_batch(Rng& rng, std::size_t h_in, std::size_t h_out, std::size_t rank,
+                   const std::vector<std::size_t>& sizes) {
+  std::vector<std::size_t> bounds{0};
+  for (std::size_t s : sizes) bounds.push_back(bounds.back() + s);
+  Segments segs(bounds);
+  Matrix x = random_matrix(rng, segs.total_rows(), h_in);
+  std::vector<LoraModel> models;
+  for (std::size_t s = 0; s < sizes.size(); ++s) {
+    Matrix a = random_matrix(rng, h_in, rank);
+    Matrix b = random_matrix(rng, rank, h_out);
+    models.emplace_back(static_cast<LoraId>(s), std::move(a), std::move(b));
+  }
+  return Batch(std::move(x), std::move(segs), std::move(models));
+}
+
+Matrix quantized(const Matrix& m) {
+  Matrix q = m;
+  for (double& v : q.data()) v = b200::quantize(v, b200::precision());
+  return q;
+}
+
+// The oracle on the dequantised inputs (only accumulation + final rounding differ).
+Matrix oracle_addon(const Batch& b, const Matrix* w = nullptr) {
+  const std::size_t n = b.models.size(), h_in = b.h_in(), r = b.models[0].rank(), h_out = b.models[0].h_out();
+  std::vector<double> A, B;
+  for (const auto& m : b.models) {
+    const Matrix qa = quantized(m.a), qb = quantized(m.b);
+    A.insert(A.end(), qa.data().begin(), qa.data().end());
+    B.insert(B.end(), qb.data().begin(), qb.data().end());
+  }
+  const Matrix qx = quantized(b.x);
+  Matrix y(b.rows(), h_out);
+  std::vector<std::size_t> bounds = b.segments.boundaries();
+  if (w) {
+    const Matrix qw = quantized(*w);
+    orc_dense_projection(qx.data().data(), h_in, bounds.data(), n, A.data(), B.data(), r, h_out, qw.data().data(),
+                         y.data().data());
+  } else {
+    orc_lora_addon(qx.data().data(), h_in, bounds.data(), n, A.data(), B.data(), r, h_out, y.data().data());
+  }
+  return y;
+}
+
+// max_j |y_j - ref_j|_inf / |ref_j|_inf
+double row_err(const Matrix& y, const Matrix& ref) {
+  double worst = 0.0;
+  for (std::size_t i = 0; i < y.rows(); ++i) {
+    double num = 0.0, den = 1e-30;
+    for (std::size_t j = 0; j < y.cols(); ++j) {
+      num = std::fmax(num, std::fabs(y(i, j) - ref(i, j)));
+      den = std::fmax(den, std::fabs(ref(i, j)));
+    }
+    worst = std::fmax(worst, num / den);
+  }
+  return worst;
+}
+
+// Stated tolerance: fp16 output rounding <= 2^-11 per element, bf16 <= 2^-8.
+double tol() { return b200::precision() == b200::Precision::F16 ? 1.5e-3 : 8e-3; }
+
+// ---------------------------------------------------------------------------------------
+void validation_cases() {
+  g_case = "segments validate boundaries";
+  CHECK(Segments({0, 2, 3}).count() == 2);
+  CHECK(Segments({0, 2, 3}).total_rows() == 3);
+  CHECK(Segments({0, 2, 3}).size_of(1) == 1);
+  CHECK(Segments::single(5).count() == 1);
+  CHECK(Segments::empty().count() == 0);
+  CHECK_THROWS_MSG(Segments({1, 3}), "s_0 must be 0");
+  CHECK_THROWS_MSG(Segments({0, 0, 3}), "strictly increasing");
+  CHECK_THROWS_MSG(Segments({0, 3, 2}), "strictly increasing");
+  CHECK_THROWS_MSG(Segments(std::vector<std::size_t>{}), "boundary list empty");
+
+  g_case = "model validation";
+  Matrix a(2, 1), b(1, 2);
+  a(0, 0) = 1;
+  a(1, 0) = 1;
+  b(0, 0) = 1;
+  b(0, 1) = 1;
+  CHECK(LoraModel(7, a, b).rank() == 1);
+  CHECK_THROWS_MSG(LoraModel(0, a, Matrix(2, 2)), "A columns != B rows");
+  CHECK_THROWS_MSG(LoraModel(0, Matrix(2, 3), Matrix(3, 2)), "rank exceeds");
+  Matrix nan_a = a;
+  nan_a(0, 0) = std::nan("");
+  CHECK_THROWS_MSG(LoraModel(0, nan_a, b), "non-finite entry in A");
+
+  g_case = "shape and consistency errors";
+  Matrix x = Matrix::zeros(3, 2);
+  Segments segs({0, 2, 3});
+  LoraModel m0(0, Matrix::zeros(2, 1), Matrix::zeros(1, 2));
+  LoraModel m1(1, Matrix::zeros(2, 1), Matrix::zeros(1, 2));
+  CHECK_THROWS_MSG(Batch(x, segs, {m0}), "model count != segment count");
+  CHECK_THROWS_MSG(Batch(Matrix::zeros(2, 2), segs, {m0, m1}), "x row count != segment total");
+  LoraModel wide(1, Matrix::zeros(2, 2), Matrix::zeros(2, 2));
+  Batch het(x, segs, {m0, wide});
+  CHECK_THROWS_MSG(sgmv_shrink(het), "heterogeneous adapter ranks");
+  CHECK_THROWS_MSG(lora_addon(het), "heterogeneous adapter ranks");
+  Batch ok(x, segs, {m0, m1});
+  CHECK_THROWS_MSG(dense_projection(ok, Matrix::zeros(3, 2)), "w rows != batch hidden dim");
+  CHECK_THROWS_MSG(sgmv_expand(Matrix::zeros(3, 2), ok.segments, ok.models), "adapter rank != v column count");
+  CHECK_THROWS_MSG(sgmv_expand(Matrix::zeros(2, 1), ok.segments, ok.models), "v row count != segment total");
+  LoraModel other_out(1, Matrix::zeros(2, 1), Matrix::zeros(1, 3));
+  Batch mixed_out(x, segs, {m0, other_out});
+  CHECK_THROWS_MSG(lora_loop_oracle(mixed_out), "lora_loop_oracle: adapters disagree on output dim");
+  CHECK_THROWS_MSG(gather_bmm_oracle(mixed_out), "gather_bmm_oracle: adapters disagree on output dim");
+  CHECK_THROWS_MSG(lora_addon(mixed_out), "sgmv_expand: adapters disagree on output dim");
+  CHECK_THROWS_MSG(dense_projection(mixed_out, Matrix::zeros(2, 2)), "adapter output dim != w columns");
+
+  g_case = "empty batch";
+  Batch e(Matrix(0, 4), Segments::empty(), {});
+  CHECK(lora_addon(e).rows() == 0);
+  const Matrix dy = dense_projection(e, Matrix::zeros(4, 6));
+  CHECK(dy.rows() == 0 && dy.cols() == 6);
+
+  g_case = "quantize is round-to-nearest-even";
+  using b200::Precision;
+  CHECK(b200::quantize(1.0 + std::ldexp(1.0, -11), Precision::F16) == 1.0);             // tie -> even
+  CHECK(b200::quantize(1.0 + 3 * std::ldexp(1.0, -11), Precision::F16) == 1.0 + std::ldexp(1.0, -9));
+  CHECK(b200::quantize(70000.0, Precision::F16) == INFINITY);
+  CHECK(b200::quantize(std::ldexp(1.0, -25), Precision::F16) == 0.0);                   // half of min subnormal
+  CHECK(b200::quantize(1.0 + std::ldexp(1.0, -8), Precision::BF16) == 1.0);
+}
+
+void gpu_cases() {
+  g_case = "hand-checked two-segment add-on";
+  Batch b(from_rows({{1, 2}, {3, 4}, {5, 6}}), Segments({0, 2, 3}),
+          {LoraModel(0, from_rows({{1, 0}, {0, 1}}), from_rows({{1, 1}, {2, 0}})),
+           LoraModel(1, from_rows({{2, 0}, {1, 1}}), from_rows({{1, 3}, {0, 1}}))});
+  const Matrix expected = from_rows({{5, 1}, {11, 3}, {16, 54}});
+  CHECK(max_abs_diff(lora_addon(b), expected) == 0.0);
+  CHECK(max_abs_diff(lora_loop_oracle(b), expected) == 0.0);
+  CHECK(max_abs_diff(gather_bmm_oracle(b), expected) == 0.0);
+  CHECK(max_abs_diff(dense_projection(b, from_rows({{1, 0}, {0, 1}})), from_rows({{6, 3}, {14, 7}, {21, 60}})) == 0.0);
+  const Matrix v = sgmv_shrink(b);
+  CHECK(max_abs_diff(v, from_rows({{1, 2}, {3, 4}, {16, 6}})) == 0.0);
+  CHECK(max_abs_diff(sgmv_expand(v, b.segments, b.models), expected) == 0.0);
+
+  g_case = "single row rank-1 add-on";
+  Batch r1(from_rows({{1, 2}}), Segments({0, 1}), {LoraModel(0, from_rows({{1}, {1}}), from_rows({{1, 1}}))});
+  const Matrix y1 = lora_addon(r1);
+  CHECK(y1.rows() == 1 && y1(0, 0) == 3.0 && y1(0, 1) == 3.0);
+
+  g_case = "zero adapter weights give zero add-on";
+  Rng rng(11);
+  Matrix x = random_matrix(rng, 4, 8);
+  Batch z(x, Segments({0, 4}), {LoraModel(0, Matrix::zeros(8, 2), Matrix::zeros(2, 8))});
+  CHECK(max_abs_diff(lora_addon(z), Matrix::zeros(4, 8)) == 0.0);
+
+  g_case = "segmented kernel vs formulations and oracle over mixed groupings";
+  Rng rr(20240805);
+  const std::vector<std::vector<std::size_t>> patterns = {{1}, {8}, {1, 1, 1, 1}, {3, 1, 4}, {2, 2, 2, 2, 2}, {16, 1, 7}};
+  double worst = 0.0;
+  for (std::size_t h_in : {8u, 64u, 128u, 4096u}) {
+    for (std::size_t h_out : {16u, 128u, 4096u}) {
+      for (std::size_t rank : {1u, 4u, 8u, 16u}) {
+        for (const auto& pat : patterns) {
+          Batch bb = random_batch(rr, h_in, h_out, rank, pat);
+          const Matrix fused = lora_addon(bb);
+          CHECK(max_abs_diff(fused, lora_loop_oracle(bb)) < 1e-10);   // bitwise in practice
+          CHECK(max_abs_diff(fused, gather_bmm_oracle(bb)) < 1e-10);
+          const double e = row_err(fused, oracle_addon(bb));
+          worst = std::fmax(worst, e);
+          CHECK(e <= tol());
+        }
+      }
+    }
+  }
+  std::printf("  mixed groupings: worst normalised error vs oracle %.3e (tolerance %.1e)\n", worst, tol());
+
+  g_case = "dense projection equals x*w plus add-on";
+  Rng r77(77);
+  Batch db = random_batch(r77, 32, 48, 8, {4, 4, 8});
+  Matrix w = random_matrix(r77, 32, 48);
+  // y0 = x*W is rounded to the working precision before the LoRA term is added,
+  // so allow two output roundings
+  CHECK(row_err(dense_projection(db, w), oracle_addon(db, &w)) <= 2 * tol());
+
+  g_case = "add-on is linear in the activations";
+  Rng r5(5);
+  Batch lb = random_batch(r5, 16, 16, 4, {2, 3});
+  const Matrix base = lora_addon(lb);
+  Batch doubled = lb;
+  for (double& v : doubled.x.data()) v *= 2.0;  // exact in 16-bit: the result doubles bit for bit
+  const Matrix got2 = lora_addon(doubled);
+  double w2 = 0.0;
+  for (std::size_t i = 0; i < got2.data().size(); ++i) w2 = std::fmax(w2, std::fabs(got2.data()[i] - 2.0 * base.data()[i]));
+  CHECK(w2 == 0.0);
+  Batch scaled = lb;
+  for (double& v : scaled.x.data()) v *= 3.5;
+  Matrix ref35 = base;
+  for (double& v : ref35.data()) v *= 3.5;
+  CHECK(row_err(lora_addon(scaled), ref35) <= 3 * tol());
+
+  g_case = "segment order permutation permutes rows exactly";
+  Rng r99(99);
+  Batch pb = random_batch(r99, 4096, 4096, 16, {2, 3, 1});
+  const Matrix pbase = lora_addon(pb);
+  const std::vector<std::size_t> order = {1, 0, 2};
+  std::vector<std::size_t> bounds{0}, src_rows;
+  Matrix px(pb.rows(), pb.h_in());
+  std::vector<LoraModel> pmodels;
+  std::size_t out_row = 0;
+  for (std::size_t s : order) {
+    bounds.push_back(bounds.back() + pb.segments.size_of(s));
+    pmodels.push_back(pb.models[s]);
+    for (std::size_t r = pb.segments.begin_of(s); r < pb.segments.end_of(s); ++r, ++out_row) {
+      for (std::size_t c = 0; c < pb.h_in(); ++c) px(out_row, c) = pb.x(r, c);
+      src_rows.push_back(r);
+    }
+  }
+  const Matrix pgot = lora_addon(Batch(std::move(px), Segments(bounds), std::move(pmodels)));
+  bool same = true;
+  for (std::size_t r = 0; r < pgot.rows(); ++r)
+    for (std::size_t c = 0; c < pgot.cols(); ++c) same = same && pgot(r, c) == pbase(src_rows[r], c);
+  CHECK(same);
+
+  g_case = "shrink output shape is rows x rank";
+  Rng r3(3);
+  Batch sb = random_batch(r3, 16, 32, 4, {2, 3});
+  const Matrix sv = sgmv_shrink(sb);
+  CHECK(sv.rows() == 5 && sv.cols() == 4);
+
+  g_case = "verify_sgmv passes clean and catches a planted fault";
+  const VerifyReport okr = verify_sgmv(200, 42);
+  CHECK(okr.passed() && okr.trials == 200 && okr.failures == 0 && okr.worst_deviation < okr.tolerance);
+  const VerifyReport bad = verify_sgmv(8, 42, true);
+  CHECK(!bad.passed() && !bad.failed_cases.empty() && bad.failed_cases[0].deviation > bad.tolerance);
+  // the failing trial is the reference's trial 0 (shape pinned in tests/golden/verify_digest.json)
+  CHECK(!bad.failed_cases.empty() && bad.failed_cases[0].h_in == 64 && bad.failed_cases[0].h_out == 8 &&
+        bad.failed_cases[0].rank == 8 && bad.failed_cases[0].rows == 6 && bad.failed_cases[0].models == 6);
+  const VerifyReport a1 = verify_sgmv(50, 7), a2 = verify_sgmv(50, 7);
+  CHECK(a1.worst_deviation == a2.worst_deviation);
+
+  g_case = "serving pool indexes slots and layers";
+  b200::AdapterPool pool(4, 3, 4096, 4096, 16);
+  Rng rp(8);
+  Matrix pa = random_matrix(rp, 4096, 16), pbm = random_matrix(rp, 16, 4096);
+  CHECK(pool.load(1234, 2, pa, pbm) == 0);
+  CHECK(pool.slot_of(1234) == 0 && pool.slot_of(99) == -1);
+  CHECK(pool.table().num_layers == 3 && pool.table().rank == 16);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool cpu_only = argc > 1 && std::string(argv[1]) == "cpu";
+  validation_cases();
+  if (!cpu_only) {
+    gpu_cases();
+    b200::set_precision(b200::Precision::BF16);
+    g_case = "bf16";
+    gpu_cases();
+  }
+  std::printf("%s: %d checks, %d failures\n", cpu_only ? "drop-in (cpu)" : "drop-in (gpu)", g_checks, g_failures);
+  return g_failures == 0 ? 0 : 1;
+}
