@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--popularity", choices=list(POPS), default="distinct")
     ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--cluster", type=int, default=0, help="force the split-K cluster size (0 = library heuristic)")
+    ap.add_argument("--tile-rows", type=int, default=0, help="force rows per tile, 1 or 8 (0 = heuristic)")
     ap.add_argument("--sites", type=int, default=SITES_PER_LAYER * LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -231,6 +233,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dtype = torch.float16 if a.dtype == "fp16" else torch.bfloat16
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
     bounds = segments(a.popularity, batch)
     nseg = len(bounds) - 1
@@ -299,9 +303,9 @@ def main():
     flush = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2; hides launch latency
     lat = []
     for i in range(20):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
+            flush.zero_()  # same stream: evicts L2 and covers the host launch latency
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             lsg.sgmv(ys[i], xs[i], pool, seg_starts, seg_slot, i)
             e1.record(stream)

@@ -159,6 +159,13 @@ int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t 
                      int32_t kernel /* 0 fused, 1 shrink, 2 expand, 3 bgmv */,
                      lsg_launch_info* info);
 
+/* Phase tracing (profiling aid, off by default): when installed, thread 0 of
+ * every fast-path CTA (up to max_ctas, CTA index = blockIdx.y * C + rank) writes
+ * 16 u64 to device_buffer: clock64() at the kernel's phase boundaries in slots
+ * 0..11, %globaltimer at entry in slot 14 and the SM id in slot 15.  Pass
+ * (NULL, 0) to turn it off.  See scripts/trace_phases.py. */
+int lsg_set_trace(unsigned long long* device_buffer, int32_t max_ctas);
+
 const char* lsg_status_string(int status);
 const char* lsg_last_error(void);
 int lsg_version(void); /* major*10000 + minor*100 + patch */

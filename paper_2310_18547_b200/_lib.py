@@ -22,7 +22,7 @@ EXPORTED = (
     "lsg_sgmv", "lsg_sgmv_shrink", "lsg_sgmv_expand", "lsg_bgmv",
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
-    "lsg_last_error", "lsg_version",
+    "lsg_last_error", "lsg_version", "lsg_set_trace",
 )
 
 
@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         L.lsg_status_string.restype = C.c_char_p
         L.lsg_last_error.restype = C.c_char_p
         L.lsg_version.restype = C.c_int
+        L.lsg_set_trace.argtypes = [vp, i32]
         _lib = L
     return _lib
 

@@ -11,7 +11,8 @@
 
 namespace lsg {
 
-constexpr int kSmemBudget = 225 * 1024;
+constexpr int kSmemBudget = 225 * 1024;     // one CTA per SM at most
+constexpr int kCoresidentSmem = 113 * 1024;  // two CTAs per SM (228 KB incl. 1 KB reserved each)
 constexpr int kMaxCluster = 16;
 
 struct Plan {
@@ -24,6 +25,7 @@ struct Plan {
   int ncv_max = 0;
   int smem = 0;
   int mode = kFused;
+  int red_all = 0;
 };
 
 // Set by the API layer; read at launch.

@@ -36,6 +36,8 @@ std::atomic<int> g_opt_pdl{0};
 std::atomic<int> g_opt_force_cluster{0};
 std::atomic<int> g_opt_force_generic{0};
 std::atomic<int> g_opt_force_tile_rows{0};
+unsigned long long* g_trace = nullptr;
+int g_trace_ctas = 0;
 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -100,17 +102,23 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     pl.clusters = n_seg * pl.row_splits;
   }
   const int nq = t->h_in / KW, ncvt = t->h_out / 8;
+  // one-round (every CTA gets every chunk partial) reduction while that buffer is small
+  pl.red_all = pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0;
   auto smem_for = [&](int c) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
-    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nqc, ncv).total);
+    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, pl.red_all).total);
   };
-  int c_fit = 1;
-  while (c_fit < kMaxCluster && smem_for(c_fit) > kSmemBudget) ++c_fit;
+  // Split-K cluster size: the smallest C whose CTA fits next to a CTA of the
+  // following launch on the same SM (2 x ~113 KB), so programmatic dependent
+  // launches overlap; then grow C until the grid covers every SM once.
+  const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::min(nq, ncvt));
+  int c_full = 1;
+  while (c_full < kMaxCluster && smem_for(c_full) > kSmemBudget) ++c_full;
+  int c = 1;
+  while (c < kMaxCluster && smem_for(c) > kCoresidentSmem) ++c;
   const int sms = num_sms();
-  int c_fill = std::max(1, std::min(kMaxCluster, sms / std::max(1, pl.clusters)));
-  int c = std::max(c_fit, c_fill);
-  const int span = pl.mode == kExpand ? ncvt : std::min(nq, pl.mode == kShrink ? nq : ncvt);
-  c = std::max(c_fit, std::min(c, std::max(1, span)));
+  while (c < kMaxCluster && c < span && pl.clusters * c < sms) ++c;
+  c = std::max(c, c_full);
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.cluster = c;
@@ -192,6 +200,9 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.ncvt = tbl->h_out / 8;
   p.nqc_max = pl.nqc_max;
   p.ncv_max = pl.ncv_max;
+  p.red_all = pl.red_all;
+  p.trace = g_trace;
+  p.trace_ctas = g_trace_ctas;
   switch (pl.mode) {
     case kFused: return launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs);
     case kShrink: return launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs);
@@ -360,6 +371,13 @@ int lsg_gather_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, 
 int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, const int32_t* row_perm,
                      int32_t rows, int32_t cols, lsg_stream_t stream) {
   return permute_rows(false, dst, ld_dst, src, ld_src, row_perm, rows, cols, stream);
+}
+
+int lsg_set_trace(unsigned long long* device_buffer, int32_t max_ctas) {
+  if (max_ctas < 0 || (max_ctas > 0 && device_buffer == nullptr)) return fail(LSG_EINVAL, "lsg_set_trace: bad buffer");
+  g_trace = max_ctas ? device_buffer : nullptr;
+  g_trace_ctas = max_ctas;
+  return LSG_OK;
 }
 
 const char* lsg_status_string(int status) {

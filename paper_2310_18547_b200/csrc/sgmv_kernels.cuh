@@ -34,7 +34,8 @@ namespace cg = cooperative_groups;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int KW = 128;  // rows of A (h_in elements) per canonical reduction chunk
+constexpr int KW = 128;     // rows of A (h_in elements) per canonical reduction chunk
+constexpr int kPieces = 4;  // A arrives in up to 4 bulk copies, one mbarrier each
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 
@@ -62,17 +63,36 @@ struct FastParams {
   int32_t ncvt;  // h_out / 8
   int32_t nqc_max;
   int32_t ncv_max;
+  int32_t red_all;  // 1: every CTA receives every chunk partial; 0: owner-sliced two-round reduction
+  unsigned long long* trace;  // optional phase trace (lsg_set_trace), 16 u64 per CTA
+  int32_t trace_ctas;
 };
 
+// Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
+// globaltimer at entry, slot 15: SM id).  Off unless lsg_set_trace() installed a buffer.
+#define LSG_TRACE(i)                                                                                   \
+  do {                                                                                                 \
+    if (p.trace != nullptr && threadIdx.x == 0) {                                                      \
+      const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                            \
+      if (cta_ < p.trace_ctas) p.trace[cta_ * 16 + (i)] = clock64();                                   \
+    }                                                                                                  \
+  } while (0)
+
 struct SmemLayout {
-  uint32_t bars, a, x, b, y, p, vpart, v, total;
+  uint32_t bars, a, x, b, y, recv, v, total;
 };
 
 __host__ __device__ inline uint32_t align128(uint32_t v) { return (v + 127u) & ~127u; }
 
+// Floats of the reduction receive buffer: all chunk partials (red_all) or the
+// chunk partials of this CTA's slice of the rows*R outputs.
+__host__ __device__ inline int recv_floats(int red_all, int nq, int MT, int R, int C) {
+  return red_all ? nq * MT * R : nq * ((MT * R + C - 1) / C);
+}
+
 // Identical on host (launch sizing) and device (carve-up).
-__host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C, int nqc_max,
-                                                  int ncv_max) {
+__host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C, int nq, int nqc_max, int ncv_max,
+                                                  int red_all) {
   SmemLayout L;
   uint32_t o = 0;
   const bool sh = mode != kExpand, ex = mode != kShrink;
@@ -86,10 +106,8 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
   if (ex) o = align128(o + R * ncv_max * 16);
   L.y = o;
   if (ex) o = align128(o + MT * ncv_max * 16);
-  L.p = o;
-  if (sh) o = align128(o + nqc_max * MT * R * 4);
-  L.vpart = o;
-  if (sh) o = align128(o + ((MT * R + C - 1) / C) * 4);
+  L.recv = o;
+  if (sh) o = align128(o + recv_floats(red_all, nq, MT, R, C) * 4);
   L.v = o;
   o = align128(o + MT * R * 4);
   L.total = o;
@@ -100,56 +118,44 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
 __device__ __forceinline__ int split_lo(int i, int n, int c) { return (i * n) / c; }
 __device__ __forceinline__ int split_owner(int q, int n, int c) { return ((q + 1) * c - 1) / n; }
 
-// Largest rows*R*nq handled by the one-barrier (every-CTA-reduces-everything) form.
-constexpr int kRedundantReduceMax = 8192;
-
-// v[o] = sum over chunks q ascending of P_q[o], reading each chunk partial from
-// the shared memory of the CTA that owns it.  Owners hold contiguous ascending
-// chunk ranges, so walking owners in rank order walks q in order; loads are
-// issued in independent batches of 8 and summed strictly in sequence.
-template <int MT, int R>
-__device__ __forceinline__ float reduce_chunks(const float* P_sm, int o, int nq, int C) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int m = o / R, k = o - m * R;
-  float s = 0.f;
-  for (int r = 0; r < C; ++r) {
-    const int n = split_lo(r + 1, nq, C) - split_lo(r, nq, C);
-    const float* base = cluster.map_shared_rank(P_sm, r) + m * R + k;
-    int ql = 0;
-    for (; ql + 8 <= n; ql += 8) {
-      float t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = base[(ql + u) * MT * R];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s += t[u];
-    }
-    for (; ql < n; ++ql) s += base[ql * MT * R];
-  }
-  return s;
-}
-
 template <typename T, int R, int MT, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
+__global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
   static_assert(R == 8 || R == 16 || R == 32 || R == 64, "fast path ranks");
   constexpr int VPR = R / 8;       // 16-byte vectors per A row
   constexpr int RPI = 32 / VPR;    // A rows covered by one warp instruction
   constexpr int ITER = KW / RPI;   // per-lane FMA chain length per chunk
   constexpr bool kSh = MODE != kExpand;
   constexpr bool kEx = MODE != kShrink;
+  constexpr int kBarB = kPieces, kBarRed = kPieces + 1, kBarV = kPieces + 2;
 
   extern __shared__ __align__(128) uint8_t smem[];
   const int C = static_cast<int>(gridDim.x);
   const int crank = static_cast<int>(blockIdx.x);  // cluster dims (C,1,1), grid.x == C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const SmemLayout L = make_layout(MODE, R, MT, C, p.nqc_max, p.ncv_max);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);  // 0 A, 1 B, 2 x, 3 y
+  const int red_all = MODE == kFused ? p.red_all : 0;
+  const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   T* A_sm = reinterpret_cast<T*>(smem + L.a);
   T* x_sm = reinterpret_cast<T*>(smem + L.x);
   uint4* B_sm = reinterpret_cast<uint4*>(smem + L.b);
   uint4* y_sm = reinterpret_cast<uint4*>(smem + L.y);
-  float* P_sm = reinterpret_cast<float*>(smem + L.p);
-  float* Vpart_sm = reinterpret_cast<float*>(smem + L.vpart);
+  float* recv = reinterpret_cast<float*>(smem + L.recv);
   float* V_sm = reinterpret_cast<float*>(smem + L.v);
+
+  if (p.trace != nullptr && tid == 0 && blockIdx.y * gridDim.x + blockIdx.x < p.trace_ctas) {
+    unsigned long long gt;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 14] = gt;
+    p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 15] = smid;
+  }
+  LSG_TRACE(0);
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < kPieces + 3; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
 
   // ---- which rows / adapter this cluster serves (uniform across the cluster) ----
   int slot, seg_begin, seg_end, first_tile, tile_step;
@@ -183,77 +189,94 @@ __global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_con
     return;
   }
 
+  LSG_TRACE(1);
   const int q0 = split_lo(crank, p.nq, C), nqc = split_lo(crank + 1, p.nq, C) - q0;
   const int cv0 = split_lo(crank, p.ncvt, C), ncv = split_lo(crank + 1, p.ncvt, C) - cv0;
   const int ndl = nqc * KW;  // this CTA's slice of h_in (x_sm row stride)
-  const T* A = kSh ? static_cast<const T*>(p.a_ptr[slot]) + p.a_off : nullptr;
-  const T* B = kEx ? static_cast<const T*>(p.b_ptr[slot]) + p.b_off : nullptr;
+  const int npieces = min(kPieces, nqc);
+  const int slice_max = (MT * R + C - 1) / C;
 
-  if (tid == 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  // Adapter weights: every byte this CTA will ever need, requested up front.
+  __syncthreads();                 // barrier inits visible to this CTA
+  if constexpr (kSh) cluster_arrive();  // ... and to the cluster (waited on before the first push)
+
+  // Adapter weights: every byte this CTA needs, requested at entry (before the
+  // PDL wait, so they stream while the previous kernel drains).  A arrives in
+  // kPieces chunk-aligned pieces with their own barriers so the shrink starts
+  // on the first piece; B follows on one barrier.
   if (tid == 0) {
     const uint64_t pol = l2_evict_first_policy();
     if (kSh && nqc > 0) {
-      const uint32_t bytes = static_cast<uint32_t>(ndl * R * sizeof(T));
-      mbar_arrive_expect_tx(&bars[0], bytes);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(A + static_cast<int64_t>(q0) * KW * R);
-      uint8_t* dst = reinterpret_cast<uint8_t*>(A_sm);
-      for (uint32_t off = 0; off < bytes; off += 32768u) {
-        const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-        bulk_g2s_hint(dst + off, src + off, n, &bars[0], pol);
+      const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
+      for (int i = 0; i < npieces; ++i) {
+        const int c0 = (i * nqc) / npieces, c1 = ((i + 1) * nqc) / npieces;
+        const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
+        mbar_arrive_expect_tx(&bars[i], bytes);
+        bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[i], pol);
       }
     }
     if (kEx && ncv > 0) {
-      mbar_arrive_expect_tx(&bars[1], static_cast<uint32_t>(R * ncv * 16));
+      const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
+      mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
       for (int k = 0; k < R; ++k)
-        bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out + cv0 * 8,
-                      static_cast<uint32_t>(ncv * 16), &bars[1], pol);
+        bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
+                      &bars[kBarB], pol);
     }
   }
+  LSG_TRACE(2);
   // x, v and y may be produced by the preceding kernel: wait for it here.
   pdl_wait();
   pdl_launch_dependents();
+  LSG_TRACE(3);
 
   uint32_t phase = 0;
   for (int t = first_tile; t < ntiles; t += tile_step, phase ^= 1u) {
     const int r0 = seg_begin + t * MT;
     const int rows = min(MT, seg_end - r0);
-    __syncthreads();  // previous tile's x_sm / y_sm / V_sm reads are complete
-    if (tid == 0) {
-      if (kSh && nqc > 0) {
-        mbar_arrive_expect_tx(&bars[2], static_cast<uint32_t>(rows * ndl * sizeof(T)));
-        for (int m = 0; m < rows; ++m)
-          bulk_g2s(x_sm + m * ndl,
-                   static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW,
-                   static_cast<uint32_t>(ndl * sizeof(T)), &bars[2]);
+    const int no = rows * R;
+    const int o0 = split_lo(crank, no, C), o1 = split_lo(crank + 1, no, C);
+    // Activations go through cp.async (LDGSTS), not the TMA queue the weights
+    // occupy, so they land about one memory latency after the wait.
+    if constexpr (kSh) {
+      const int nv = ndl / 8;  // 16-byte vectors per x row slice
+      for (int i = tid; i < rows * nv; i += kThreads) {
+        const int m = i / nv, c = i - m * nv;
+        cp_async16(x_sm + m * ndl + c * 8,
+                   static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW + c * 8);
       }
-      if (kEx && ncv > 0) {
-        mbar_arrive_expect_tx(&bars[3], static_cast<uint32_t>(rows * ncv * 16));
-        for (int m = 0; m < rows; ++m)
-          bulk_g2s(y_sm + m * ncv,
-                   static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + cv0 * 8,
-                   static_cast<uint32_t>(ncv * 16), &bars[3]);
+    }
+    cp_async_commit();
+    if constexpr (kEx) {
+      for (int i = tid; i < rows * ncv; i += kThreads) {
+        const int m = i / ncv, c = i - m * ncv;
+        cp_async16(y_sm + m * ncv + c,
+                   static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + c) * 8);
       }
+    }
+    cp_async_commit();
+    if (kSh && tid == 0) {
+      // bytes this CTA will receive this tile (peers may already be sending:
+      // the tx-count may go transiently negative, the phase cannot complete
+      // before this arrive)
+      mbar_arrive_expect_tx(&bars[kBarRed],
+                            static_cast<uint32_t>(p.nq * (red_all ? no : (o1 - o0)) * 4));
+      if (MODE == kFused && !red_all) mbar_arrive_expect_tx(&bars[kBarV], static_cast<uint32_t>(no * 4));
     }
 
     if constexpr (MODE == kExpand) {
-      for (int i = tid; i < rows * R; i += kThreads)
-        V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
-      __syncthreads();
+      for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
     } else {
-      // ---- shrink: per-chunk partials P_q[m, k] ---------------------------------
-      if (nqc > 0) {
-        mbar_wait(&bars[0], 0);
-        mbar_wait(&bars[2], phase);
-      }
+      cp_async_wait<1>();  // this thread's x vectors
+      __syncthreads();     // everyone's
+      LSG_TRACE(4);
+      if (t == first_tile) cluster_wait();  // every peer's barriers are initialised
+      LSG_TRACE(5);
+      // ---- shrink: per-chunk partials P_q[m, k], pushed to the reducers ------------
       const int rowoff = lane / VPR, vec = lane % VPR;
       const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
       for (int ql = warp; ql < nqc; ql += kWarps) {
+        int piece = 0;  // wait for the piece holding chunk ql (no-op after the first tile)
+        while (((piece + 1) * nqc) / npieces <= ql) ++piece;
+        mbar_wait(&bars[piece], 0);
         float acc[MT][8];
 #pragma unroll
         for (int m = 0; m < MT; ++m)
@@ -281,54 +304,72 @@ __global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_con
 #pragma unroll
               for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
         if (lane < VPR) {
+          const int q = q0 + ql;
+          if (red_all) {
+            for (int dst = 0; dst < C; ++dst) {
+              const uint32_t rbar = mapa_u32(&bars[kBarRed], static_cast<uint32_t>(dst));
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            if (m < rows) {
-              float4* dst = reinterpret_cast<float4*>(P_sm + (ql * MT + m) * R + vec * 8);
-              dst[0] = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
-              dst[1] = make_float4(acc[m][4], acc[m][5], acc[m][6], acc[m][7]);
+              for (int m = 0; m < MT; ++m) {
+                if (m < rows) {
+                  const uint32_t ra = mapa_u32(recv + (q * MT + m) * R + vec * 8, static_cast<uint32_t>(dst));
+                  st_async_v4(ra, acc[m][0], acc[m][1], acc[m][2], acc[m][3], rbar);
+                  st_async_v4(ra + 16, acc[m][4], acc[m][5], acc[m][6], acc[m][7], rbar);
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              if (m < rows) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const int o = m * R + vec * 8 + j;
+                  const int owner = split_owner(o, no, C);
+                  const int jl = o - split_lo(owner, no, C);
+                  st_async_f32(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[m][j],
+                               mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
+                }
+              }
             }
           }
         }
       }
-      // ---- cluster reduction over chunks, ascending q --------------------------
-      cluster_sync();  // B1: every CTA's P_sm is visible cluster-wide
-      const int no = rows * R;
-      if (MODE == kFused && no * p.nq <= kRedundantReduceMax) {
-        // Small reductions (decode): every CTA sums all rows*R outputs itself --
-        // one cluster barrier fewer than the distributed form, same order.
-        for (int o = tid; o < no; o += kThreads) V_sm[o] = reduce_chunks<MT, R>(P_sm, o, p.nq, C);
-        cluster_arrive();  // B3 (arrive): done reading remote shared memory
-        __syncthreads();
+      // ---- reduction over chunks, ascending q ------------------------------------
+      LSG_TRACE(6);
+      mbar_wait(&bars[kBarRed], phase);
+      LSG_TRACE(7);
+      if (red_all) {
+        for (int o = tid; o < no; o += kThreads) {
+          float s = 0.f;
+          for (int q = 0; q < p.nq; ++q) s += recv[(q * MT) * R + o];
+          V_sm[o] = s;
+        }
       } else {
-        const int o0 = split_lo(crank, no, C), o1 = split_lo(crank + 1, no, C);
         for (int o = o0 + tid; o < o1; o += kThreads) {
-          const float s = reduce_chunks<MT, R>(P_sm, o, p.nq, C);
+          float s = 0.f;
+          for (int q = 0; q < p.nq; ++q) s += recv[q * slice_max + (o - o0)];
           if constexpr (MODE == kShrink) {
             const int m = o / R;
             p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
           } else {
-            Vpart_sm[o - o0] = s;
+            for (int dst = 0; dst < C; ++dst)
+              st_async_f32(mapa_u32(V_sm + o, static_cast<uint32_t>(dst)), s,
+                           mapa_u32(&bars[kBarV], static_cast<uint32_t>(dst)));
           }
         }
-        cluster_sync();  // B2: shares visible (shrink: remote P_sm reads done)
-        if constexpr (MODE == kFused) {
-          cg::cluster_group cluster = cg::this_cluster();
-          for (int o = tid; o < no; o += kThreads) {
-            const int owner = split_owner(o, no, C);
-            V_sm[o] = cluster.map_shared_rank(Vpart_sm, owner)[o - split_lo(owner, no, C)];
-          }
-          cluster_arrive();  // B3 (arrive)
-          __syncthreads();
-        }
+        if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
       }
     }
 
     if constexpr (kEx) {
+      LSG_TRACE(8);
+      cp_async_wait<0>();  // this thread's y vectors
+      __syncthreads();     // V_sm and every y vector visible
+      LSG_TRACE(9);
       // ---- expand: y[m, n] += sum_k v[m, k] B[k, n] -----------------------------
       if (ncv > 0) {
-        mbar_wait(&bars[1], 0);
-        mbar_wait(&bars[3], phase);
+        mbar_wait(&bars[kBarB], 0);
+        LSG_TRACE(10);
         for (int i = tid; i < rows * ncv; i += kThreads) {
           const int m = i / ncv, cv = i - m * ncv;
           float acc[8];
@@ -351,7 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) sgmv_fast_kernel(const __grid_con
         }
       }
     }
-    if constexpr (MODE == kFused) cluster_wait();  // B3 (wait)
+    LSG_TRACE(11);
+    // Next tile reuses x_sm / y_sm / V_sm and the receive buffer: every CTA of
+    // the cluster must be done with this tile first.
+    if (t + tile_step < ntiles) {
+      if constexpr (kSh) cluster_sync();
+      else __syncthreads();
+    }
   }
 }
 

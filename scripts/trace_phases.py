@@ -1,0 +1,80 @@
+"""Per-phase timeline of one fused SGMV launch inside a back-to-back stream.
+
+Uses the library's phase trace (lsg_set_trace): thread 0 of every CTA stamps
+clock64 at the kernel's phase boundaries.  Prints, per phase, the median and
+max over CTAs of the time since that CTA's entry, plus the entry skew
+(%globaltimer) across CTAs.
+
+    python scripts/trace_phases.py --popularity distinct --batch 64 [--cluster C] [--pdl 1]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2310_18547_b200 as lsg  # noqa: E402
+from paper_2310_18547_b200 import _lib  # noqa: E402
+from bench import segments  # noqa: E402
+
+PHASES = ["entry", "metadata", "tma_issued", "pdl_wait_done", "x_landed", "cluster_ready", "shrink_pushed",
+          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--popularity", default="distinct")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--rank", type=int, default=16)
+    ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--sites", type=int, default=64)
+    a = ap.parse_args()
+    lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
+    h, r = a.hidden, a.rank
+    bounds = segments(a.popularity, a.batch)
+    n = len(bounds) - 1
+    pool = lsg.AdapterPool(n, a.sites, h, h, r, torch.float16)
+    pool.a.uniform_(-1, 1)
+    pool.b.uniform_(-1, 1)
+    xs = torch.empty(a.sites, a.batch, h, dtype=torch.float16, device="cuda").uniform_(-1, 1)
+    ys = torch.zeros_like(xs)
+    ss = torch.tensor(bounds, dtype=torch.int32, device="cuda")
+    sl = torch.arange(n, dtype=torch.int32, device="cuda")
+    info = lsg.query_launch(pool, n, a.batch)
+    ctas = info["grid_ctas"]
+    buf = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        for s in range(a.sites):
+            lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
+    torch.cuda.synchronize()
+    mid = a.sites // 2
+    for s in range(a.sites):
+        if s == mid:
+            _lib.call("lsg_set_trace", C.c_void_p(buf.data_ptr()), ctas)
+        lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
+        if s == mid:
+            _lib.call("lsg_set_trace", None, 0)
+    torch.cuda.synchronize()
+    t = buf.view(ctas, 16).cpu()
+    ghz = 1.965
+    rel = (t[:, :12] - t[:, :1]).double() / ghz / 1e3  # us since this CTA's entry
+    valid = t[:, 11] != 0
+    print(f"config {a.popularity} batch={a.batch} h={h} r={r} launch={info} pdl={a.pdl} traced CTAs={int(valid.sum())}")
+    ent = t[valid, 14].double()
+    print(f"entry skew across CTAs (globaltimer): {(ent.max() - ent.min()).item() / 1e3:.2f} us")
+    for i, name in enumerate(PHASES):
+        col = rel[valid, i]
+        col = col[t[valid, i] != 0]
+        if col.numel():
+            print(f"  {i:2d} {name:15s} median {col.median().item():7.2f} us   max {col.max().item():7.2f} us")
+    end = ent + rel[valid, 11] * 1e3
+    print(f"first entry -> last tile_done: {(end.max() - ent.min()).item() / 1e3:.2f} us")
+
+
+if __name__ == "__main__":
+    main()
