@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -102,11 +103,12 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     pl.clusters = n_seg * pl.row_splits;
   }
   const int nq = t->h_in / KW, ncvt = t->h_out / 8;
-  // one-round (every CTA gets every chunk partial) reduction while that buffer is small
-  pl.red_all = pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0;
+  // one-round reduction (every CTA receives every chunk partial) while that
+  // receive buffer stays <= 16 KB; otherwise owner-sliced with a second round
+  auto red_all_for = [&](int c) { return pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0; };
   auto smem_for = [&](int c) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
-    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, pl.red_all).total);
+    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c)).total);
   };
   // Split-K cluster size: the smallest C whose CTA fits next to a CTA of the
   // following launch on the same SM (2 x ~113 KB), so programmatic dependent
@@ -121,6 +123,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   c = std::max(c, c_full);
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
+  pl.red_all = red_all_for(c);
   pl.cluster = c;
   pl.nqc_max = (nq + c - 1) / c;
   pl.ncv_max = (ncvt + c - 1) / c;
@@ -203,6 +206,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.red_all = pl.red_all;
   p.trace = g_trace;
   p.trace_ctas = g_trace_ctas;
+  static const int exp_flags = [] {
+    const char* e = std::getenv("LSG_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.exp_flags = exp_flags;
   switch (pl.mode) {
     case kFused: return launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs);
     case kShrink: return launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs);

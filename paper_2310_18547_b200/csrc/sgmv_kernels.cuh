@@ -66,6 +66,7 @@ struct FastParams {
   int32_t red_all;  // 1: every CTA receives every chunk partial; 0: owner-sliced two-round reduction
   unsigned long long* trace;  // optional phase trace (lsg_set_trace), 16 u64 per CTA
   int32_t trace_ctas;
+  int32_t exp_flags;  // LSG_EXP experiment bits (profiling only; 0 in production)
 };
 
 // Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
@@ -84,11 +85,9 @@ struct SmemLayout {
 
 __host__ __device__ inline uint32_t align128(uint32_t v) { return (v + 127u) & ~127u; }
 
-// Floats of the reduction receive buffer: all chunk partials (red_all) or the
-// chunk partials of this CTA's slice of the rows*R outputs.
-__host__ __device__ inline int recv_floats(int red_all, int nq, int MT, int R, int C) {
-  return red_all ? nq * MT * R : nq * ((MT * R + C - 1) / C);
-}
+// Owner-sliced reduction: the rows*R outputs are split over the C CTAs in
+// quads of 4 floats; slice_max floats per CTA.
+__host__ __device__ inline int slice_floats(int MT, int R, int C) { return ((MT * R / 4 + C - 1) / C) * 4; }
 
 // Identical on host (launch sizing) and device (carve-up).
 __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C, int nq, int nqc_max, int ncv_max,
@@ -106,8 +105,8 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
   if (ex) o = align128(o + R * ncv_max * 16);
   L.y = o;
   if (ex) o = align128(o + MT * ncv_max * 16);
-  L.recv = o;
-  if (sh) o = align128(o + recv_floats(red_all, nq, MT, R, C) * 4);
+  L.recv = o;  // chunk partials received from the cluster
+  if (sh) o = align128(o + (red_all ? nq * MT * R : nq * slice_floats(MT, R, C)) * 4);
   L.v = o;
   o = align128(o + MT * R * 4);
   L.total = o;
@@ -151,9 +150,15 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 15] = smid;
   }
   LSG_TRACE(0);
+  // Let the next launch on the stream start as soon as SM resources allow: its
+  // prologue and weight stream then overlap this kernel (it still waits for us
+  // before touching activations).
+  pdl_launch_dependents();
   if (tid == 0) {
 #pragma unroll
-    for (int i = 0; i < kPieces + 3; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i <= kBarB; ++i) mbar_init(&bars[i], 1);
+    mbar_init(&bars[kBarRed], gridDim.x);  // one arrival per CTA of the cluster
+    mbar_init(&bars[kBarV], gridDim.x);
     fence_mbar_init();
   }
 
@@ -193,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   const int q0 = split_lo(crank, p.nq, C), nqc = split_lo(crank + 1, p.nq, C) - q0;
   const int cv0 = split_lo(crank, p.ncvt, C), ncv = split_lo(crank + 1, p.ncvt, C) - cv0;
   const int ndl = nqc * KW;  // this CTA's slice of h_in (x_sm row stride)
-  const int npieces = min(kPieces, nqc);
-  const int slice_max = (MT * R + C - 1) / C;
+  const int npieces = (p.exp_flags & 2) ? min(1, nqc) : min(kPieces, nqc);
+  const int slice_max = slice_floats(MT, R, C);
 
   __syncthreads();                 // barrier inits visible to this CTA
   if constexpr (kSh) cluster_arrive();  // ... and to the cluster (waited on before the first push)
@@ -202,22 +207,31 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   // Adapter weights: every byte this CTA needs, requested at entry (before the
   // PDL wait, so they stream while the previous kernel drains).  A arrives in
   // kPieces chunk-aligned pieces with their own barriers so the shrink starts
-  // on the first piece; B follows on one barrier.
-  if (tid == 0) {
-    const uint64_t pol = l2_evict_first_policy();
-    if (kSh && nqc > 0) {
-      const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
-      for (int i = 0; i < npieces; ++i) {
-        const int c0 = (i * nqc) / npieces, c1 = ((i + 1) * nqc) / npieces;
-        const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
-        mbar_arrive_expect_tx(&bars[i], bytes);
-        bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[i], pol);
-      }
+  // on the first piece; B follows on one barrier.  Warp 0 issues A, warp 1
+  // issues B (one row per lane) -- the two pointer loads and the issue run in
+  // parallel.
+  const int a_warp = (p.exp_flags & 4) ? 1 : 0, b_warp = (p.exp_flags & 4) ? 0 : (kSh ? 1 : 0);
+  if (kSh && warp == a_warp && nqc > 0) {
+    const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
+    if (lane < npieces) {
+      const int c0 = (lane * nqc) / npieces, c1 = ((lane + 1) * nqc) / npieces;
+      const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
+      mbar_arrive_expect_tx(&bars[lane], bytes);
+      if (p.exp_flags & 1)
+        bulk_g2s(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane]);
+      else
+        bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane], l2_evict_first_policy());
     }
-    if (kEx && ncv > 0) {
-      const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
-      mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
-      for (int k = 0; k < R; ++k)
+  }
+  if (kEx && warp == b_warp && ncv > 0) {
+    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
+    if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    for (int k = lane; k < R; k += 32) {
+      if (p.exp_flags & 1)
+        bulk_g2s(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16), &bars[kBarB]);
+      else
         bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
                       &bars[kBarB], pol);
     }
@@ -225,7 +239,6 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   LSG_TRACE(2);
   // x, v and y may be produced by the preceding kernel: wait for it here.
   pdl_wait();
-  pdl_launch_dependents();
   LSG_TRACE(3);
 
   uint32_t phase = 0;
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     const int r0 = seg_begin + t * MT;
     const int rows = min(MT, seg_end - r0);
     const int no = rows * R;
-    const int o0 = split_lo(crank, no, C), o1 = split_lo(crank + 1, no, C);
+    const int o0 = split_lo(crank, no / 4, C) * 4, o1 = split_lo(crank + 1, no / 4, C) * 4;
     // Activations go through cp.async (LDGSTS), not the TMA queue the weights
     // occupy, so they land about one memory latency after the wait.
     if constexpr (kSh) {
@@ -253,14 +266,6 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       }
     }
     cp_async_commit();
-    if (kSh && tid == 0) {
-      // bytes this CTA will receive this tile (peers may already be sending:
-      // the tx-count may go transiently negative, the phase cannot complete
-      // before this arrive)
-      mbar_arrive_expect_tx(&bars[kBarRed],
-                            static_cast<uint32_t>(p.nq * (red_all ? no : (o1 - o0)) * 4));
-      if (MODE == kFused && !red_all) mbar_arrive_expect_tx(&bars[kBarV], static_cast<uint32_t>(no * 4));
-    }
 
     if constexpr (MODE == kExpand) {
       for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
@@ -273,70 +278,67 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       // ---- shrink: per-chunk partials P_q[m, k], pushed to the reducers ------------
       const int rowoff = lane / VPR, vec = lane % VPR;
       const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
-      for (int ql = warp; ql < nqc; ql += kWarps) {
-        int piece = 0;  // wait for the piece holding chunk ql (no-op after the first tile)
+      // Work unit = (chunk, row): every warp takes units until none are left.  A
+      // unit's arithmetic depends only on its chunk and row, never on which warp,
+      // CTA or tile size computes it.
+      const int nunits = nqc * rows;
+      for (int u = warp; u < nunits; u += kWarps) {
+        const int ql = u / rows, m = u - ql * rows;
+        int piece = 0;  // wait for the piece holding chunk ql (no-op once it has landed)
         while (((piece + 1) * nqc) / npieces <= ql) ++piece;
         mbar_wait(&bars[piece], 0);
-        float acc[MT][8];
+        if (u == 0) LSG_TRACE(12);
+        float acc[8];
 #pragma unroll
-        for (int m = 0; m < MT; ++m)
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
+        const T* xc = x_sm + m * ndl + ql * KW + rowoff;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
-#pragma unroll 4
         for (int it = 0; it < ITER; ++it) {
-          const int dl = ql * KW + it * RPI + rowoff;
           float a[8];
-          Cvt<T>::unpack8(Av[dl * VPR + vec], a);
+          Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
+          const float xm = Cvt<T>::to_f(xc[it * RPI]);
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            if (m < rows) {
-              const float xm = Cvt<T>::to_f(x_sm[m * ndl + dl]);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(xm, a[j], acc[m][j]);
-            }
-          }
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
         }
+        if (u == 0) LSG_TRACE(13);
 #pragma unroll
         for (int off = VPR; off < 32; off <<= 1)
 #pragma unroll
-          for (int m = 0; m < MT; ++m)
-            if (m < rows)
+          for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+        // Every lane now holds its vec's 8 partial sums P_q[m, vec*8 .. +8).  Store
+        // them straight into the reducers' shared memory (DSMEM, 16-byte quads);
+        // the 32/VPR lanes sharing a vec split the destinations between them.
+        const int q = q0 + ql;
+        const int g = lane / VPR;
 #pragma unroll
-              for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
-        if (lane < VPR) {
-          const int q = q0 + ql;
+        for (int h = 0; h < 2; ++h) {
+          const int o = m * R + vec * 8 + h * 4;
           if (red_all) {
-            for (int dst = 0; dst < C; ++dst) {
-              const uint32_t rbar = mapa_u32(&bars[kBarRed], static_cast<uint32_t>(dst));
-#pragma unroll
-              for (int m = 0; m < MT; ++m) {
-                if (m < rows) {
-                  const uint32_t ra = mapa_u32(recv + (q * MT + m) * R + vec * 8, static_cast<uint32_t>(dst));
-                  st_async_v4(ra, acc[m][0], acc[m][1], acc[m][2], acc[m][3], rbar);
-                  st_async_v4(ra + 16, acc[m][4], acc[m][5], acc[m][6], acc[m][7], rbar);
-                }
-              }
+            const uint32_t local = smem_u32(recv + q * MT * R + o);
+            for (int dst = (g + h) % RPI; dst < C; dst += RPI) {
+              uint32_t ra;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
+              st_cluster_v4(ra, acc[h * 4 + 0], acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3]);
             }
-          } else {
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-              if (m < rows) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const int o = m * R + vec * 8 + j;
-                  const int owner = split_owner(o, no, C);
-                  const int jl = o - split_lo(owner, no, C);
-                  st_async_f32(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[m][j],
-                               mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
-                }
-              }
-            }
+          } else if (g == h) {
+            const int owner = split_owner(o / 4, no / 4, C);
+            const int jl = o - split_lo(owner, no / 4, C) * 4;
+            st_cluster_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[h * 4 + 0],
+                          acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3]);
           }
         }
       }
+      // Publish: every thread's remote stores precede the CTA barrier; then one
+      // thread per destination releases them to that CTA (cluster scope).
+      __syncthreads();
+      if (tid < C) {
+        fence_acq_rel_cluster();
+        mbar_arrive_remote(mapa_u32(&bars[kBarRed], static_cast<uint32_t>(tid)));
+      }
       // ---- reduction over chunks, ascending q ------------------------------------
       LSG_TRACE(6);
-      mbar_wait(&bars[kBarRed], phase);
+      mbar_wait_cluster(&bars[kBarRed], phase);
       LSG_TRACE(7);
       if (red_all) {
         for (int o = tid; o < no; o += kThreads) {
@@ -352,12 +354,22 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
             const int m = o / R;
             p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
           } else {
-            for (int dst = 0; dst < C; ++dst)
-              st_async_f32(mapa_u32(V_sm + o, static_cast<uint32_t>(dst)), s,
-                           mapa_u32(&bars[kBarV], static_cast<uint32_t>(dst)));
+            const uint32_t local = smem_u32(V_sm + o);
+            for (int dst = 0; dst < C; ++dst) {
+              uint32_t ra;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
+              st_cluster_f32(ra, s);
+            }
           }
         }
-        if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
+        if constexpr (MODE == kFused) {
+          __syncthreads();
+          if (tid < C) {
+            fence_acq_rel_cluster();
+            mbar_arrive_remote(mapa_u32(&bars[kBarV], static_cast<uint32_t>(tid)));
+          }
+          mbar_wait_cluster(&bars[kBarV], phase);
+        }
       }
     }
 
@@ -393,12 +405,11 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       }
     }
     LSG_TRACE(11);
-    // Next tile reuses x_sm / y_sm / V_sm and the receive buffer: every CTA of
-    // the cluster must be done with this tile first.
-    if (t + tile_step < ntiles) {
-      if constexpr (kSh) cluster_sync();
-      else __syncthreads();
-    }
+    // Every CTA of the cluster must be done with this tile (its outgoing bulk
+    // copies read our staging buffers; the next tile reuses them) before anyone
+    // restages -- or exits.
+    if constexpr (kSh) cluster_sync();
+    else if (t + tile_step < ntiles) __syncthreads();
   }
 }
 

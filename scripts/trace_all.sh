@@ -1,5 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for args in "--popularity distinct" "--popularity distinct --pdl 0" "--popularity distinct --cluster 4" "--popularity identical" "--popularity identical --cluster 8" "--popularity uniform --cluster 8"; do
-  timeout 120 python scripts/trace_phases.py $args
+for pop in ${TRACE_POPS:-distinct identical}; do
+  for pdl in 1 0; do
+    timeout 120 python scripts/trace_phases.py --popularity $pop --pdl $pdl
+  done
 done

@@ -20,7 +20,7 @@ from paper_2310_18547_b200 import _lib  # noqa: E402
 from bench import segments  # noqa: E402
 
 PHASES = ["entry", "metadata", "tma_issued", "pdl_wait_done", "x_landed", "cluster_ready", "shrink_pushed",
-          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done"]
+          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done", "chunk0_ready", "chunk0_fma_done"]
 
 
 def main():
@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--sites", type=int, default=64)
+    ap.add_argument("--graph", type=int, default=1, help="1: trace inside a CUDA-graph replay (steady state)")
     a = ap.parse_args()
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
@@ -48,21 +49,33 @@ def main():
     info = lsg.query_launch(pool, n, a.batch)
     ctas = info["grid_ctas"]
     buf = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
-    for _ in range(3):
-        for s in range(a.sites):
-            lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
-    torch.cuda.synchronize()
     mid = a.sites // 2
-    for s in range(a.sites):
-        if s == mid:
-            _lib.call("lsg_set_trace", C.c_void_p(buf.data_ptr()), ctas)
-        lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
-        if s == mid:
-            _lib.call("lsg_set_trace", None, 0)
+
+    def step(trace):
+        for s in range(a.sites):
+            if trace and s == mid:
+                _lib.call("lsg_set_trace", C.c_void_p(buf.data_ptr()), ctas)
+            lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
+            if trace and s == mid:
+                _lib.call("lsg_set_trace", None, 0)
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        step(False)
+    torch.cuda.synchronize()
+    if a.graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(True)  # the traced launch sits mid-stream, replayed back to back
+        for _ in range(5):
+            g.replay()
+    else:
+        with torch.cuda.stream(stream):
+            step(True)
     torch.cuda.synchronize()
     t = buf.view(ctas, 16).cpu()
     ghz = 1.965
-    rel = (t[:, :12] - t[:, :1]).double() / ghz / 1e3  # us since this CTA's entry
+    rel = (t[:, :14] - t[:, :1]).double() / ghz / 1e3  # us since this CTA's entry
     valid = t[:, 11] != 0
     print(f"config {a.popularity} batch={a.batch} h={h} r={r} launch={info} pdl={a.pdl} traced CTAs={int(valid.sum())}")
     ent = t[valid, 14].double()
