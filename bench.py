@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--cluster", type=int, default=0, help="force the split-K cluster size (0 = library heuristic)")
     ap.add_argument("--tile-rows", type=int, default=0, help="force rows per tile, 1 or 8 (0 = heuristic)")
+    ap.add_argument("--no-l2-staging", action="store_true", help="keep B resident from kernel entry")
     ap.add_argument("--sites", type=int, default=SITES_PER_LAYER * LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -235,6 +236,7 @@ def main():
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
+    lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, int(a.no_l2_staging))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
     bounds = segments(a.popularity, batch)
     nseg = len(bounds) - 1

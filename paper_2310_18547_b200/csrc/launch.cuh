@@ -12,7 +12,7 @@
 namespace lsg {
 
 constexpr int kSmemBudget = 225 * 1024;     // one CTA per SM at most
-constexpr int kCoresidentSmem = 113 * 1024;  // two CTAs per SM (228 KB incl. 1 KB reserved each)
+constexpr int kCoresidentSmem = 74 * 1024;   // three CTAs' smem per SM (measured best: C=4 at the headline shape)
 constexpr int kMaxCluster = 16;
 
 struct Plan {
@@ -26,6 +26,7 @@ struct Plan {
   int smem = 0;
   int mode = kFused;
   int red_all = 0;
+  int alias_ab = 0;
 };
 
 // Set by the API layer; read at launch.

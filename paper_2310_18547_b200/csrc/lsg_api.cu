@@ -37,6 +37,7 @@ std::atomic<int> g_opt_pdl{0};
 std::atomic<int> g_opt_force_cluster{0};
 std::atomic<int> g_opt_force_generic{0};
 std::atomic<int> g_opt_force_tile_rows{0};
+std::atomic<int> g_opt_no_alias{0};
 unsigned long long* g_trace = nullptr;
 int g_trace_ctas = 0;
 
@@ -106,9 +107,12 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   // one-round reduction (every CTA receives every chunk partial) while that
   // receive buffer stays <= 16 KB; otherwise owner-sliced with a second round
   auto red_all_for = [&](int c) { return pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0; };
+  // Single-tile clusters (every segment one tile) keep only A resident ahead of
+  // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
+  pl.alias_ab = pl.mode == kFused && (kernel == kKBgmv || s_n <= n_seg * pl.mt) && !(g_opt_no_alias.load()) ? 1 : 0;
   auto smem_for = [&](int c) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
-    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c)).total);
+    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), pl.alias_ab).total);
   };
   // Split-K cluster size: the smallest C whose CTA fits next to a CTA of the
   // following launch on the same SM (2 x ~113 KB), so programmatic dependent
@@ -204,6 +208,7 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.nqc_max = pl.nqc_max;
   p.ncv_max = pl.ncv_max;
   p.red_all = pl.red_all;
+  p.alias_ab = pl.alias_ab;
   p.trace = g_trace;
   p.trace_ctas = g_trace_ctas;
   static const int exp_flags = [] {
@@ -272,6 +277,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       if (value != 0 && value != 1 && value != 8) return fail(LSG_EINVAL, "lsg: tile rows must be 0, 1 or 8");
       g_opt_force_tile_rows = value;
       return LSG_OK;
+    case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -282,6 +288,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_FORCE_CLUSTER: return g_opt_force_cluster.load();
     case LSG_OPT_FORCE_GENERIC: return g_opt_force_generic.load();
     case LSG_OPT_FORCE_TILE_ROWS: return g_opt_force_tile_rows.load();
+    case LSG_OPT_NO_L2_STAGING: return g_opt_no_alias.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -67,6 +67,7 @@ struct FastParams {
   unsigned long long* trace;  // optional phase trace (lsg_set_trace), 16 u64 per CTA
   int32_t trace_ctas;
   int32_t exp_flags;  // LSG_EXP experiment bits (profiling only; 0 in production)
+  int32_t alias_ab;   // 1: single-tile clusters; B is prefetched into L2 and later loaded over A's smem
 };
 
 // Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
@@ -91,18 +92,26 @@ __host__ __device__ inline int slice_floats(int MT, int R, int C) { return ((MT 
 
 // Identical on host (launch sizing) and device (carve-up).
 __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C, int nq, int nqc_max, int ncv_max,
-                                                  int red_all) {
+                                                  int red_all, int alias_ab = 0) {
   SmemLayout L;
   uint32_t o = 0;
   const bool sh = mode != kExpand, ex = mode != kShrink;
+  const uint32_t a_bytes = sh ? nqc_max * KW * R * 2 : 0, b_bytes = ex ? R * ncv_max * 16 : 0;
   L.bars = o;
   o += 128;
   L.a = o;
-  if (sh) o = align128(o + nqc_max * KW * R * 2);
-  L.x = o;
-  if (sh) o = align128(o + MT * nqc_max * KW * 2);
-  L.b = o;
-  if (ex) o = align128(o + R * ncv_max * 16);
+  if (alias_ab) {  // B is loaded over A once the shrink has consumed it
+    L.b = o;
+    o = align128(o + (a_bytes > b_bytes ? a_bytes : b_bytes));
+    L.x = o;
+    o = align128(o + MT * nqc_max * KW * 2);
+  } else {
+    o = align128(o + a_bytes);
+    L.x = o;
+    if (sh) o = align128(o + MT * nqc_max * KW * 2);
+    L.b = o;
+    o = align128(o + b_bytes);
+  }
   L.y = o;
   if (ex) o = align128(o + MT * ncv_max * 16);
   L.recv = o;  // chunk partials received from the cluster
@@ -132,7 +141,8 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   const int crank = static_cast<int>(blockIdx.x);  // cluster dims (C,1,1), grid.x == C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int red_all = MODE == kFused ? p.red_all : 0;
-  const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all);
+  const int alias_ab = MODE == kFused ? p.alias_ab : 0;
+  const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all, alias_ab);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   T* A_sm = reinterpret_cast<T*>(smem + L.a);
   T* x_sm = reinterpret_cast<T*>(smem + L.x);
@@ -223,8 +233,17 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane], l2_evict_first_policy());
     }
   }
+  const T* Bslice = nullptr;
   if (kEx && warp == b_warp && ncv > 0) {
     const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
+    Bslice = B;
+  }
+  if (kEx && warp == b_warp && ncv > 0 && alias_ab) {
+    // B's smem is still holding A: only warm L2 now, load after the shrink
+    for (int k = lane; k < R; k += 32)
+      bulk_prefetch_l2(Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16));
+  } else if (kEx && warp == b_warp && ncv > 0) {
+    const T* B = Bslice;
     if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
     __syncwarp();
     const uint64_t pol = l2_evict_first_policy();
@@ -237,6 +256,19 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     }
   }
   LSG_TRACE(2);
+  if (p.exp_flags & 8) {  // experiment: weight stream only
+    for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
+    if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
+    if constexpr (kSh) cluster_wait();
+    return;
+  }
+  if (p.exp_flags & 16) {  // experiment: weights + activations, no compute
+    pdl_wait();
+    for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
+    if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
+    if constexpr (kSh) cluster_wait();
+    return;
+  }
   // x, v and y may be produced by the preceding kernel: wait for it here.
   pdl_wait();
   LSG_TRACE(3);
@@ -331,7 +363,16 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       }
       // Publish: every thread's remote stores precede the CTA barrier; then one
       // thread per destination releases them to that CTA (cluster scope).
+      if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
       __syncthreads();
+      if (kEx && alias_ab && warp == b_warp && ncv > 0) {
+        // A is consumed: bring the (L2-warm) B slice into the same shared memory
+        if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
+        __syncwarp();
+        for (int k = lane; k < R; k += 32)
+          bulk_g2s(B_sm + k * ncv, Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
+                   &bars[kBarB]);
+      }
       if (tid < C) {
         fence_acq_rel_cluster();
         mbar_arrive_remote(mapa_u32(&bars[kBarRed], static_cast<uint32_t>(tid)));

@@ -87,6 +87,16 @@ def main():
             print(f"  {i:2d} {name:15s} median {col.median().item():7.2f} us   max {col.max().item():7.2f} us")
     end = ent + rel[valid, 11] * 1e3
     print(f"first entry -> last tile_done: {(end.max() - ent.min()).item() / 1e3:.2f} us")
+    # absolute timeline anchored at the earliest return from griddepcontrol.wait
+    # (= the previous launch's completion in a back-to-back stream)
+    absu = ent.unsqueeze(1) / 1e3 + rel[valid]  # us
+    t0 = absu[:, 3].min()
+    print("absolute (us after the first pdl_wait return): median / max over CTAs")
+    for i, name in enumerate(PHASES):
+        col = absu[:, i] - t0
+        ok = t[valid, i] != 0
+        if ok.any():
+            print(f"  {i:2d} {name:15s} {col[ok].median().item():7.2f}  {col[ok].max().item():7.2f}")
 
 
 if __name__ == "__main__":
