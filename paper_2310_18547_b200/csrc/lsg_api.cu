@@ -109,7 +109,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   auto red_all_for = [&](int c) { return pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0; };
   // Single-tile clusters (every segment one tile) keep only A resident ahead of
   // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
-  pl.alias_ab = pl.mode == kFused && (kernel == kKBgmv || s_n <= n_seg * pl.mt) && !(g_opt_no_alias.load()) ? 1 : 0;
+  // (s_n == n_seg: every segment is one row, so every cluster has exactly one tile)
+  pl.alias_ab = pl.mode == kFused && (kernel == kKBgmv || s_n == n_seg) && !(g_opt_no_alias.load()) ? 1 : 0;
   auto smem_for = [&](int c) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
     return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), pl.alias_ab).total);

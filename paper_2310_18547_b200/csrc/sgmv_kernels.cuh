@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i <= kBarB; ++i) mbar_init(&bars[i], 1);
-    mbar_init(&bars[kBarRed], gridDim.x);  // one arrival per CTA of the cluster
-    mbar_init(&bars[kBarV], gridDim.x);
+    mbar_init(&bars[kBarRed], 1);  // completed by the bytes the cluster pushes (st.async complete_tx)
+    mbar_init(&bars[kBarV], 1);
     fence_mbar_init();
   }
 
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
   const int slice_max = slice_floats(MT, R, C);
 
   __syncthreads();                 // barrier inits visible to this CTA
-  if constexpr (kSh) cluster_arrive();  // ... and to the cluster (waited on before the first push)
+  if constexpr (kSh) cluster_arrive_relaxed();  // ... and (fence.mbarrier_init) to the cluster; waited on before the first push
 
   // Adapter weights: every byte this CTA needs, requested at entry (before the
   // PDL wait, so they stream while the previous kernel drains).  A arrives in
@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       }
     }
     cp_async_commit();
+    if (kSh && tid == 0) {
+      // bytes this CTA will receive this tile; peers may already be pushing (the
+      // tx-count may go transiently negative; the phase needs this arrive too)
+      mbar_arrive_expect_tx(&bars[kBarRed], static_cast<uint32_t>(p.nq * (red_all ? no : (o1 - o0)) * 4));
+      if (MODE == kFused && !red_all) mbar_arrive_expect_tx(&bars[kBarV], static_cast<uint32_t>(no * 4));
+    }
 
     if constexpr (MODE == kExpand) {
       for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
@@ -319,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         int piece = 0;  // wait for the piece holding chunk ql (no-op once it has landed)
         while (((piece + 1) * nqc) / npieces <= ql) ++piece;
         mbar_wait(&bars[piece], 0);
-        if (u == 0) LSG_TRACE(12);
         float acc[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
@@ -333,38 +338,40 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
         }
-        if (u == 0) LSG_TRACE(13);
 #pragma unroll
         for (int off = VPR; off < 32; off <<= 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
-        // Every lane now holds its vec's 8 partial sums P_q[m, vec*8 .. +8).  Store
-        // them straight into the reducers' shared memory (DSMEM, 16-byte quads);
-        // the 32/VPR lanes sharing a vec split the destinations between them.
+        // Every lane now holds its vec's 8 partial sums P_q[m, vec*8 .. +8).  Push
+        // them into the reducers' shared memory with st.async (async proxy: the
+        // receiver's mbarrier completes on the bytes -- no cluster fence); the
+        // 32/VPR lanes sharing a vec split the 16-byte quads / destinations.
         const int q = q0 + ql;
         const int g = lane / VPR;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int o = m * R + vec * 8 + h * 4;
           if (red_all) {
-            const uint32_t local = smem_u32(recv + q * MT * R + o);
+            const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
             for (int dst = (g + h) % RPI; dst < C; dst += RPI) {
-              uint32_t ra;
+              uint32_t ra, rb;
               asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-              st_cluster_v4(ra, acc[h * 4 + 0], acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3]);
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
+              st_async_v4(ra, acc[h * 4 + 0], acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3], rb);
             }
           } else if (g == h) {
             const int owner = split_owner(o / 4, no / 4, C);
             const int jl = o - split_lo(owner, no / 4, C) * 4;
-            st_cluster_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[h * 4 + 0],
-                          acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3]);
+            st_async_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[h * 4 + 0],
+                        acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3],
+                        mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
           }
         }
       }
-      // Publish: every thread's remote stores precede the CTA barrier; then one
-      // thread per destination releases them to that CTA (cluster scope).
+      LSG_TRACE(12);
       if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
       __syncthreads();
+      LSG_TRACE(13);
       if (kEx && alias_ab && warp == b_warp && ncv > 0) {
         // A is consumed: bring the (L2-warm) B slice into the same shared memory
         if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
@@ -373,13 +380,9 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
           bulk_g2s(B_sm + k * ncv, Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
                    &bars[kBarB]);
       }
-      if (tid < C) {
-        fence_acq_rel_cluster();
-        mbar_arrive_remote(mapa_u32(&bars[kBarRed], static_cast<uint32_t>(tid)));
-      }
       // ---- reduction over chunks, ascending q ------------------------------------
       LSG_TRACE(6);
-      mbar_wait_cluster(&bars[kBarRed], phase);
+      mbar_wait(&bars[kBarRed], phase);
       LSG_TRACE(7);
       if (red_all) {
         for (int o = tid; o < no; o += kThreads) {
@@ -395,22 +398,16 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
             const int m = o / R;
             p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
           } else {
-            const uint32_t local = smem_u32(V_sm + o);
+            const uint32_t local = smem_u32(V_sm + o), lbar = smem_u32(&bars[kBarV]);
             for (int dst = 0; dst < C; ++dst) {
-              uint32_t ra;
+              uint32_t ra, rb;
               asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-              st_cluster_f32(ra, s);
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
+              st_async_f32(ra, s, rb);
             }
           }
         }
-        if constexpr (MODE == kFused) {
-          __syncthreads();
-          if (tid < C) {
-            fence_acq_rel_cluster();
-            mbar_arrive_remote(mapa_u32(&bars[kBarV], static_cast<uint32_t>(tid)));
-          }
-          mbar_wait_cluster(&bars[kBarV], phase);
-        }
+        if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
       }
     }
 
@@ -446,11 +443,14 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       }
     }
     LSG_TRACE(11);
-    // Every CTA of the cluster must be done with this tile (its outgoing bulk
-    // copies read our staging buffers; the next tile reuses them) before anyone
-    // restages -- or exits.
-    if constexpr (kSh) cluster_sync();
-    else if (t + tile_step < ntiles) __syncthreads();
+    // The next tile reuses x_sm / y_sm / V_sm and the receive buffers: every CTA
+    // of the cluster must be done with this tile before anyone pushes again.
+    // (After the last tile nothing more is sent to anyone, and every incoming
+    // byte was awaited, so CTAs exit without a cluster barrier.)
+    if (t + tile_step < ntiles) {
+      if constexpr (kSh) cluster_sync();
+      else __syncthreads();
+    }
   }
 }
 

@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for pop in ${TRACE_POPS:-distinct identical}; do
-  for pdl in 1 0; do
-    timeout 120 python scripts/trace_phases.py --popularity $pop --pdl $pdl
-  done
+for c in ${TRACE_CS:-2 4}; do
+  timeout 120 python scripts/trace_phases.py --popularity distinct --pdl 1 --cluster $c
 done

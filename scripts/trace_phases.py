@@ -20,7 +20,7 @@ from paper_2310_18547_b200 import _lib  # noqa: E402
 from bench import segments  # noqa: E402
 
 PHASES = ["entry", "metadata", "tma_issued", "pdl_wait_done", "x_landed", "cluster_ready", "shrink_pushed",
-          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done", "chunk0_ready", "chunk0_fma_done"]
+          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done", "units_done", "cta_synced"]
 
 
 def main():
