@@ -39,6 +39,16 @@ POPS = {"distinct": 0, "uniform": 1, "skewed": 2, "identical": 3}
 SITES_PER_LAYER, LAYERS = 7, 32
 
 
+PRESETS = {
+    "c1": dict(hidden=4096, rank=16, batch=32, segments="8,8,8,8"),
+    "c2": dict(hidden=4096, rank=16, batch=64, popularity="distinct"),
+    "c3": dict(hidden=5120, rank=64, batch=64, popularity="uniform"),
+    "c3-bgmv": dict(hidden=5120, rank=64, batch=64, popularity="uniform", kernel="bgmv"),
+    "c4": dict(hidden=4096, rank=16, prefill=2048, sites=32),
+    "c5": dict(hidden=8192, rank=16, batch=64, popularity="distinct", slots=1000, sites=32),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -54,12 +64,28 @@ def parse():
     ap.add_argument("--cluster", type=int, default=0, help="force the split-K cluster size (0 = library heuristic)")
     ap.add_argument("--tile-rows", type=int, default=0, help="force rows per tile, 1 or 8 (0 = heuristic)")
     ap.add_argument("--no-l2-staging", action="store_true", help="keep B resident from kernel entry")
+    ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
+                    help="sgmv: segmented launch; bgmv: per-row adapter slots (decode BGMV)")
+    ap.add_argument("--slots", type=int, default=0, help="adapter-pool slots (0 = one per segment)")
+    ap.add_argument("--segments", default="", help="explicit segment sizes, e.g. 8,8,8,8 (overrides popularity)")
+    ap.add_argument("--prefill", type=int, default=0, help="mixed batch: one prefill segment of this many rows "
+                    "plus 31 distinct decode rows (configs[3])")
+    ap.add_argument("--preset", choices=["c1", "c2", "c3", "c3-bgmv", "c4", "c5"], default="",
+                    help="BASELINE.json configs: c1 h4096 r16 32 rows/4 LoRAs; c2 headline; c3 h5120 r64 uniform; "
+                         "c4 prefill 2048 + 31 decodes; c5 h8192 r16 1000-slot pool")
     ap.add_argument("--sites", type=int, default=SITES_PER_LAYER * LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also print per-(popularity,batch) lines to stderr")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graph, no extras)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    for k, v in PRESETS.get(a.preset, {}).items():
+        setattr(a, k, v)
+    if a.prefill:
+        a.segments = ",".join([str(a.prefill)] + ["1"] * 31)
+    if a.segments:
+        a.batch = sum(int(x) for x in a.segments.split(","))
+    return a
 
 
 def alg_bytes(rows, nseg, h, r, e=2):
@@ -82,7 +108,19 @@ def segments(pop: str, batch: int, seed: int = 11):
 
 
 def workload_name(a):
-    return f"llama2-7b-lora h={a.hidden} r={a.rank} batch={a.batch} decode {a.popularity} ({a.dtype})"
+    model = {4096: "llama2-7b", 5120: "llama2-13b", 8192: "llama2-70b"}.get(a.hidden, "custom")
+    shape = (f"prefill {a.prefill} + 31 decode" if a.prefill else
+             f"segments {a.segments}" if a.segments else f"batch={a.batch} decode {a.popularity}")
+    return f"{model}-lora h={a.hidden} r={a.rank} {shape} {a.kernel} ({a.dtype})"
+
+
+def bounds_for(a):
+    if a.segments:
+        b = [0]
+        for x in a.segments.split(","):
+            b.append(b[-1] + int(x))
+        return b
+    return segments(a.popularity, a.batch)
 
 
 # ----------------------------------------------------------------------------------
@@ -141,7 +179,7 @@ class ClockSampler:
 def _cpu_problem(a, seed=5):
     from oracle.oracle import Oracle
     o = Oracle()
-    bounds = np.array(segments(a.popularity, a.batch), dtype=np.uint64)
+    bounds = np.array(bounds_for(a), dtype=np.uint64)
     g = o.rng(seed)
     n = len(bounds) - 1
     h, r = a.hidden, a.rank
@@ -238,24 +276,34 @@ def main():
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, int(a.no_l2_staging))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
-    bounds = segments(a.popularity, batch)
+    bounds = bounds_for(a)
     nseg = len(bounds) - 1
     # Request-partitioned weak scaling: every rank owns its own batch of `batch` rows
     # and its own replica of the adapter pool -- no collective on the data path.
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    pool = lsg.AdapterPool(nseg, sites, h, h, r, dtype)
+    nslots = max(a.slots, nseg)
+    pool = lsg.AdapterPool(nslots, sites, h, h, r, dtype)
     pool.a.uniform_(-1, 1, generator=gen)
     pool.b.uniform_(-1, 1, generator=gen)
     xs = torch.empty(sites, batch, h, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen)
     ys = torch.zeros(sites, batch, h, dtype=dtype, device="cuda")
     seg_starts = torch.tensor(bounds, dtype=torch.int32, device="cuda")
-    seg_slot = torch.arange(nseg, dtype=torch.int32, device="cuda")
+    # the batch's adapters are distinct slots spread over the pool
+    slots = torch.randperm(nslots, generator=torch.Generator().manual_seed(7 + rank))[:nseg].to(torch.int32)
+    seg_slot = slots.cuda()
+    row_slot = torch.repeat_interleave(slots, torch.tensor(np.diff(bounds))).to(torch.int32).cuda()
     bytes_per_launch = alg_bytes(batch, nseg, h, r)
-    info = lsg.query_launch(pool, nseg, batch)
+    info = lsg.query_launch(pool, nseg, batch, lsg.KERNEL_BGMV if a.kernel == "bgmv" else lsg.KERNEL_FUSED)
+
+    def launch(s):
+        if a.kernel == "bgmv":
+            lsg.bgmv(ys[s], xs[s], pool, row_slot, s)
+        else:
+            lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
 
     def step():
         for s in range(sites):
-            lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
+            launch(s)
 
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
@@ -309,7 +357,7 @@ def main():
             flush.zero_()  # same stream: evicts L2 and covers the host launch latency
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            lsg.sgmv(ys[i], xs[i], pool, seg_starts, seg_slot, i)
+            launch(i)
             e1.record(stream)
         torch.cuda.synchronize()
         lat.append(e0.elapsed_time(e1) * 1e3)
@@ -333,7 +381,7 @@ def main():
         def e2e_step():
             for s in range(sites):
                 xs[s].copy_(hx[s], non_blocking=True)
-                lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
+                launch(s)
                 hy[s].copy_(ys[s], non_blocking=True)
 
         with torch.cuda.stream(stream):
@@ -379,6 +427,7 @@ def main():
                    "batch_per_gpu": batch, "global_batch": batch * world, "segments": nseg,
                    "popularity": a.popularity, "step": f"{sites} fused SGMV launches (7 sites x 32 layers), CUDA graph",
                    "parallelism": f"request-partitioned x{world} (no collective)",
+                   "kernel": a.kernel, "pool_slots": nslots, "preset": a.preset or None,
                    "l2": "inputs larger than L2: weights rotate over a "
                          f"{pool.a.numel() * 2 * 2 / 2**30:.2f} GiB pool, x/y over {2 * xs.numel() * 2 / 2**20:.0f} MiB per step",
                    "pdl": bool(a.pdl), "launch": info},

@@ -27,6 +27,7 @@ struct Plan {
   int mode = kFused;
   int red_all = 0;
   int alias_ab = 0;
+  int tile_scan = 0;
 };
 
 // Set by the API layer; read at launch.
@@ -39,6 +40,8 @@ int launch_fast_fused(int dtype, int rank, const FastParams& p, const Plan& pl, 
 int launch_fast_shrink(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
 int launch_fast_expand(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
 int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st);
+struct TcParams;
+int launch_tc(int dtype, int rank, const TcParams& p, int cluster, int tiles, cudaStream_t st);
 
 template <typename K>
 cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cudaStream_t st,

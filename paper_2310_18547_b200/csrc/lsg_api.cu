@@ -11,11 +11,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <string>
 
 #include "../../include/lsg_sgmv.h"
 #include "segment_builder.cuh"
+#include <cuda.h>
+
 #include "launch.cuh"
+#include "sgmv_tc.cuh"
 
 namespace lsg {
 
@@ -38,6 +42,24 @@ std::atomic<int> g_opt_force_cluster{0};
 std::atomic<int> g_opt_force_generic{0};
 std::atomic<int> g_opt_force_tile_rows{0};
 std::atomic<int> g_opt_no_alias{0};
+std::atomic<int> g_opt_no_tile_scan{0};
+std::atomic<int> g_opt_no_tc{0};
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
 unsigned long long* g_trace = nullptr;
 int g_trace_ctas = 0;
 
@@ -98,6 +120,13 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   if (kernel == kKBgmv) {
     pl.row_splits = 1;
     pl.clusters = s_n;
+  } else if (pl.mt > 1 && !(g_opt_no_tile_scan.load())) {
+    // one cluster per row tile, mapped on the device; sum_i ceil(len_i/MT) is
+    // at most (s_n + n_seg*(MT-1))/MT, and never more than s_n
+    pl.tile_scan = 1;
+    pl.row_splits = 1;
+    const int64_t bound = (static_cast<int64_t>(s_n) + static_cast<int64_t>(n_seg) * (pl.mt - 1)) / pl.mt;
+    pl.clusters = static_cast<int>(std::min<int64_t>(bound, s_n));
   } else {
     const int tiles_per_seg = (s_n + pl.mt * n_seg - 1) / (pl.mt * n_seg);
     pl.row_splits = std::max(1, tiles_per_seg);
@@ -110,22 +139,29 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   // Single-tile clusters (every segment one tile) keep only A resident ahead of
   // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
   // (s_n == n_seg: every segment is one row, so every cluster has exactly one tile)
-  pl.alias_ab = pl.mode == kFused && (kernel == kKBgmv || s_n == n_seg) && !(g_opt_no_alias.load()) ? 1 : 0;
+  pl.alias_ab =
+      pl.mode == kFused && (kernel == kKBgmv || s_n == n_seg || pl.tile_scan) && !(g_opt_no_alias.load()) ? 1 : 0;
   auto smem_for = [&](int c) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
     return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), pl.alias_ab).total);
   };
-  // Split-K cluster size: the smallest C whose CTA fits next to a CTA of the
-  // following launch on the same SM (2 x ~113 KB), so programmatic dependent
-  // launches overlap; then grow C until the grid covers every SM once.
-  const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::min(nq, ncvt));
-  int c_full = 1;
-  while (c_full < kMaxCluster && smem_for(c_full) > kSmemBudget) ++c_full;
-  int c = 1;
-  while (c < kMaxCluster && smem_for(c) > kCoresidentSmem) ++c;
+  // Split-K cluster size.  Candidates divide the chunk / column-group counts
+  // (every CTA gets the same share).  Take the smallest candidate whose CTA
+  // leaves room for the next launch's CTAs on the same SM (programmatic
+  // dependent launches then overlap) and whose grid covers every SM; else the
+  // largest candidate that fits at all.
+  const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::gcd(nq, ncvt));
+  const int est_clusters = pl.tile_scan ? std::max((s_n + pl.mt - 1) / pl.mt, n_seg) : pl.clusters;
   const int sms = num_sms();
-  while (c < kMaxCluster && c < span && pl.clusters * c < sms) ++c;
-  c = std::max(c, c_full);
+  int c = 0, c_fit = 0;
+  for (int cand = 1; cand <= kMaxCluster; ++cand) {
+    if (span % cand != 0 && cand != kMaxCluster) continue;
+    const int sm = smem_for(cand);
+    if (sm > kSmemBudget) continue;
+    c_fit = cand;  // largest candidate that fits so far
+    if (c == 0 && sm <= kCoresidentSmem && static_cast<int64_t>(est_clusters) * cand >= sms) c = cand;
+  }
+  if (c == 0) c = c_fit > 0 ? c_fit : kMaxCluster;
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);
@@ -184,6 +220,43 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
     return launch_generic(tbl->dtype, pl.mode, g, s_n, pl.smem, cs);
   }
 
+  // Long segments (>= kTcMinRows rows) of a fused launch go to the tensor-core
+  // kernel; the CUDA-core kernel then skips them.
+  int skip_long = 0;
+  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= kTcMinRows && (tbl->rank == 16 || tbl->rank == 32) &&
+      tbl->h_in % kTcKC == 0 && tbl->h_out == tbl->h_in && tbl->h_in / kTcKC >= 2 && tbl->h_in / kTcKC <= 16 &&
+      aligned16(x) && aligned16(y) && ldx % 8 == 0 && ldy % 8 == 0 && encode_tiled_fn() != nullptr) {
+    TcParams tp{};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_in), static_cast<cuuint64_t>(s_n)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcKB), static_cast<cuuint32_t>(kTcM)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult cr = encode_tiled_fn()(
+        &tp.tmap_x, tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+        const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr == CUDA_SUCCESS) {
+      tp.y = y;
+      tp.a_ptr = tbl->a_ptr;
+      tp.b_ptr = tbl->b_ptr;
+      tp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+      tp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+      tp.ldy = ldy;
+      tp.seg_starts = seg_starts;
+      tp.seg_slot = seg_slot;
+      tp.n_seg = n_seg;
+      tp.s_n = s_n;
+      tp.num_slots = tbl->num_slots;
+      tp.h_in = tbl->h_in;
+      tp.h_out = tbl->h_out;
+      // tiles of long segments: sum ceil(len/128) over len >= 128 is at most s_n/64
+      const int tiles = std::max(1, s_n / (kTcM / 2));
+      const int st_tc = launch_tc(tbl->dtype, tbl->rank, tp, tbl->h_in / kTcKC, tiles, cs);
+      if (st_tc != LSG_OK) return st_tc;
+      skip_long = kTcMinRows;
+    }
+  }
+
   FastParams p{};
   p.y = y;
   p.x = x;
@@ -210,6 +283,8 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.ncv_max = pl.ncv_max;
   p.red_all = pl.red_all;
   p.alias_ab = pl.alias_ab;
+  p.tile_scan = pl.tile_scan;
+  p.skip_long = skip_long;
   p.trace = g_trace;
   p.trace_ctas = g_trace_ctas;
   static const int exp_flags = [] {
@@ -279,6 +354,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       g_opt_force_tile_rows = value;
       return LSG_OK;
     case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_NO_TENSOR_CORES: g_opt_no_tc = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -290,6 +366,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_FORCE_GENERIC: return g_opt_force_generic.load();
     case LSG_OPT_FORCE_TILE_ROWS: return g_opt_force_tile_rows.load();
     case LSG_OPT_NO_L2_STAGING: return g_opt_no_alias.load();
+    case LSG_OPT_NO_TENSOR_CORES: return g_opt_no_tc.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -68,6 +68,8 @@ struct FastParams {
   int32_t trace_ctas;
   int32_t exp_flags;  // LSG_EXP experiment bits (profiling only; 0 in production)
   int32_t alias_ab;   // 1: single-tile clusters; B is prefetched into L2 and later loaded over A's smem
+  int32_t tile_scan;  // 1: cluster blockIdx.y = global tile index, mapped to (segment, tile) on device
+  int32_t skip_long;  // >0: segments with at least this many rows belong to the tensor-core kernel
 };
 
 // Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
@@ -182,6 +184,47 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     seg_end = row + 1;
     first_tile = 0;
     tile_step = 1;
+  } else if (p.tile_scan) {
+    // Tile t of the launch: walk the segments' tile counts ceil(len/MT) with a
+    // warp prefix sum (32 segments per step) until t falls inside one.
+    __shared__ int s_seg, s_tile;
+    if (warp == 0) {
+      const int t = blockIdx.y;
+      int base = 0, seg = -1, tin = 0;
+      for (int c0 = 0; c0 < p.n_seg && seg < 0; c0 += 32) {
+        const int sg = c0 + lane;
+        int nt = 0;
+        if (sg < p.n_seg) {
+          const int len = p.seg_starts[sg + 1] - p.seg_starts[sg];
+          nt = (p.skip_long > 0 && len >= p.skip_long) ? 0 : (len + MT - 1) / MT;
+        }
+        int incl = nt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += v;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
+        if (hit) {
+          const int l = __ffs(hit) - 1;
+          seg = c0 + l;
+          tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) {
+        s_seg = seg;
+        s_tile = tin;
+      }
+    }
+    __syncthreads();
+    if (s_seg < 0) return;  // past the last tile (the grid is an upper bound)
+    const int s = s_seg;
+    first_tile = s_tile;
+    tile_step = 1 << 30;  // exactly one tile per cluster
+    seg_begin = p.seg_starts[s];
+    seg_end = p.seg_starts[s + 1];
+    slot = p.seg_slot[s];
   } else {
     const int s = blockIdx.y / p.row_splits;
     if (s >= p.n_seg) return;
@@ -190,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     seg_begin = p.seg_starts[s];
     seg_end = p.seg_starts[s + 1];
     slot = p.seg_slot[s];
+    if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return;  // tensor-core kernel's
   }
   const int ntiles = (seg_end - seg_begin + MT - 1) / MT;
   if (first_tile >= ntiles) return;

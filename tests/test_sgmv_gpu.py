@@ -34,7 +34,8 @@ def lsg():
 @pytest.fixture(autouse=True)
 def _reset_options(lsg):
     yield
-    for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL):
+    for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
+                lsg.LSG_OPT_NO_TENSOR_CORES):
         lsg.set_option(opt, 0)
 
 
@@ -182,6 +183,45 @@ def test_mixed_prefill_plus_decodes(lsg, prefill):
     x, A, B = random_problem(4096, 4096, 16, bounds, prefill)
     p = Problem(lsg, x, A, B, bounds, torch.float16)
     err = row_norm_err(p.run().double().cpu().numpy(), p.reference())
+    assert err <= tol(torch.float16), err
+
+
+# ---------------------------------------------------------------------------------
+# Long segments: the tcgen05 path (segments >= 128 rows, r in {16, 32}, h % 512 == 0)
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", [(4096, 16), (4096, 32), (5120, 16), (8192, 32), (1024, 16)])
+@pytest.mark.parametrize("lens", [(128,), (129, 3, 1, 255), (1, 700, 5, 2048, 1, 1)])
+def test_long_segments_tensor_core_path(lsg, dtype, shape, lens):
+    h, r = shape
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(h, h, r, bounds, 5 + len(lens))
+    y0 = oracle().rng(123).fill_pm1(int(bounds[-1]) * h).reshape(-1, h)
+    p = Problem(lsg, x, A, B, bounds, dtype, y0=y0)
+    got = p.run()
+    err = row_norm_err(got.double().cpu().numpy(), p.reference())
+    assert err <= tol(dtype), err
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 1)
+    try:
+        cc = p.run()
+    finally:
+        lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 0)
+    # short segments take the CUDA-core kernel in both runs: bit-identical there
+    for s, n in enumerate(lens):
+        a, b = int(bounds[s]), int(bounds[s + 1])
+        if n < 128:
+            assert torch.equal(got[a:b], cc[a:b]), s
+    assert torch.equal(p.run(), got)  # run-to-run deterministic
+
+
+def test_long_segment_no_adapter_slot_untouched(lsg):
+    bounds = np.array([0, 300, 301, 600], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 31)
+    y0 = oracle().rng(7).fill_pm1(600 * 4096).reshape(600, 4096)
+    p = Problem(lsg, x, A, B, bounds, torch.float16, slots=[0, 1, -1], num_slots=2, y0=y0)
+    got = p.run()
+    assert torch.equal(got[301:], p.y0[301:])
+    err = row_norm_err(got.double().cpu().numpy(), p.reference())
     assert err <= tol(torch.float16), err
 
 
