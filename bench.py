@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cluster", type=int, default=0, help="force the split-K cluster size (0 = library heuristic)")
     ap.add_argument("--tile-rows", type=int, default=0, help="force rows per tile, 1 or 8 (0 = heuristic)")
     ap.add_argument("--no-l2-staging", action="store_true", help="keep B resident from kernel entry")
+    ap.add_argument("--no-tc", action="store_true", help="long segments stay on the CUDA-core kernel")
     ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
                     help="sgmv: segmented launch; bgmv: per-row adapter slots (decode BGMV)")
     ap.add_argument("--slots", type=int, default=0, help="adapter-pool slots (0 = one per segment)")
@@ -78,9 +79,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also print per-(popularity,batch) lines to stderr")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graph, no extras)")
+    pre, _ = ap.parse_known_args()
+    ap.set_defaults(**PRESETS.get(pre.preset, {}))  # a preset sets defaults; explicit flags still win
     a = ap.parse_args()
-    for k, v in PRESETS.get(a.preset, {}).items():
-        setattr(a, k, v)
     if a.prefill:
         a.segments = ",".join([str(a.prefill)] + ["1"] * 31)
     if a.segments:
@@ -275,6 +276,7 @@ def main():
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, int(a.no_l2_staging))
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
     bounds = bounds_for(a)
     nseg = len(bounds) - 1

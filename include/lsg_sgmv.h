@@ -93,6 +93,20 @@ int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
              const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
              int32_t total_rows, int32_t layer, lsg_stream_t stream);
 
+/* Fused call with a caller-owned workspace (device memory, 16-byte aligned).
+ * Segments of >= 128 rows take the tensor-core path, which keeps v (fp32) for
+ * their rows in the workspace; lsg_sgmv_workspace_size() gives the bytes needed
+ * (0 when the shape never uses it).  With a NULL / too small workspace those
+ * segments stay on the CUDA-core kernel (same results to within the stated
+ * tolerance).  lsg_sgmv() itself uses a library-owned workspace, grown outside
+ * stream capture; concurrent lsg_sgmv() calls on different streams should use
+ * lsg_sgmv_ws() with their own workspaces. */
+size_t lsg_sgmv_workspace_size(const lsg_weight_table* tbl, int32_t total_rows);
+int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                int32_t total_rows, int32_t layer, void* workspace, size_t workspace_bytes,
+                lsg_stream_t stream);
+
 /* Shrink only: v[s_n, rank] (fp32, row stride rank) = x . A per segment (overwrite). */
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,
                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
@@ -161,11 +175,13 @@ int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t 
                      int32_t kernel /* 0 fused, 1 shrink, 2 expand, 3 bgmv */,
                      lsg_launch_info* info);
 
-/* Phase tracing (profiling aid, off by default): when installed, thread 0 of
- * every fast-path CTA (up to max_ctas, CTA index = blockIdx.y * C + rank) writes
- * 16 u64 to device_buffer: clock64() at the kernel's phase boundaries in slots
- * 0..11, %globaltimer at entry in slot 14 and the SM id in slot 15.  Pass
- * (NULL, 0) to turn it off.  See scripts/trace_phases.py. */
+/* Phase tracing (profiling aid, off by default).  device_buffer holds
+ * 2 * max_ctas * 16 u64.  Thread 0 of every CUDA-core fast-path CTA (up to
+ * max_ctas, CTA index = blockIdx.y * C + rank) writes entries [0, max_ctas):
+ * clock64() at the kernel's phase boundaries in slots 0..13, %globaltimer at
+ * entry in slot 14 and the SM id in slot 15.  Tensor-core CTAs write entries
+ * [max_ctas, 2 * max_ctas): %globaltimer at their phase boundaries.  Pass
+ * (NULL, 0) to turn it off.  See scripts/trace_phases.py, scripts/trace_tc.py. */
 int lsg_set_trace(unsigned long long* device_buffer, int32_t max_ctas);
 
 const char* lsg_status_string(int status);

@@ -20,7 +20,7 @@ KERNEL_FUSED, KERNEL_SHRINK, KERNEL_EXPAND, KERNEL_BGMV = 0, 1, 2, 3
 
 # Every symbol include/lsg_sgmv.h declares (checked by tests/test_abi.py).
 EXPORTED = (
-    "lsg_sgmv", "lsg_sgmv_shrink", "lsg_sgmv_expand", "lsg_bgmv",
+    "lsg_sgmv", "lsg_sgmv_ws", "lsg_sgmv_workspace_size", "lsg_sgmv_shrink", "lsg_sgmv_expand", "lsg_bgmv",
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
     "lsg_last_error", "lsg_version", "lsg_set_trace",
@@ -68,6 +68,9 @@ def lib() -> C.CDLL:
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         tp = C.POINTER(WeightTable)
         L.lsg_sgmv.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp]
+        L.lsg_sgmv_ws.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
+        L.lsg_sgmv_workspace_size.argtypes = [tp, i32]
+        L.lsg_sgmv_workspace_size.restype = C.c_size_t
         L.lsg_sgmv_shrink.argtypes = [vp, vp, i64, tp, vp, vp, i32, i32, i32, vp]
         L.lsg_sgmv_expand.argtypes = [vp, i64, vp, tp, vp, vp, i32, i32, i32, vp]
         L.lsg_bgmv.argtypes = [vp, i64, vp, i64, tp, vp, i32, i32, vp]

@@ -1,4 +1,4 @@
-// inst_tc.cu -- sm_100a instantiations of the tensor-core SGMV kernel (K5) and its launcher.
+// inst_tc.cu -- sm_100a instantiations of the tensor-core SGMV kernels (K5) and their launchers.
 #include <cuda.h>
 
 #include "launch.cuh"
@@ -7,28 +7,62 @@
 namespace lsg {
 
 template <typename T, int R>
-static int launch_tc_inst(const TcParams& p, int cluster, int tiles, cudaStream_t st) {
-  auto kern = sgmv_tc_kernel<T, R>;
+static int launch_tc_shrink_inst(const TcShrinkParams& p, int nq, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_shrink_kernel<T, R>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLayout<R>::kTotal + 1024);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc smem)");
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc shrink smem)");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc cluster)");
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc shrink cluster)");
     configured = true;
   }
-  const dim3 grid(static_cast<unsigned>(cluster), static_cast<unsigned>(tiles), 1);
-  cudaError_t e = launch_ex(kern, grid, dim3(kTcThreads), static_cast<int>(TcLayout<R>::kTotal + 1024), cluster, st, &p);
-  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_kernel launch");
+  const dim3 grid(static_cast<unsigned>(nq), static_cast<unsigned>(tiles), 1);
+  const int smem = static_cast<int>(tc_shrink_smem(R, p.kcs));
+  const cudaError_t e = launch_ex(kern, grid, dim3(kTcThreads), smem, nq, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_shrink_kernel launch");
 }
 
-int launch_tc(int dtype, int rank, const TcParams& p, int cluster, int tiles, cudaStream_t st) {
-  if (dtype == LSG_F16) {
-    if (rank == 16) return launch_tc_inst<__half, 16>(p, cluster, tiles, st);
-    return launch_tc_inst<__half, 32>(p, cluster, tiles, st);
+template <typename T, int R>
+static int launch_tc_expand_inst(const TcExpandParams& p, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_expand_kernel<T, R>;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcExpandLayout<R>::kTotal);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc expand smem)");
+    configured = true;
   }
-  if (rank == 16) return launch_tc_inst<__nv_bfloat16, 16>(p, cluster, tiles, st);
-  return launch_tc_inst<__nv_bfloat16, 32>(p, cluster, tiles, st);
+  const dim3 grid(static_cast<unsigned>(p.h_out / kTcNT), static_cast<unsigned>(tiles), 1);
+  const cudaError_t e =
+      launch_ex(kern, grid, dim3(kTcThreads), static_cast<int>(TcExpandLayout<R>::kTotal), 0, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_expand_kernel launch");
+}
+
+int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int tiles, cudaStream_t st) {
+#define LSG_TC_R(T)                                                                   \
+  switch (rank) {                                                                     \
+    case 16: return launch_tc_shrink_inst<T, 16>(p, nq, tiles, st);                   \
+    case 32: return launch_tc_shrink_inst<T, 32>(p, nq, tiles, st);                   \
+    case 64: return launch_tc_shrink_inst<T, 64>(p, nq, tiles, st);                   \
+    default: return fail(LSG_EUNSUPPORTED, "tensor-core shrink: rank not in {16,32,64}"); \
+  }
+  if (dtype == LSG_F16) LSG_TC_R(__half)
+  LSG_TC_R(__nv_bfloat16)
+#undef LSG_TC_R
+}
+
+int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st) {
+#define LSG_TC_R(T)                                                               \
+  switch (rank) {                                                                 \
+    case 16: return launch_tc_expand_inst<T, 16>(p, tiles, st);                   \
+    case 32: return launch_tc_expand_inst<T, 32>(p, tiles, st);                   \
+    case 64: return launch_tc_expand_inst<T, 64>(p, tiles, st);                   \
+    default: return fail(LSG_EUNSUPPORTED, "tensor-core expand: rank not in {16,32,64}"); \
+  }
+  if (dtype == LSG_F16) LSG_TC_R(__half)
+  LSG_TC_R(__nv_bfloat16)
+#undef LSG_TC_R
 }
 
 }  // namespace lsg

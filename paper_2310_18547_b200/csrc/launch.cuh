@@ -4,6 +4,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <string>
 
 #include "../../include/lsg_sgmv.h"
@@ -40,8 +42,10 @@ int launch_fast_fused(int dtype, int rank, const FastParams& p, const Plan& pl, 
 int launch_fast_shrink(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
 int launch_fast_expand(int dtype, int rank, const FastParams& p, const Plan& pl, cudaStream_t st);
 int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st);
-struct TcParams;
-int launch_tc(int dtype, int rank, const TcParams& p, int cluster, int tiles, cudaStream_t st);
+struct TcShrinkParams;
+struct TcExpandParams;
+int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int tiles, cudaStream_t st);
+int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st);
 
 template <typename K>
 cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cudaStream_t st,
@@ -82,7 +86,25 @@ int launch_fast_inst(const FastParams& p, const Plan& pl, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(non-portable cluster)");
     configured = true;
   }
-  const dim3 grid(static_cast<unsigned>(pl.cluster), static_cast<unsigned>(pl.clusters), 1);
+  int clusters = pl.clusters;
+  if (pl.tile_scan) {
+    // Tile-scan grids are an upper bound on the real tile count; cap them at
+    // twice the co-resident cluster count (clusters loop over further tiles).
+    static int sms = 0, occ_smem = -1, occ = 1;
+    if (sms == 0) {
+      int dev = 0;
+      sms = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (occ_smem != pl.smem) {
+      int n = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, pl.smem) != cudaSuccess || n < 1) n = 1;
+      occ = n;
+      occ_smem = pl.smem;
+    }
+    clusters = std::min(clusters, std::max(1, 2 * sms * occ / pl.cluster));
+  }
+  const dim3 grid(static_cast<unsigned>(pl.cluster), static_cast<unsigned>(clusters), 1);
   cudaError_t e = launch_ex(kern, grid, dim3(kThreads), pl.smem, pl.cluster, st, &p);
   if (e != cudaSuccess) return cuda_fail(e, "sgmv_fast_kernel launch");
   return LSG_OK;

@@ -14,11 +14,13 @@
 #include <numeric>
 #include <string>
 
-#include "../../include/lsg_sgmv.h"
-#include "segment_builder.cuh"
 #include <cuda.h>
 
+#include <mutex>
+
+#include "../../include/lsg_sgmv.h"
 #include "launch.cuh"
+#include "segment_builder.cuh"
 #include "sgmv_tc.cuh"
 
 namespace lsg {
@@ -66,6 +68,118 @@ int g_trace_ctas = 0;
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// ---- tensor-core path (K5) for segments of >= kTcMinRows rows ----------------------
+// K chunks of the shrink cluster: the largest nq in {16, 8, 4, 2} that splits h_in
+// into whole 64-column boxes with the CTA's shared memory in budget.
+int tc_nq(const lsg_weight_table* t) {
+  if (t->rank != 16 && t->rank != 32 && t->rank != 64) return 0;
+  if (t->h_out % kTcNT != 0 || t->a_layer_stride % 8 != 0 || t->b_layer_stride % 8 != 0) return 0;
+  for (int nq = 16; nq >= 2; nq /= 2) {
+    if (t->h_in % (nq * kTcKB) != 0) continue;
+    if (tc_shrink_smem(t->rank, t->h_in / nq) <= static_cast<uint32_t>(kSmemBudget)) return nq;
+  }
+  return 0;
+}
+
+size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
+  return tc_nq(t) > 0 && s_n >= kTcMinRows ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
+}
+
+// Library-owned workspace of lsg_sgmv(): grown (never during stream capture)
+std::mutex g_ws_mu;
+void* g_ws = nullptr;
+size_t g_ws_bytes = 0;
+
+void* library_workspace(size_t need, cudaStream_t cs) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if (g_ws_bytes >= need) return g_ws;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(cs, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return nullptr;
+  size_t bytes = std::max<size_t>(need, static_cast<size_t>(1) << 20);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (g_ws != nullptr) {
+    cudaDeviceSynchronize();  // the old buffer may still be read by queued launches
+    cudaFree(g_ws);
+  }
+  g_ws = p;
+  g_ws_bytes = bytes;
+  return g_ws;
+}
+
+bool encode_rows_map(CUtensorMap* m, int dtype, const void* base, int cols, int rows, int64_t ld) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcKB), static_cast<cuuint32_t>(kTcM)};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode_tiled_fn()(m, dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Parameters of the shrink + expand tensor-core kernels over the long segments;
+// false when this call cannot use them (shape, alignment, workspace).
+struct LongPlan {
+  TcShrinkParams sp;
+  TcExpandParams ep;
+  int nq = 0, tiles = 0;
+};
+bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, int64_t ldx,
+                           const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
+                           int s_n, int layer, void* ws, size_t ws_bytes) {
+  const int nq = tc_nq(tbl);
+  if (nq == 0 || s_n < kTcMinRows || ws == nullptr || ws_bytes < tc_workspace_bytes(tbl, s_n) || !aligned16(ws))
+    return false;
+  if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
+  TcShrinkParams& sp = lp.sp;
+  TcExpandParams& ep = lp.ep;
+  sp = TcShrinkParams{};
+  ep = TcExpandParams{};
+  if (!encode_rows_map(&sp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx) ||
+      !encode_rows_map(&ep.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
+    return false;
+  // tiles of long segments: sum ceil(len/128) over len >= 128 is at most s_n/64
+  const int tiles = std::max(1, s_n / (kTcM / 2));
+  lp.nq = nq;
+  lp.tiles = tiles;
+  sp.v = static_cast<float*>(ws);
+  sp.a_ptr = tbl->a_ptr;
+  sp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+  sp.seg_starts = seg_starts;
+  sp.seg_slot = seg_slot;
+  sp.n_seg = n_seg;
+  sp.s_n = s_n;
+  sp.num_slots = tbl->num_slots;
+  sp.h_in = tbl->h_in;
+  sp.kcs = tbl->h_in / nq;
+  sp.trace = g_trace;
+  sp.trace_ctas = g_trace_ctas;
+  ep.y = y;
+  ep.ldy = ldy;
+  ep.v = static_cast<const float*>(ws);
+  ep.b_ptr = tbl->b_ptr;
+  ep.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+  ep.seg_starts = seg_starts;
+  ep.seg_slot = seg_slot;
+  ep.n_seg = n_seg;
+  ep.s_n = s_n;
+  ep.num_slots = tbl->num_slots;
+  ep.h_out = tbl->h_out;
+  ep.trace = g_trace;
+  ep.trace_ctas = g_trace_ctas;
+  return true;
+}
+
+int launch_long_segments(const LongPlan& lp, int dtype, int rank, cudaStream_t cs) {
+  const int st = launch_tc_shrink(dtype, rank, lp.sp, lp.nq, lp.tiles, cs);
+  if (st != LSG_OK) return st;
+  return launch_tc_expand(dtype, rank, lp.ep, lp.tiles, cs);
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -101,7 +215,7 @@ bool fast_shape_ok(const lsg_weight_table* t) {
 }
 
 // Choose tile rows, row splits and the split-K cluster size for a launch.
-Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast) {
+Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast, bool long_on_tc = false) {
   Plan pl;
   pl.mode = kernel == kKShrink ? kShrink : kernel == kKExpand ? kExpand : kFused;
   if (!fast || g_opt_force_generic.load()) {
@@ -146,22 +260,25 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), pl.alias_ab).total);
   };
   // Split-K cluster size.  Candidates divide the chunk / column-group counts
-  // (every CTA gets the same share).  Take the smallest candidate whose CTA
-  // leaves room for the next launch's CTAs on the same SM (programmatic
-  // dependent launches then overlap) and whose grid covers every SM; else the
-  // largest candidate that fits at all.
+  // (every CTA gets the same share).  Measured on B200 (profiles/README.md):
+  // a launch runs best with about 128-256 CTAs in all, and clusters of 8-16
+  // schedule poorly once the grid needs more than one CTA per SM.  So take the
+  // largest candidate whose grid stays within 148 CTAs (C >= 8) or 256 CTAs
+  // (C <= 4; tile-scan launches: 256 for every C); if none does, the smallest
+  // candidate that fits in shared memory.  With the long segments on the tensor
+  // cores, the CUDA-core launch serves short segments only: estimate one
+  // cluster per segment.
   const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::gcd(nq, ncvt));
-  const int est_clusters = pl.tile_scan ? std::max((s_n + pl.mt - 1) / pl.mt, n_seg) : pl.clusters;
-  const int sms = num_sms();
-  int c = 0, c_fit = 0;
+  const int64_t est_clusters = long_on_tc ? n_seg : pl.clusters;
+  int c = 0, c_small = 0;
   for (int cand = 1; cand <= kMaxCluster; ++cand) {
     if (span % cand != 0 && cand != kMaxCluster) continue;
-    const int sm = smem_for(cand);
-    if (sm > kSmemBudget) continue;
-    c_fit = cand;  // largest candidate that fits so far
-    if (c == 0 && sm <= kCoresidentSmem && static_cast<int64_t>(est_clusters) * cand >= sms) c = cand;
+    if (smem_for(cand) > kSmemBudget) continue;
+    if (c_small == 0) c_small = cand;
+    const int64_t limit = (pl.tile_scan || cand <= 4) ? 256 : 148;
+    if (est_clusters * cand <= limit) c = cand;
   }
-  if (c == 0) c = c_fit > 0 ? c_fit : kMaxCluster;
+  if (c == 0) c = c_small > 0 ? c_small : kMaxCluster;
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);
@@ -175,7 +292,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
 // Shared entry for all four SGMV kernels.
 int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_out, const float* v_in,
         const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
-        const int32_t* row_slot, int32_t n_seg, int32_t s_n, int32_t layer, lsg_stream_t stream) {
+        const int32_t* row_slot, int32_t n_seg, int32_t s_n, int32_t layer, lsg_stream_t stream,
+        void* ws = nullptr, size_t ws_bytes = 0, bool library_ws = false) {
   int st = validate_table(tbl);
   if (st != LSG_OK) return st;
   if (s_n < 0) return fail(LSG_EINVAL, "lsg: total_rows must be >= 0");
@@ -193,10 +311,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   bool fast = fast_shape_ok(tbl);
   if (need_x) fast = fast && aligned16(x) && ldx % 8 == 0;
   if (need_y) fast = fast && aligned16(y) && ldy % 8 == 0;
-  const Plan pl = make_plan(tbl, kernel, n_seg, s_n, fast);
+  const Plan pl0 = make_plan(tbl, kernel, n_seg, s_n, fast);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
 
-  if (pl.path == 1) {
+  if (pl0.path == 1) {
+    const Plan& pl = pl0;
     GenericParams g{};
     g.y = y;
     g.x = x;
@@ -221,41 +340,21 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   }
 
   // Long segments (>= kTcMinRows rows) of a fused launch go to the tensor-core
-  // kernel; the CUDA-core kernel then skips them.
+  // kernels; the CUDA-core kernel then skips them.
+  // Launch order: CUDA-core kernel (short segments), then the tensor-core shrink
+  // and expand.  The tensor-core shrink triggers its dependents only after its
+  // own PDL wait, so the expand may stage y_old before waiting for v.
   int skip_long = 0;
-  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= kTcMinRows && (tbl->rank == 16 || tbl->rank == 32) &&
-      tbl->h_in % kTcKC == 0 && tbl->h_out == tbl->h_in && tbl->h_in / kTcKC >= 2 && tbl->h_in / kTcKC <= 16 &&
-      aligned16(x) && aligned16(y) && ldx % 8 == 0 && ldy % 8 == 0 && encode_tiled_fn() != nullptr) {
-    TcParams tp{};
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_in), static_cast<cuuint64_t>(s_n)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcKB), static_cast<cuuint32_t>(kTcM)};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult cr = encode_tiled_fn()(
-        &tp.tmap_x, tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-        const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr == CUDA_SUCCESS) {
-      tp.y = y;
-      tp.a_ptr = tbl->a_ptr;
-      tp.b_ptr = tbl->b_ptr;
-      tp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
-      tp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
-      tp.ldy = ldy;
-      tp.seg_starts = seg_starts;
-      tp.seg_slot = seg_slot;
-      tp.n_seg = n_seg;
-      tp.s_n = s_n;
-      tp.num_slots = tbl->num_slots;
-      tp.h_in = tbl->h_in;
-      tp.h_out = tbl->h_out;
-      // tiles of long segments: sum ceil(len/128) over len >= 128 is at most s_n/64
-      const int tiles = std::max(1, s_n / (kTcM / 2));
-      const int st_tc = launch_tc(tbl->dtype, tbl->rank, tp, tbl->h_in / kTcKC, tiles, cs);
-      if (st_tc != LSG_OK) return st_tc;
-      skip_long = kTcMinRows;
+  LongPlan lp;
+  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= kTcMinRows && tc_nq(tbl) > 0) {
+    if (library_ws) {
+      ws_bytes = tc_workspace_bytes(tbl, s_n);
+      ws = library_workspace(ws_bytes, cs);
     }
+    if (prepare_long_segments(lp, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, ws, ws_bytes))
+      skip_long = kTcMinRows;
   }
+  const Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
 
   FastParams p{};
   p.y = y;
@@ -293,10 +392,12 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   }();
   p.exp_flags = exp_flags;
   switch (pl.mode) {
-    case kFused: return launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs);
-    case kShrink: return launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs);
-    default: return launch_fast_expand(tbl->dtype, tbl->rank, p, pl, cs);
+    case kFused: st = launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs); break;
+    case kShrink: st = launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs); break;
+    default: st = launch_fast_expand(tbl->dtype, tbl->rank, p, pl, cs); break;
   }
+  if (st != LSG_OK || !skip_long) return st;
+  return launch_long_segments(lp, tbl->dtype, tbl->rank, cs);
 }
 
 }  // namespace
@@ -318,7 +419,20 @@ int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
              const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
              int32_t total_rows, int32_t layer, lsg_stream_t stream) {
   return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
-             num_segments, total_rows, layer, stream);
+             num_segments, total_rows, layer, stream, nullptr, 0, true);
+}
+
+size_t lsg_sgmv_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
+  if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
+  return tc_workspace_bytes(tbl, total_rows);
+}
+
+int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
+                int32_t total_rows, int32_t layer, void* workspace, size_t workspace_bytes,
+                lsg_stream_t stream) {
+  return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
+             num_segments, total_rows, layer, stream, workspace, workspace_bytes, false);
 }
 
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,

@@ -174,327 +174,356 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
     fence_mbar_init();
   }
 
-  // ---- which rows / adapter this cluster serves (uniform across the cluster) ----
-  int slot, seg_begin, seg_end, first_tile, tile_step;
-  if (p.row_slot != nullptr) {
-    const int row = blockIdx.y;
-    if (row >= p.s_n) return;
-    slot = p.row_slot[row];
-    seg_begin = row;
-    seg_end = row + 1;
-    first_tile = 0;
-    tile_step = 1;
-  } else if (p.tile_scan) {
-    // Tile t of the launch: walk the segments' tile counts ceil(len/MT) with a
-    // warp prefix sum (32 segments per step) until t falls inside one.
-    __shared__ int s_seg, s_tile;
-    if (warp == 0) {
-      const int t = blockIdx.y;
-      int base = 0, seg = -1, tin = 0;
-      for (int c0 = 0; c0 < p.n_seg && seg < 0; c0 += 32) {
-        const int sg = c0 + lane;
-        int nt = 0;
-        if (sg < p.n_seg) {
-          const int len = p.seg_starts[sg + 1] - p.seg_starts[sg];
-          nt = (p.skip_long > 0 && len >= p.skip_long) ? 0 : (len + MT - 1) / MT;
-        }
-        int incl = nt;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += v;
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
-        if (hit) {
-          const int l = __ffs(hit) - 1;
-          seg = c0 + l;
-          tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
-        }
-        base += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (lane == 0) {
-        s_seg = seg;
-        s_tile = tin;
-      }
-    }
-    __syncthreads();
-    if (s_seg < 0) return;  // past the last tile (the grid is an upper bound)
-    const int s = s_seg;
-    first_tile = s_tile;
-    tile_step = 1 << 30;  // exactly one tile per cluster
-    seg_begin = p.seg_starts[s];
-    seg_end = p.seg_starts[s + 1];
-    slot = p.seg_slot[s];
-  } else {
-    const int s = blockIdx.y / p.row_splits;
-    if (s >= p.n_seg) return;
-    first_tile = blockIdx.y - s * p.row_splits;
-    tile_step = p.row_splits;
-    seg_begin = p.seg_starts[s];
-    seg_end = p.seg_starts[s + 1];
-    slot = p.seg_slot[s];
-    if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return;  // tensor-core kernel's
-  }
-  const int ntiles = (seg_end - seg_begin + MT - 1) / MT;
-  if (first_tile >= ntiles) return;
-  if (slot < 0 || slot >= p.num_slots) {  // "no adapter": v = 0, y untouched
-    if (MODE == kShrink && crank == 0) {
-      pdl_wait();
-      for (int t = first_tile; t < ntiles; t += tile_step) {
-        const int r0 = seg_begin + t * MT, rows = min(MT, seg_end - r0);
-        for (int i = tid; i < rows * R; i += kThreads) p.v_out[static_cast<int64_t>(r0) * R + i] = 0.f;
-      }
-    }
-    return;
-  }
-
-  LSG_TRACE(1);
-  const int q0 = split_lo(crank, p.nq, C), nqc = split_lo(crank + 1, p.nq, C) - q0;
-  const int cv0 = split_lo(crank, p.ncvt, C), ncv = split_lo(crank + 1, p.ncvt, C) - cv0;
-  const int ndl = nqc * KW;  // this CTA's slice of h_in (x_sm row stride)
-  const int npieces = (p.exp_flags & 2) ? min(1, nqc) : min(kPieces, nqc);
-  const int slice_max = slice_floats(MT, R, C);
-
-  __syncthreads();                 // barrier inits visible to this CTA
-  if constexpr (kSh) cluster_arrive_relaxed();  // ... and (fence.mbarrier_init) to the cluster; waited on before the first push
-
-  // Adapter weights: every byte this CTA needs, requested at entry (before the
-  // PDL wait, so they stream while the previous kernel drains).  A arrives in
-  // kPieces chunk-aligned pieces with their own barriers so the shrink starts
-  // on the first piece; B follows on one barrier.  Warp 0 issues A, warp 1
-  // issues B (one row per lane) -- the two pointer loads and the issue run in
-  // parallel.
-  const int a_warp = (p.exp_flags & 4) ? 1 : 0, b_warp = (p.exp_flags & 4) ? 0 : (kSh ? 1 : 0);
-  if (kSh && warp == a_warp && nqc > 0) {
-    const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
-    if (lane < npieces) {
-      const int c0 = (lane * nqc) / npieces, c1 = ((lane + 1) * nqc) / npieces;
-      const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
-      mbar_arrive_expect_tx(&bars[lane], bytes);
-      if (p.exp_flags & 1)
-        bulk_g2s(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane]);
-      else
-        bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane], l2_evict_first_policy());
-    }
-  }
-  const T* Bslice = nullptr;
-  if (kEx && warp == b_warp && ncv > 0) {
-    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
-    Bslice = B;
-  }
-  if (kEx && warp == b_warp && ncv > 0 && alias_ab) {
-    // B's smem is still holding A: only warm L2 now, load after the shrink
-    for (int k = lane; k < R; k += 32)
-      bulk_prefetch_l2(Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16));
-  } else if (kEx && warp == b_warp && ncv > 0) {
-    const T* B = Bslice;
-    if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
-    __syncwarp();
-    const uint64_t pol = l2_evict_first_policy();
-    for (int k = lane; k < R; k += 32) {
-      if (p.exp_flags & 1)
-        bulk_g2s(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16), &bars[kBarB]);
-      else
-        bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
-                      &bars[kBarB], pol);
-    }
-  }
-  LSG_TRACE(2);
-  if (p.exp_flags & 8) {  // experiment: weight stream only
-    for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
-    if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
-    if constexpr (kSh) cluster_wait();
-    return;
-  }
-  if (p.exp_flags & 16) {  // experiment: weights + activations, no compute
-    pdl_wait();
-    for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
-    if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
-    if constexpr (kSh) cluster_wait();
-    return;
-  }
-  // x, v and y may be produced by the preceding kernel: wait for it here.
-  pdl_wait();
-  LSG_TRACE(3);
-
-  uint32_t phase = 0;
-  for (int t = first_tile; t < ntiles; t += tile_step, phase ^= 1u) {
-    const int r0 = seg_begin + t * MT;
-    const int rows = min(MT, seg_end - r0);
-    const int no = rows * R;
-    const int o0 = split_lo(crank, no / 4, C) * 4, o1 = split_lo(crank + 1, no / 4, C) * 4;
-    // Activations go through cp.async (LDGSTS), not the TMA queue the weights
-    // occupy, so they land about one memory latency after the wait.
-    if constexpr (kSh) {
-      const int nv = ndl / 8;  // 16-byte vectors per x row slice
-      for (int i = tid; i < rows * nv; i += kThreads) {
-        const int m = i / nv, c = i - m * nv;
-        cp_async16(x_sm + m * ndl + c * 8,
-                   static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW + c * 8);
-      }
-    }
-    cp_async_commit();
-    if constexpr (kEx) {
-      for (int i = tid; i < rows * ncv; i += kThreads) {
-        const int m = i / ncv, c = i - m * ncv;
-        cp_async16(y_sm + m * ncv + c,
-                   static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + c) * 8);
-      }
-    }
-    cp_async_commit();
-    if (kSh && tid == 0) {
-      // bytes this CTA will receive this tile; peers may already be pushing (the
-      // tx-count may go transiently negative; the phase needs this arrive too)
-      mbar_arrive_expect_tx(&bars[kBarRed], static_cast<uint32_t>(p.nq * (red_all ? no : (o1 - o0)) * 4));
-      if (MODE == kFused && !red_all) mbar_arrive_expect_tx(&bars[kBarV], static_cast<uint32_t>(no * 4));
-    }
-
-    if constexpr (MODE == kExpand) {
-      for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
-    } else {
-      cp_async_wait<1>();  // this thread's x vectors
-      __syncthreads();     // everyone's
-      LSG_TRACE(4);
-      if (t == first_tile) cluster_wait();  // every peer's barriers are initialised
-      LSG_TRACE(5);
-      // ---- shrink: per-chunk partials P_q[m, k], pushed to the reducers ------------
-      const int rowoff = lane / VPR, vec = lane % VPR;
-      const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
-      // Work unit = (chunk, row): every warp takes units until none are left.  A
-      // unit's arithmetic depends only on its chunk and row, never on which warp,
-      // CTA or tile size computes it.
-      const int nunits = nqc * rows;
-      for (int u = warp; u < nunits; u += kWarps) {
-        const int ql = u / rows, m = u - ql * rows;
-        int piece = 0;  // wait for the piece holding chunk ql (no-op once it has landed)
-        while (((piece + 1) * nqc) / npieces <= ql) ++piece;
-        mbar_wait(&bars[piece], 0);
-        float acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-        const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
-        const T* xc = x_sm + m * ndl + ql * KW + rowoff;
-#pragma unroll
-        for (int it = 0; it < ITER; ++it) {
-          float a[8];
-          Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
-          const float xm = Cvt<T>::to_f(xc[it * RPI]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
-        }
-#pragma unroll
-        for (int off = VPR; off < 32; off <<= 1)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
-        // Every lane now holds its vec's 8 partial sums P_q[m, vec*8 .. +8).  Push
-        // them into the reducers' shared memory with st.async (async proxy: the
-        // receiver's mbarrier completes on the bytes -- no cluster fence); the
-        // 32/VPR lanes sharing a vec split the 16-byte quads / destinations.
-        const int q = q0 + ql;
-        const int g = lane / VPR;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int o = m * R + vec * 8 + h * 4;
-          if (red_all) {
-            const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
-            for (int dst = (g + h) % RPI; dst < C; dst += RPI) {
-              uint32_t ra, rb;
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
-              st_async_v4(ra, acc[h * 4 + 0], acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3], rb);
-            }
-          } else if (g == h) {
-            const int owner = split_owner(o / 4, no / 4, C);
-            const int jl = o - split_lo(owner, no / 4, C) * 4;
-            st_async_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[h * 4 + 0],
-                        acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3],
-                        mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
+  // ---- work items (uniform across the cluster) ---------------------------------
+  // bgmv / row-split launches: one item per cluster.  Tile-scan launches: the
+  // cluster takes global tiles blockIdx.y, blockIdx.y + gridDim.y, ... (the grid
+  // is capped near the co-resident cluster count, so tiles past the last real
+  // one cost one scan, not one cluster launch).
+  uint32_t phase = 0;   // reduction barriers: flips every tile
+  uint32_t wphase = 0;  // weight barriers: flips every item
+  bool first = true;    // first tile this CTA computes (cluster barrier-init wait)
+  bool first_item = true;
+  for (int item = blockIdx.y;; item += gridDim.y, wphase ^= 1u) {
+    int slot, seg_begin, seg_end, first_tile, tile_step;
+    if (p.row_slot != nullptr) {
+      const int row = item;
+      if (row >= p.s_n) return;
+      slot = p.row_slot[row];
+      seg_begin = row;
+      seg_end = row + 1;
+      first_tile = 0;
+      tile_step = 1;
+    } else if (p.tile_scan) {
+      // Tile t: walk the segments' tile counts ceil(len/MT) with a warp prefix
+      // sum (32 segments per step) until t falls inside one.
+      __shared__ int s_seg, s_tile;
+      __syncthreads();  // previous item's s_seg / s_tile consumed
+      if (warp == 0) {
+        const int t = item;
+        int base = 0, seg = -1, tin = 0;
+        for (int c0 = 0; c0 < p.n_seg && seg < 0; c0 += 32) {
+          const int sg = c0 + lane;
+          int nt = 0;
+          if (sg < p.n_seg) {
+            const int len = p.seg_starts[sg + 1] - p.seg_starts[sg];
+            nt = (p.skip_long > 0 && len >= p.skip_long) ? 0 : (len + MT - 1) / MT;
           }
+          int incl = nt;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
+          if (hit) {
+            const int l = __ffs(hit) - 1;
+            seg = c0 + l;
+            tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
+          }
+          base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) {
+          s_seg = seg;
+          s_tile = tin;
         }
       }
-      LSG_TRACE(12);
-      if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
       __syncthreads();
-      LSG_TRACE(13);
-      if (kEx && alias_ab && warp == b_warp && ncv > 0) {
-        // A is consumed: bring the (L2-warm) B slice into the same shared memory
-        if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
-        __syncwarp();
-        for (int k = lane; k < R; k += 32)
-          bulk_g2s(B_sm + k * ncv, Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
-                   &bars[kBarB]);
+      if (s_seg < 0) return;  // past the last tile
+      // A later item reuses every buffer: the whole cluster finishes the previous one first.
+      if (!first_item) {
+        if constexpr (kSh) cluster_sync();
       }
-      // ---- reduction over chunks, ascending q ------------------------------------
-      LSG_TRACE(6);
-      mbar_wait(&bars[kBarRed], phase);
-      LSG_TRACE(7);
-      if (red_all) {
-        for (int o = tid; o < no; o += kThreads) {
-          float s = 0.f;
-          for (int q = 0; q < p.nq; ++q) s += recv[(q * MT) * R + o];
-          V_sm[o] = s;
+      const int s = s_seg;
+      first_tile = s_tile;
+      tile_step = 1 << 30;  // exactly one tile per item
+      seg_begin = p.seg_starts[s];
+      seg_end = p.seg_starts[s + 1];
+      slot = p.seg_slot[s];
+    } else {
+      const int s = item / p.row_splits;
+      if (s >= p.n_seg) return;
+      first_tile = item - s * p.row_splits;
+      tile_step = p.row_splits;
+      seg_begin = p.seg_starts[s];
+      seg_end = p.seg_starts[s + 1];
+      slot = p.seg_slot[s];
+      if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return;  // tensor-core kernels'
+    }
+    const bool last_item = !p.tile_scan;  // bgmv / row-split: one item per cluster
+    const int ntiles = (seg_end - seg_begin + MT - 1) / MT;
+    if (first_tile >= ntiles) {
+      if (last_item) return;
+      wphase ^= 1u;  // no weights were requested for this item: keep the barrier phase
+      continue;
+    }
+    if (slot < 0 || slot >= p.num_slots) {  // "no adapter": v = 0, y untouched
+      if (MODE == kShrink && crank == 0) {
+        pdl_wait();
+        for (int t = first_tile; t < ntiles; t += tile_step) {
+          const int r0 = seg_begin + t * MT, rows = min(MT, seg_end - r0);
+          for (int i = tid; i < rows * R; i += kThreads) p.v_out[static_cast<int64_t>(r0) * R + i] = 0.f;
         }
-      } else {
-        for (int o = o0 + tid; o < o1; o += kThreads) {
-          float s = 0.f;
-          for (int q = 0; q < p.nq; ++q) s += recv[q * slice_max + (o - o0)];
-          if constexpr (MODE == kShrink) {
-            const int m = o / R;
-            p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
-          } else {
-            const uint32_t local = smem_u32(V_sm + o), lbar = smem_u32(&bars[kBarV]);
-            for (int dst = 0; dst < C; ++dst) {
-              uint32_t ra, rb;
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
-              st_async_f32(ra, s, rb);
-            }
-          }
-        }
-        if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
       }
+      if (last_item) return;
+      wphase ^= 1u;  // no weights were requested for this item: keep the barrier phase
+      continue;
     }
 
-    if constexpr (kEx) {
-      LSG_TRACE(8);
-      cp_async_wait<0>();  // this thread's y vectors
-      __syncthreads();     // V_sm and every y vector visible
-      LSG_TRACE(9);
-      // ---- expand: y[m, n] += sum_k v[m, k] B[k, n] -----------------------------
-      if (ncv > 0) {
-        mbar_wait(&bars[kBarB], 0);
-        LSG_TRACE(10);
+    LSG_TRACE(1);
+    const int q0 = split_lo(crank, p.nq, C), nqc = split_lo(crank + 1, p.nq, C) - q0;
+    const int cv0 = split_lo(crank, p.ncvt, C), ncv = split_lo(crank + 1, p.ncvt, C) - cv0;
+    const int ndl = nqc * KW;  // this CTA's slice of h_in (x_sm row stride)
+    const int npieces = (p.exp_flags & 2) ? min(1, nqc) : min(kPieces, nqc);
+    const int slice_max = slice_floats(MT, R, C);
+
+    if (first) {
+      __syncthreads();                              // barrier inits visible to this CTA
+      if constexpr (kSh) cluster_arrive_relaxed();  // ... and (fence.mbarrier_init) to the cluster
+    } else {
+      fence_proxy_async_smem();  // previous item's generic smem reads before the weight TMA
+    }
+
+    // Adapter weights: every byte this CTA needs, requested before the PDL wait
+    // on the first item (so they stream while the previous kernel drains).  A
+    // arrives in kPieces chunk-aligned pieces with their own barriers so the
+    // shrink starts on the first piece; B follows on one barrier.  Warp 0 issues
+    // A, warp 1 issues B (one row per lane).
+    const int a_warp = (p.exp_flags & 4) ? 1 : 0, b_warp = (p.exp_flags & 4) ? 0 : (kSh ? 1 : 0);
+    if (kSh && warp == a_warp && nqc > 0) {
+      const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
+      if (lane < npieces) {
+        const int c0 = (lane * nqc) / npieces, c1 = ((lane + 1) * nqc) / npieces;
+        const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
+        mbar_arrive_expect_tx(&bars[lane], bytes);
+        if (p.exp_flags & 1)
+          bulk_g2s(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane]);
+        else
+          bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane], l2_evict_first_policy());
+      }
+    }
+    const T* Bslice = nullptr;
+    if (kEx && warp == b_warp && ncv > 0) {
+      const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
+      Bslice = B;
+    }
+    if (kEx && warp == b_warp && ncv > 0 && alias_ab) {
+      // B's smem is still holding A: only warm L2 now, load after the shrink
+      for (int k = lane; k < R; k += 32)
+        bulk_prefetch_l2(Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16));
+    } else if (kEx && warp == b_warp && ncv > 0) {
+      const T* B = Bslice;
+      if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
+      __syncwarp();
+      const uint64_t pol = l2_evict_first_policy();
+      for (int k = lane; k < R; k += 32) {
+        if (p.exp_flags & 1)
+          bulk_g2s(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
+                   &bars[kBarB]);
+        else
+          bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
+                        &bars[kBarB], pol);
+      }
+    }
+    LSG_TRACE(2);
+    if (p.exp_flags & 8) {  // experiment: weight stream only
+      for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
+      if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
+      if constexpr (kSh) cluster_wait();
+      return;
+    }
+    if (p.exp_flags & 16) {  // experiment: weights + activations, no compute
+      pdl_wait();
+      for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
+      if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
+      if constexpr (kSh) cluster_wait();
+      return;
+    }
+    // x, v and y may be produced by the preceding kernel: wait for it here
+    // (returns at once after the first item).
+    pdl_wait();
+    LSG_TRACE(3);
+
+    for (int t = first_tile; t < ntiles; t += tile_step, phase ^= 1u) {
+      const int r0 = seg_begin + t * MT;
+      const int rows = min(MT, seg_end - r0);
+      const int no = rows * R;
+      const int o0 = split_lo(crank, no / 4, C) * 4, o1 = split_lo(crank + 1, no / 4, C) * 4;
+      // Activations go through cp.async (LDGSTS), not the TMA queue the weights
+      // occupy, so they land about one memory latency after the wait.
+      if constexpr (kSh) {
+        const int nv = ndl / 8;  // 16-byte vectors per x row slice
+        for (int i = tid; i < rows * nv; i += kThreads) {
+          const int m = i / nv, c = i - m * nv;
+          cp_async16(x_sm + m * ndl + c * 8,
+                     static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW + c * 8);
+        }
+      }
+      cp_async_commit();
+      if constexpr (kEx) {
         for (int i = tid; i < rows * ncv; i += kThreads) {
-          const int m = i / ncv, cv = i - m * ncv;
+          const int m = i / ncv, c = i - m * ncv;
+          cp_async16(y_sm + m * ncv + c,
+                     static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + c) * 8);
+        }
+      }
+      cp_async_commit();
+      if (kSh && tid == 0) {
+        // bytes this CTA will receive this tile; peers may already be pushing (the
+        // tx-count may go transiently negative; the phase needs this arrive too)
+        mbar_arrive_expect_tx(&bars[kBarRed], static_cast<uint32_t>(p.nq * (red_all ? no : (o1 - o0)) * 4));
+        if (MODE == kFused && !red_all) mbar_arrive_expect_tx(&bars[kBarV], static_cast<uint32_t>(no * 4));
+      }
+
+      if constexpr (MODE == kExpand) {
+        for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
+      } else {
+        cp_async_wait<1>();  // this thread's x vectors
+        __syncthreads();     // everyone's
+        LSG_TRACE(4);
+        if (first) cluster_wait();  // every peer's barriers are initialised
+        first = false;
+        LSG_TRACE(5);
+        // ---- shrink: per-chunk partials P_q[m, k], pushed to the reducers ----------
+        const int rowoff = lane / VPR, vec = lane % VPR;
+        const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
+        // Work unit = (chunk, row): every warp takes units until none are left.  A
+        // unit's arithmetic depends only on its chunk and row, never on which warp,
+        // CTA or tile size computes it.
+        const int nunits = nqc * rows;
+        for (int u = warp; u < nunits; u += kWarps) {
+          const int ql = u / rows, m = u - ql * rows;
+          int piece = 0;  // wait for the piece holding chunk ql (no-op once it has landed)
+          while (((piece + 1) * nqc) / npieces <= ql) ++piece;
+          mbar_wait(&bars[piece], wphase);
           float acc[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+          const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
+          const T* xc = x_sm + m * ndl + ql * KW + rowoff;
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            float b[8];
-            Cvt<T>::unpack8(B_sm[k * ncv + cv], b);
-            const float vk = V_sm[m * R + k];
+          for (int it = 0; it < ITER; ++it) {
+            float a[8];
+            Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
+            const float xm = Cvt<T>::to_f(xc[it * RPI]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = fmaf(vk, b[j], acc[j]);
+            for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
           }
-          float yo[8];
-          Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = acc[j] + yo[j];
-          st_global_v4(static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + cv) * 8,
-                       Cvt<T>::pack8(acc));
+          for (int off = VPR; off < 32; off <<= 1)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+          // Every lane now holds its vec's 8 partial sums P_q[m, vec*8 .. +8).  Push
+          // them into the reducers' shared memory with st.async (async proxy: the
+          // receiver's mbarrier completes on the bytes -- no cluster fence); the
+          // 32/VPR lanes sharing a vec split the 16-byte quads / destinations.
+          const int q = q0 + ql;
+          const int g = lane / VPR;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = m * R + vec * 8 + h * 4;
+            if (red_all) {
+              const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
+              for (int dst = (g + h) % RPI; dst < C; dst += RPI) {
+                uint32_t ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
+                st_async_v4(ra, acc[h * 4 + 0], acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3], rb);
+              }
+            } else if (g == h) {
+              const int owner = split_owner(o / 4, no / 4, C);
+              const int jl = o - split_lo(owner, no / 4, C) * 4;
+              st_async_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[h * 4 + 0],
+                          acc[h * 4 + 1], acc[h * 4 + 2], acc[h * 4 + 3],
+                          mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
+            }
+          }
+        }
+        LSG_TRACE(12);
+        if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
+        __syncthreads();
+        LSG_TRACE(13);
+        if (kEx && alias_ab && warp == b_warp && ncv > 0) {
+          // A is consumed: bring the (L2-warm) B slice into the same shared memory
+          if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
+          __syncwarp();
+          for (int k = lane; k < R; k += 32)
+            bulk_g2s(B_sm + k * ncv, Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
+                     &bars[kBarB]);
+        }
+        // ---- reduction over chunks, ascending q ----------------------------------
+        LSG_TRACE(6);
+        mbar_wait(&bars[kBarRed], phase);
+        LSG_TRACE(7);
+        if (red_all) {
+          for (int o = tid; o < no; o += kThreads) {
+            float s = 0.f;
+            for (int q = 0; q < p.nq; ++q) s += recv[(q * MT) * R + o];
+            V_sm[o] = s;
+          }
+        } else {
+          for (int o = o0 + tid; o < o1; o += kThreads) {
+            float s = 0.f;
+            for (int q = 0; q < p.nq; ++q) s += recv[q * slice_max + (o - o0)];
+            if constexpr (MODE == kShrink) {
+              const int m = o / R;
+              p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
+            } else {
+              const uint32_t local = smem_u32(V_sm + o), lbar = smem_u32(&bars[kBarV]);
+              for (int dst = 0; dst < C; ++dst) {
+                uint32_t ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
+                st_async_f32(ra, s, rb);
+              }
+            }
+          }
+          if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
         }
       }
+
+      if constexpr (kEx) {
+        LSG_TRACE(8);
+        cp_async_wait<0>();  // this thread's y vectors
+        __syncthreads();     // V_sm and every y vector visible
+        LSG_TRACE(9);
+        // ---- expand: y[m, n] += sum_k v[m, k] B[k, n] ---------------------------
+        if (ncv > 0) {
+          mbar_wait(&bars[kBarB], wphase);
+          LSG_TRACE(10);
+          for (int i = tid; i < rows * ncv; i += kThreads) {
+            const int m = i / ncv, cv = i - m * ncv;
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              float b[8];
+              Cvt<T>::unpack8(B_sm[k * ncv + cv], b);
+              const float vk = V_sm[m * R + k];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[j] = fmaf(vk, b[j], acc[j]);
+            }
+            float yo[8];
+            Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = acc[j] + yo[j];
+            st_global_v4(static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + cv) * 8,
+                         Cvt<T>::pack8(acc));
+          }
+        }
+      }
+      LSG_TRACE(11);
+      // The next tile reuses x_sm / y_sm / V_sm and the receive buffers: every CTA
+      // of the cluster must be done with this tile before anyone pushes again.
+      // (After the last tile nothing more is sent to anyone, and every incoming
+      // byte was awaited, so CTAs exit without a cluster barrier.)
+      if (t + tile_step < ntiles) {
+        if constexpr (kSh) cluster_sync();
+        else __syncthreads();
+      }
     }
-    LSG_TRACE(11);
-    // The next tile reuses x_sm / y_sm / V_sm and the receive buffers: every CTA
-    // of the cluster must be done with this tile before anyone pushes again.
-    // (After the last tile nothing more is sent to anyone, and every incoming
-    // byte was awaited, so CTAs exit without a cluster barrier.)
-    if (t + tile_step < ntiles) {
-      if constexpr (kSh) cluster_sync();
-      else __syncthreads();
-    }
+    if (last_item || static_cast<int64_t>(item) + gridDim.y >= p.s_n) return;
+    first_item = false;
   }
 }
 

@@ -1,25 +1,25 @@
 // sgmv_tc.cuh -- K5: tensor-core SGMV for long segments (prefill rows).
 //
-// Segments with >= kTcMinRows rows are cut into 128-row tiles.  Each tile is
-// served by a cluster of C = h_in / 512 CTAs; CTA c owns the 512-wide K chunk c
-// of the shrink and the 512-wide column block c of the expand:
+// Segments with >= kTcMinRows rows are cut into 128-row tiles and run through
+// two tcgen05 kernels (launched back to back with programmatic dependent launch):
 //
-//   shrink  D1[128 x r] (TMEM, fp32) = x[128 x 512] . A[512 x r]
-//           x arrives by TMA (tensor map, 128B swizzle, 4-stage ring), A is
-//           re-laid out into the UMMA MN-major swizzled layout; one elected
-//           thread issues tcgen05.mma (M=128, N=r, K=16) per 16-wide K step.
-//   reduce  D1 is drained (tcgen05.ld) and each row's partial is pushed with
-//           st.async to the CTA owning that row; owners sum the C chunk
-//           partials in chunk order and push v back to every CTA.
-//   expand  v is split into 16-bit hi + lo parts (v = hi + lo to ~22 bits) and
-//           D2[128 x 256] = hi . B + lo . B per 256-column block (two blocks,
-//           two TMEM buffers); the epilogue drains D2, adds y and stores the
-//           segment's rows.
+//   shrink  grid (nq, tiles), cluster (nq): CTA q computes the partial
+//           D1[128 x r] (TMEM, fp32) = x[128 x kcs] . A[kcs x r] over its K
+//           chunk q (kcs = h_in / nq).  x arrives by TMA (128B-swizzled boxes
+//           of 64 x 128, ring of up to 6); A is re-laid out into the UMMA
+//           MN-major swizzled form.  Each row's partial is pushed with st.async
+//           to the CTA owning that row; owners sum the nq partials in chunk
+//           order and store v [rows x r] (fp32) into the workspace.
+//   expand  grid (h_out / 256, tiles), no cluster: v is split into 16-bit
+//           hi + lo parts and D2[128 x 256] = hi . B + lo . B (TMEM); y_old is
+//           staged by TMA (4 boxes of 64 x 128, 128B swizzle), the epilogue adds
+//           D2 in place and the tile goes back by TMA store (partial tiles:
+//           per-row stores of the segment's rows only).
 //
-// Canonical arithmetic for rows of long segments: v = sum over 512-chunks q
+// Canonical arithmetic for rows of long segments: v = sum over K chunks q
 // (ascending) of the MMA partial of chunk q; y = rn(fp32(hi.B + lo.B) + y_old).
-// Whether a segment takes this path depends only on its length, so results
-// stay independent of batch composition and segment order.
+// Whether a segment takes this path depends only on its length and the shape,
+// so results are independent of batch composition and segment order.
 #pragma once
 
 #include <cuda.h>
@@ -31,26 +31,55 @@
 
 namespace lsg {
 
-constexpr int kTcMinRows = 128;   // segments at least this long use the tensor-core path
-constexpr int kTcM = 128;         // rows per tile (UMMA M)
-constexpr int kTcKC = 512;        // K chunk per CTA (canonical reduction unit)
-constexpr int kTcKB = 64;         // K per TMA box / stage (128 bytes of fp16)
-constexpr int kTcStages = 4;      // x ring depth
-constexpr int kTcNT = 256;        // expand N tile (UMMA N)
-constexpr int kTcThreads = 256;
+constexpr int kTcMinRows = 128;  // segments at least this long use the tensor-core path
+constexpr int kTcM = 128;        // rows per tile (UMMA M)
+constexpr int kTcKB = 64;        // K per x box (128 bytes of 16-bit)
+constexpr int kTcBox = kTcM * kTcKB * 2;  // 16 KB per 64 x 128 box
+constexpr int kTcMaxStages = 6;  // x ring depth (shrink)
+constexpr int kTcNT = 256;       // expand N tile (UMMA N)
+constexpr int kTcThreads = 128;
 
-struct TcParams {
+struct TcShrinkParams {
   CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 128, 128B swizzle
-  void* y;
+  float* v;            // workspace [s_n][r] fp32 (rows of long segments only)
   const void* const* a_ptr;
-  const void* const* b_ptr;
-  int64_t a_off, b_off, ldy;
+  int64_t a_off;
   const int32_t* seg_starts;
   const int32_t* seg_slot;
-  int32_t n_seg, s_n, num_slots, h_in, h_out;
+  int32_t n_seg, s_n, num_slots, h_in, kcs;
+  unsigned long long* trace;  // lsg_set_trace: %globaltimer stamps, entries [trace_ctas, 2 trace_ctas)
+  int32_t trace_ctas;
 };
 
-// ---- tcgen05 / UMMA helpers ------------------------------------------------------
+struct TcExpandParams {
+  CUtensorMap tmap_y;  // y [s_n, h_out], box 64 x 128, 128B swizzle
+  void* y;
+  int64_t ldy;
+  const float* v;
+  const void* const* b_ptr;
+  int64_t b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  int32_t n_seg, s_n, num_slots, h_out;
+  unsigned long long* trace;
+  int32_t trace_ctas;
+};
+
+// Shrink CTAs trace into entries [trace_ctas, 1.5 trace_ctas), expand CTAs into
+// [1.5 trace_ctas, 2 trace_ctas); 16 %globaltimer stamps each.
+#define LSG_TC_TRACE(base, i)                                                                        \
+  do {                                                                                               \
+    if (p.trace != nullptr && threadIdx.x == 0) {                                                    \
+      const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                          \
+      if (cta_ < p.trace_ctas / 2) {                                                                 \
+        unsigned long long gt_;                                                                      \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                                     \
+        p.trace[(p.trace_ctas + (base) * (p.trace_ctas / 2) + cta_) * 16 + (i)] = gt_;               \
+      }                                                                                              \
+    }                                                                                                \
+  } while (0)
+
+// ---- tcgen05 / UMMA / TMA helpers ---------------------------------------------------
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -60,7 +89,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= static_cast<uint64_t>(layout & 7) << 61;
   return d;
 }
-// layout codes of the smem descriptor
+// layout codes of the shared-memory descriptor
 constexpr uint32_t kSwNone = 0, kSw128 = 2, kSw64 = 4, kSw32 = 6;
 
 // kind::f16 instruction descriptor: D fp32, A K-major, B MN-major
@@ -85,6 +114,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t tmem) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(NCOLS));
+}
+
 // 32 lanes x 16 consecutive 32-bit TMEM columns -> 16 registers per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
@@ -107,6 +147,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tmap, 
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tmap, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
+}
+
 // 16-byte chunk index XOR of the 32/64/128-byte swizzles for row k
 template <int ROWB>
 __device__ __forceinline__ int swz(int k) {
@@ -115,115 +172,135 @@ __device__ __forceinline__ int swz(int k) {
   else return k & 7;
 }
 
+// Tile t of a launch -> (long segment, tile within it): warp-wide prefix sum of
+// ceil(len / 128) over the segments with len >= kTcMinRows, 32 segments per step.
+// Call from one full warp; seg = -1 past the last tile.
+__device__ __forceinline__ void tc_tile_of(const int32_t* seg_starts, int n_seg, int t, int lane, int& seg,
+                                           int& tin) {
+  int base = 0;
+  seg = -1;
+  tin = 0;
+  for (int c0 = 0; c0 < n_seg && seg < 0; c0 += 32) {
+    const int sg = c0 + lane;
+    int nt = 0;
+    if (sg < n_seg) {
+      const int len = seg_starts[sg + 1] - seg_starts[sg];
+      nt = len >= kTcMinRows ? (len + kTcM - 1) / kTcM : 0;
+    }
+    int incl = nt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      seg = c0 + l;
+      tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ---- shared-memory plans (host and device) ---------------------------------------------
+__host__ __device__ constexpr int tc_shrink_stages(int kcs) {
+  return kcs / kTcKB < kTcMaxStages ? kcs / kTcKB : kTcMaxStages;
+}
+__host__ __device__ constexpr uint32_t tc_shrink_off_a(int kcs) { return tc_shrink_stages(kcs) * kTcBox; }
+__host__ __device__ constexpr uint32_t tc_shrink_off_recv(int R, int kcs) {
+  return (tc_shrink_off_a(kcs) + kcs * R * 2 + 127) & ~127u;
+}
+__host__ __device__ constexpr uint32_t tc_shrink_off_bars(int R, int kcs) {
+  return tc_shrink_off_recv(R, kcs) + kTcM * R * 4;
+}
+__host__ __device__ constexpr uint32_t tc_shrink_smem(int R, int kcs) {
+  return tc_shrink_off_bars(R, kcs) + 256 + 1024;  // + alignment slack
+}
 template <int R>
-struct TcLayout {
-  static constexpr uint32_t kX = 0;                                   // ring: 4 x 16 KB (1024-aligned)
-  static constexpr uint32_t kXStage = kTcM * kTcKB * 2;               // 16 KB
-  static constexpr uint32_t kA = kX + kTcStages * kXStage;            // A chunk: 512 rows x 2R bytes
-  static constexpr uint32_t kB = kA + kTcKC * R * 2;                  // 2 N tiles of R x 256 (SW128 atoms)
-  static constexpr uint32_t kBTile = R * kTcNT * 2;
-  static constexpr uint32_t kVhi = kB + 2 * kBTile;                   // v hi/lo: 128 x R, K-major interleave
+struct TcExpandLayout {
+  static constexpr uint32_t kY = 0;                       // 4 boxes of 64 cols x 128 rows (SW128)
+  static constexpr uint32_t kB = 4 * kTcBox;              // B [R x 256], MN-major SW128 atoms
+  static constexpr uint32_t kVhi = kB + R * kTcNT * 2;    // v hi / lo: 128 x R, K-major interleave
   static constexpr uint32_t kVlo = kVhi + kTcM * R * 2;
-  static constexpr uint32_t kV = kVlo + kTcM * R * 2;                 // fp32 v [128][R]
-  static constexpr uint32_t kRecv = kV + kTcM * R * 4;                // [16 chunks][16 rows][R] fp32 partials
-  static constexpr uint32_t kBars = kRecv + 16 * 16 * R * 4;
-  static constexpr uint32_t kTotal = kBars + 256;
+  static constexpr uint32_t kBars = kVlo + kTcM * R * 2;
+  static constexpr uint32_t kTotal = kBars + 64 + 1024;  // + alignment slack
 };
 
-// Rows of the tile owned (reduced) by each CTA of the cluster
-__device__ __forceinline__ int tc_rows_per_owner(int C) { return (kTcM + C - 1) / C; }
-
+// ---------------------------------------------------------------------------------------
+// Shrink: v[tile rows] = x[tile rows] . A_slot   (cluster of nq CTAs over K)
+// ---------------------------------------------------------------------------------------
 template <typename T, int R>
-__global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_kernel(const __grid_constant__ TcParams p) {
-  static_assert(R == 16 || R == 32, "tensor-core path ranks");
-  using L = TcLayout<R>;
+__global__ void __launch_bounds__(kTcThreads) sgmv_tc_shrink_kernel(const __grid_constant__ TcShrinkParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core path ranks");
   constexpr int ROWB = 2 * R;  // bytes per A row (MN-major swizzle width)
-  constexpr uint32_t kSwA = R == 16 ? kSw32 : kSw64;
+  constexpr uint32_t kSwA = R == 16 ? kSw32 : (R == 32 ? kSw64 : kSw128);
+  constexpr int kTmemCols = R < 32 ? 32 : R;
   constexpr int fmt = std::is_same<T, __half>::value ? 0 : 1;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte aligned base (128B-swizzle atoms); the launch adds 1 KB of slack
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int C = static_cast<int>(gridDim.x);
-  const int crank = static_cast<int>(blockIdx.x);
+  uint8_t* smem = align1024(smem_raw);
+  const int nq = static_cast<int>(gridDim.x), q = static_cast<int>(blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);
-  // 0..3 full[s], 4..7 empty[s], 8 d1 ready, 9 partials in, 10 v in, 11 d2 tile 0, 12 d2 tile 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 128);
-  float* recv = reinterpret_cast<float*>(smem + L::kRecv);
-  float* V = reinterpret_cast<float*>(smem + L::kV);
+  const int kcs = p.kcs, nkb = kcs / kTcKB, stages = tc_shrink_stages(kcs);
+  uint8_t* xs = smem;
+  uint8_t* As = smem + tc_shrink_off_a(kcs);
+  float* recv = reinterpret_cast<float*>(smem + tc_shrink_off_recv(R, kcs));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc_shrink_off_bars(R, kcs));
+  // bars: [0, 8) full[s], [8, 16) empty[s], 16 D1 ready, 17 partials in
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
-  pdl_launch_dependents();
-  // ---- tile -> (long segment, tile) ------------------------------------------------
+  LSG_TC_TRACE(0, 0);
   __shared__ int s_seg, s_tile;
   if (warp == 0) {
-    const int t = blockIdx.y;
-    int base = 0, seg = -1, tin = 0;
-    for (int c0 = 0; c0 < p.n_seg && seg < 0; c0 += 32) {
-      const int sg = c0 + lane;
-      int nt = 0;
-      if (sg < p.n_seg) {
-        const int len = p.seg_starts[sg + 1] - p.seg_starts[sg];
-        nt = len >= kTcMinRows ? (len + kTcM - 1) / kTcM : 0;
-      }
-      int incl = nt;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
-      if (hit) {
-        const int l = __ffs(hit) - 1;
-        seg = c0 + l;
-        tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
-      }
-      base += __shfl_sync(0xffffffffu, incl, 31);
-    }
+    int seg, tin;
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
     if (lane == 0) {
       s_seg = seg;
       s_tile = tin;
     }
   }
   __syncthreads();
-  if (s_seg < 0) return;
-  const int seg_begin = p.seg_starts[s_seg], seg_end = p.seg_starts[s_seg + 1];
+  if (s_seg < 0) {  // past the last tile (the grid is an upper bound), whole cluster
+    pdl_wait();       // (the expand relies on every shrink CTA having waited, see below)
+    return;
+  }
   const int slot = p.seg_slot[s_seg];
-  if (slot < 0 || slot >= p.num_slots) return;
-  const int r0 = seg_begin + s_tile * kTcM;
+  if (slot < 0 || slot >= p.num_slots) {  // no adapter: the expand leaves y untouched
+    pdl_wait();
+    return;
+  }
+  const int seg_end = p.seg_starts[s_seg + 1];
+  const int r0 = p.seg_starts[s_seg] + s_tile * kTcM;
   const int rows = min(kTcM, seg_end - r0);
-  const int k0 = crank * kTcKC;             // this CTA's K chunk
-  const int n0 = crank * (p.h_out / C);     // this CTA's column block (2 x 256)
-  const int rpo = tc_rows_per_owner(C);
+  const int k0 = q * kcs;
+  const int rpo = kTcM / nq;  // rows reduced by each CTA
 
   if (tid == 0) {
-    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 18; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_x)) : "memory");
+    prefetch_tmap(&p.tmap_x);
   }
-  if (warp == 0) {  // TMEM: 512 columns (D1 shares buffer 0 with the first D2 tile)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  // ---- weights (independent of the preceding kernel): A chunk and B block, laid
-  //      out in the UMMA MN-major swizzled form --------------------------------------
+  if (warp == 0) tmem_alloc<kTmemCols>(tmem_slot);
+  // ---- A chunk (weights: independent of the preceding kernel) -> MN-major swizzled smem
   {
     const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(k0) * R;
-    uint8_t* As = smem + L::kA;
     constexpr int CPR = ROWB / 16;  // 16-byte chunks per A row
-    for (int i = tid; i < kTcKC * CPR; i += kTcThreads) {
-      const int k = i / CPR, c = i - k * CPR;
-      const uint4 v = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(k) * R + c * 8);
-      *reinterpret_cast<uint4*>(As + k * ROWB + ((c ^ swz<ROWB>(k)) * 16)) = v;
-    }
-    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
-    uint8_t* Bs = smem + L::kB;
-    // tile nt, atom na (64 cols), k-group kg: offset nt*kBTile + na*(R/8*1024) + kg*1024 + kk*128 + swz chunk
-    for (int i = tid; i < R * (2 * kTcNT / 8); i += kTcThreads) {
-      const int k = i / (2 * kTcNT / 8), cc = i - k * (2 * kTcNT / 8);  // cc: 16-byte chunk over 512 cols
-      const int nt = cc / (kTcNT / 8), na = (cc % (kTcNT / 8)) / 8, j = cc % 8;
-      const uint4 v = *reinterpret_cast<const uint4*>(B + static_cast<int64_t>(k) * p.h_out + cc * 8);
-      *reinterpret_cast<uint4*>(Bs + nt * L::kBTile + na * (R / 8) * 1024 + (k / 8) * 1024 + (k % 8) * 128 +
-                                ((j ^ (k % 8)) * 16)) = v;
+    const int total = kcs * CPR;
+    for (int base = 0; base < total; base += 8 * kTcThreads) {
+      uint4 va[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = base + j * kTcThreads + tid;
+        if (i < total) va[j] = ldg_nc_v4(A + static_cast<int64_t>(i) * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = base + j * kTcThreads + tid;
+        if (i < total) {
+          const int k = i / CPR, c = i - k * CPR;
+          *reinterpret_cast<uint4*>(As + k * ROWB + ((c ^ swz<ROWB>(k)) * 16)) = va[j];
+        }
+      }
     }
   }
   fence_proxy_async_smem();  // generic smem writes -> visible to the tensor cores
@@ -231,140 +308,245 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  cluster_arrive_relaxed();
+  cluster_arrive_relaxed();  // barrier inits -> the cluster (waited on before the first push)
+  LSG_TC_TRACE(0, 1);
 
-  pdl_wait();  // x and y may come from the preceding kernel
-
-  const uint32_t idesc1 = umma_idesc(fmt, kTcM, R);
-  const uint32_t idesc2 = umma_idesc(fmt, kTcM, kTcNT);
-  // ---- shrink: TMA producer (warp 1) / MMA issuer (warp 0) ---------------------------
-  constexpr int nkb = kTcKC / kTcKB;  // 8 K blocks per chunk
-  if (warp == 1 && lane == 0) {
+  pdl_wait();  // x may come from the preceding kernel
+  // Dependents (the expand) start only now: every kernel before this one has
+  // completed, so the expand may read y_old before its own wait (it waits only
+  // for v from this kernel).
+  pdl_launch_dependents();
+  LSG_TC_TRACE(0, 2);
+  const uint32_t idesc = umma_idesc(fmt, kTcM, R);
+  if (warp == 1 && lane == 0) {  // TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kTcStages;
-      if (kb >= kTcStages) mbar_wait(&bars[4 + s], ((kb / kTcStages) - 1) & 1);
-      mbar_arrive_expect_tx(&bars[s], L::kXStage);
-      tma_load_2d(smem + L::kX + s * L::kXStage, &p.tmap_x, k0 + kb * kTcKB, r0, &bars[s]);
+      const int s = kb % stages;
+      if (kb >= stages) mbar_wait(&bars[8 + s], ((kb / stages) - 1) & 1);
+      mbar_arrive_expect_tx(&bars[s], kTcBox);
+      tma_load_2d(xs + s * kTcBox, &p.tmap_x, k0 + kb * kTcKB, r0, &bars[s]);
     }
-  } else if (warp == 0 && lane == 0) {
+  } else if (warp == 0 && lane == 0) {  // MMA issuer
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kTcStages;
-      mbar_wait(&bars[s], (kb / kTcStages) & 1);
+      const int s = kb % stages;
+      mbar_wait(&bars[s], (kb / stages) & 1);
       tc_fence_after();
-      const uint32_t xs = smem_u32(smem + L::kX + s * L::kXStage);
-      const uint32_t as = smem_u32(smem + L::kA) + kb * kTcKB * ROWB;
+      const uint32_t xa = smem_u32(xs + s * kTcBox);
+      const uint32_t aa = smem_u32(As) + kb * kTcKB * ROWB;
 #pragma unroll
       for (int ks = 0; ks < kTcKB / 16; ++ks) {
-        const uint64_t ad = umma_desc(xs + ks * 32, 16, 1024, kSw128);                 // x: K-major SW128
-        const uint64_t bd = umma_desc(as + ks * 16 * ROWB, 16, 8 * ROWB, kSwA);        // A: MN-major
-        umma_f16(tmem, ad, bd, idesc1, (kb | ks) ? 1u : 0u);
+        const uint64_t ad = umma_desc(xa + ks * 32, 16, 1024, kSw128);           // x: K-major SW128
+        const uint64_t bd = umma_desc(aa + ks * 16 * ROWB, 16, 8 * ROWB, kSwA);  // A: MN-major
+        umma_f16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
       }
-      umma_commit(&bars[4 + s]);  // stage free once these MMAs have read it
+      umma_commit(&bars[8 + s]);  // stage free once these MMAs have read it
     }
-    umma_commit(&bars[8]);        // D1 complete
+    umma_commit(&bars[16]);  // D1 complete
   }
   __syncwarp();  // producer / issuer lanes rejoin their warps before .aligned ops
-  // ---- reduce: drain D1, push row partials to their owners ----------------------------
+
+  // ---- reduce: each row's partial -> the CTA owning the row ----------------------------
   cluster_wait();  // peers' barriers initialised
-  const int my_rows = max(0, min(rpo, kTcM - crank * rpo));
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bars[9], static_cast<uint32_t>(C * my_rows * R * 4));
-    mbar_arrive_expect_tx(&bars[10], static_cast<uint32_t>(kTcM * R * 4));
-  }
-  if (warp < 4) {
-    mbar_wait(&bars[8], 0);
-    tc_fence_after();
+  if (tid == 0) mbar_arrive_expect_tx(&bars[17], static_cast<uint32_t>(nq * rpo * R * 4));
+  mbar_wait(&bars[16], 0);
+  LSG_TC_TRACE(0, 3);
+  tc_fence_after();
+  {
     const int m = warp * 32 + lane;
     const int owner = m / rpo, ml = m - owner * rpo;
+    const uint32_t rb = mapa_u32(&bars[17], static_cast<uint32_t>(owner));
+#pragma unroll
     for (int c0 = 0; c0 < R; c0 += 16) {
       float v[16];
       tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-      const uint32_t ra = mapa_u32(recv + (crank * rpo + ml) * R + c0, static_cast<uint32_t>(owner));
-      const uint32_t rb = mapa_u32(&bars[9], static_cast<uint32_t>(owner));
+      const uint32_t ra = mapa_u32(recv + (q * rpo + ml) * R + c0, static_cast<uint32_t>(owner));
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) st_async_v4(ra + q4 * 16, v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3], rb);
+      for (int j = 0; j < 4; ++j) st_async_v4(ra + j * 16, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3], rb);
     }
   }
-  // owners: v[m][k] = sum over chunks (CTAs) in rank order, then broadcast to all CTAs
-  mbar_wait(&bars[9], 0);
-  for (int i = tid; i < my_rows * R; i += kTcThreads) {
+  mbar_wait(&bars[17], 0);
+  LSG_TC_TRACE(0, 4);
+  // v[r0 + q*rpo + ml][k] = sum over chunks qq (ascending) -- rows of this segment only
+  for (int i = tid; i < rpo * R; i += kTcThreads) {
     const int ml = i / R, k = i - ml * R;
     float s = 0.f;
-    for (int q = 0; q < C; ++q) s += recv[(q * rpo + ml) * R + k];
-    const uint32_t local = smem_u32(V + (crank * rpo + ml) * R + k), lbar = smem_u32(&bars[10]);
-    for (int dst = 0; dst < C; ++dst) {
-      uint32_t ra, rb;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
-      st_async_f32(ra, s, rb);
-    }
-  }
-  mbar_wait(&bars[10], 0);
-  // v -> 16-bit hi + lo, K-major interleave: (m,k) at (m/8)*SBO + (k/8)*128 + (m%8)*16 + (k%8)*2
-  for (int i = tid; i < kTcM * (R / 8); i += kTcThreads) {
-    const int m = i / (R / 8), kg = i - m * (R / 8);
-    float f[8], lo[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) f[j] = V[m * R + kg * 8 + j];
-    const uint4 hi = Cvt<T>::pack8(f);
-    float hf[8];
-    Cvt<T>::unpack8(hi, hf);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) lo[j] = f[j] - hf[j];
-    const uint32_t off = (m / 8) * (R / 8) * 128 + kg * 128 + (m % 8) * 16;
-    *reinterpret_cast<uint4*>(smem + L::kVhi + off) = hi;
-    *reinterpret_cast<uint4*>(smem + L::kVlo + off) = Cvt<T>::pack8(lo);
-  }
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  // ---- expand: two 256-column tiles, one TMEM buffer each ------------------------------
-  if (warp == 0 && lane == 0) {
-    tc_fence_after();
-    for (int nt = 0; nt < 2; ++nt) {
-      const uint32_t d2 = tmem + nt * kTcNT;
-      const uint32_t bs = smem_u32(smem + L::kB) + nt * L::kBTile;
-#pragma unroll
-      for (int ks = 0; ks < R / 16; ++ks) {
-        const uint64_t bd = umma_desc(bs + ks * 2 * 1024, (R / 8) * 1024, 1024, kSw128);  // B: MN-major SW128
-        const uint64_t ah = umma_desc(smem_u32(smem + L::kVhi) + ks * 256, 128, (R / 8) * 128, kSwNone);
-        const uint64_t al = umma_desc(smem_u32(smem + L::kVlo) + ks * 256, 128, (R / 8) * 128, kSwNone);
-        umma_f16(d2, ah, bd, idesc2, ks ? 1u : 0u);
-        umma_f16(d2, al, bd, idesc2, 1u);
-      }
-      umma_commit(&bars[11 + nt]);
-    }
-  }
-  __syncwarp();
-  // ---- epilogue: y[r0+m, n0 + nt*256 + c] = rn(D2 + y_old), rows of this segment only --
-  {
-    const int m = (warp & 3) * 32 + lane;
-    const int half = warp >> 2;  // warps 4..7 take the upper 128 columns of each tile
-    for (int nt = 0; nt < 2; ++nt) {
-      mbar_wait(&bars[11 + nt], 0);
-      tc_fence_after();
-      for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
-        float acc[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + nt * kTcNT + c0, acc);
-        if (m < rows) {
-          T* yp = static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + n0 + nt * kTcNT + c0;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float yo[8];
-            Cvt<T>::unpack8(*reinterpret_cast<const uint4*>(yp + h * 8), yo);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) yo[j] = acc[h * 8 + j] + yo[j];
-            st_global_v4(yp + h * 8, Cvt<T>::pack8(yo));
-          }
-        }
-      }
-    }
+    for (int qq = 0; qq < nq; ++qq) s += recv[(qq * rpo + ml) * R + k];
+    const int m = q * rpo + ml;
+    if (m < rows) p.v[static_cast<int64_t>(r0 + m) * R + k] = s;
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+  LSG_TC_TRACE(0, 5);
+}
+
+// ---------------------------------------------------------------------------------------
+// Expand: y[tile rows, n0 : n0 + 256] = rn(v . B_slot + y_old)
+// ---------------------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid_constant__ TcExpandParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core path ranks");
+  using L = TcExpandLayout<R>;
+  constexpr int fmt = std::is_same<T, __half>::value ? 0 : 1;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = static_cast<int>(blockIdx.x) * kTcNT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);  // 0 y landed, 1 D2 ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  LSG_TC_TRACE(1, 0);
+  pdl_launch_dependents();
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  __syncthreads();
+  if (s_seg < 0) return;
+  const int slot = p.seg_slot[s_seg];
+  if (slot < 0 || slot >= p.num_slots) return;  // no adapter: y untouched
+  const int seg_end = p.seg_starts[s_seg + 1];
+  const int r0 = p.seg_starts[s_seg] + s_tile * kTcM;
+  const int rows = min(kTcM, seg_end - r0);
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    prefetch_tmap(&p.tmap_y);
+  }
+  if (warp == 0) tmem_alloc<kTcNT>(tmem_slot);
+  // ---- B block [R x 256] (weights) -> MN-major SW128 atoms: 64-col atom na, k-group kg:
+  //      na*(R/8)*1024 + kg*1024 + (k%8)*128 + swizzled 16-byte chunk
+  {
+    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
+    constexpr int total = R * (kTcNT / 8);
+    constexpr int per = total / kTcThreads;  // 4 / 8 / 16
+    uint4 vb[per];
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int i = j * kTcThreads + tid, k = i / (kTcNT / 8), cc = i - k * (kTcNT / 8);
+      vb[j] = ldg_nc_v4(B + static_cast<int64_t>(k) * p.h_out + cc * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int i = j * kTcThreads + tid, k = i / (kTcNT / 8), cc = i - k * (kTcNT / 8);
+      const int na = cc / 8, jj = cc % 8;
+      *reinterpret_cast<uint4*>(smem + L::kB + na * (R / 8) * 1024 + (k / 8) * 1024 + (k % 8) * 128 +
+                                ((jj ^ (k % 8)) * 16)) = vb[j];
+    }
+  }
+  // y_old: written only by kernels before the shrink, which all completed before
+  // the shrink triggered this launch -- staged ahead of the wait for v.
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bars[0], 4 * kTcBox);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_2d(smem + L::kY + b * kTcBox, &p.tmap_y, n0 + b * kTcKB, r0, &bars[0]);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  LSG_TC_TRACE(1, 1);
+
+  pdl_wait();  // v (the shrink) is ready
+  LSG_TC_TRACE(1, 2);
+  // v -> 16-bit hi + lo, K-major interleave: (m,k) at (m/8)*SBO + (k/8)*128 + (m%8)*16 + (k%8)*2
+  {
+    const int m = tid;
+    const float* vr = p.v + static_cast<int64_t>(r0 + m) * R;
+#pragma unroll
+    for (int kg = 0; kg < R / 8; ++kg) {
+      float f[8], hf[8], lo[8];
+      if (m < rows) {
+        const float4 a = *reinterpret_cast<const float4*>(vr + kg * 8);
+        const float4 b = *reinterpret_cast<const float4*>(vr + kg * 8 + 4);
+        f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = 0.f;
+      }
+      const uint4 hi = Cvt<T>::pack8(f);
+      Cvt<T>::unpack8(hi, hf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) lo[j] = f[j] - hf[j];
+      const uint32_t off = (m / 8) * (R / 8) * 128 + kg * 128 + (m % 8) * 16;
+      *reinterpret_cast<uint4*>(smem + L::kVhi + off) = hi;
+      *reinterpret_cast<uint4*>(smem + L::kVlo + off) = Cvt<T>::pack8(lo);
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0 && lane == 0) {
+    tc_fence_after();
+    const uint32_t idesc = umma_idesc(fmt, kTcM, kTcNT);
+    const uint32_t bs = smem_u32(smem + L::kB);
+#pragma unroll
+    for (int ks = 0; ks < R / 16; ++ks) {
+      const uint64_t bd = umma_desc(bs + ks * 2 * 1024, (R / 8) * 1024, 1024, kSw128);  // B: MN-major SW128
+      const uint64_t ah = umma_desc(smem_u32(smem + L::kVhi) + ks * 256, 128, (R / 8) * 128, kSwNone);
+      const uint64_t al = umma_desc(smem_u32(smem + L::kVlo) + ks * 256, 128, (R / 8) * 128, kSwNone);
+      umma_f16(tmem, ah, bd, idesc, ks ? 1u : 0u);
+      umma_f16(tmem, al, bd, idesc, 1u);
+    }
+    umma_commit(&bars[1]);
+  }
+  __syncwarp();
+  // ---- epilogue: row m = this thread; y_old from the swizzled staging, in place ----------
+  mbar_wait(&bars[0], 0);
+  LSG_TC_TRACE(1, 3);
+  mbar_wait(&bars[1], 0);
+  LSG_TC_TRACE(1, 4);
+  tc_fence_after();
+  const int m = tid;
+  uint8_t* yrow = smem + L::kY + m * 128;  // + box * kTcBox + swizzled chunk
+#pragma unroll 4
+  for (int c = 0; c < kTcNT / 16; ++c) {
+    float acc[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, acc);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = (c % 4) * 2 + h;
+      uint4* ptr = reinterpret_cast<uint4*>(yrow + (c / 4) * kTcBox + ((j ^ (m & 7)) * 16));
+      float f[8];
+      Cvt<T>::unpack8(*ptr, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = acc[h * 8 + e] + f[e];
+      *ptr = Cvt<T>::pack8(f);
+    }
+  }
+  if (rows == kTcM) {
+    fence_proxy_async_smem();  // epilogue writes -> visible to the TMA store
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) tma_store_2d(&p.tmap_y, smem + L::kY + b * kTcBox, n0 + b * kTcKB, r0);
+      bulk_commit_group();
+      bulk_wait_group0();
+    }
+  } else if (m < rows) {  // last tile of a segment: only the segment's rows
+    T* yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + n0;
+#pragma unroll 4
+    for (int i = 0; i < kTcNT / 8; ++i) {
+      const int b = i / 8, j = i % 8;
+      st_global_v4(yg + i * 8, *reinterpret_cast<const uint4*>(yrow + b * kTcBox + ((j ^ (m & 7)) * 16)));
+    }
+  }
+  LSG_TC_TRACE(1, 5);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<kTcNT>(tmem);
   }
 }
 

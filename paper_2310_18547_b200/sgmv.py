@@ -89,9 +89,18 @@ def sgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.
     _check_i32(seg_starts, "seg_starts")
     _check_i32(seg_slot, "seg_slot")
     n = seg_slot.numel() if num_segments is None else num_segments
-    _lib.call("lsg_sgmv", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
-              _ptr(seg_slot), n, x.shape[0], layer, _stream())
+    # Segments of >= 128 rows run on the tensor cores and keep v in a workspace;
+    # it comes from torch's caching allocator (stream-ordered, graph-capture safe).
+    wsb = sgmv_workspace_size(pool, x.shape[0])
+    ws = torch.empty(wsb, dtype=torch.uint8, device=x.device) if wsb else None
+    _lib.call("lsg_sgmv_ws", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
+              _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws) if ws is not None else None, wsb, _stream())
     return y
+
+
+def sgmv_workspace_size(pool: AdapterPool, rows: int) -> int:
+    """Bytes of workspace a fused call over ``rows`` rows may use (0: none)."""
+    return int(_lib.lib().lsg_sgmv_workspace_size(C.byref(pool.table), rows))
 
 
 def sgmv_shrink(v: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.Tensor,

@@ -48,7 +48,7 @@ def main():
     sl = torch.arange(n, dtype=torch.int32, device="cuda")
     info = lsg.query_launch(pool, n, a.batch)
     ctas = info["grid_ctas"]
-    buf = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2 * ctas * 16, dtype=torch.int64, device="cuda")
     mid = a.sites // 2
 
     def step(trace):
@@ -73,7 +73,7 @@ def main():
         with torch.cuda.stream(stream):
             step(True)
     torch.cuda.synchronize()
-    t = buf.view(ctas, 16).cpu()
+    t = buf.view(2 * ctas, 16)[:ctas].cpu()
     ghz = 1.965
     rel = (t[:, :14] - t[:, :1]).double() / ghz / 1e3  # us since this CTA's entry
     valid = t[:, 11] != 0

@@ -190,13 +190,14 @@ def test_mixed_prefill_plus_decodes(lsg, prefill):
 # Long segments: the tcgen05 path (segments >= 128 rows, r in {16, 32}, h % 512 == 0)
 # ---------------------------------------------------------------------------------
 @pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("shape", [(4096, 16), (4096, 32), (5120, 16), (8192, 32), (1024, 16)])
+@pytest.mark.parametrize("shape", [(4096, 4096, 16), (4096, 4096, 32), (4096, 4096, 64), (5120, 5120, 16),
+                                   (8192, 8192, 32), (1024, 1024, 16), (4096, 11008, 16), (11008, 4096, 16)])
 @pytest.mark.parametrize("lens", [(128,), (129, 3, 1, 255), (1, 700, 5, 2048, 1, 1)])
 def test_long_segments_tensor_core_path(lsg, dtype, shape, lens):
-    h, r = shape
+    h_in, h_out, r = shape
     bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
-    x, A, B = random_problem(h, h, r, bounds, 5 + len(lens))
-    y0 = oracle().rng(123).fill_pm1(int(bounds[-1]) * h).reshape(-1, h)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 5 + len(lens))
+    y0 = oracle().rng(123).fill_pm1(int(bounds[-1]) * h_out).reshape(-1, h_out)
     p = Problem(lsg, x, A, B, bounds, dtype, y0=y0)
     got = p.run()
     err = row_norm_err(got.double().cpu().numpy(), p.reference())
@@ -246,6 +247,24 @@ def test_kernel_variants_and_cluster_sizes_bitwise_identical(lsg, dtype):
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, 0)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 0)
     assert torch.equal(p.run("fused"), base)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_many_medium_segments_bitwise_across_variants(lsg, dtype):
+    """Thousands of row tiles (more than the capped tile-scan grid): clusters loop
+    over several tiles; results stay bitwise equal to the one-row-per-cluster BGMV."""
+    lens = [(37 * i) % 127 + 1 for i in range(70)]
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 21)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    base = p.run("fused")
+    err = row_norm_err(base.double().cpu().numpy(), p.reference())
+    assert err <= tol(dtype), err
+    assert torch.equal(p.run("bgmv"), base)
+    assert torch.equal(p.run("two_launch"), base)
+    for c in (2, 16):
+        lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
+        assert torch.equal(p.run("fused"), base), c
 
 
 def test_segment_permutation_permutes_rows_bitwise(lsg):
