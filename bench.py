@@ -472,14 +472,14 @@ def sweep(a, lsg, torch, dtype, stream):
             with torch.cuda.graph(g, stream=stream):
                 for s in range(L):
                     lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
-            for _ in range(3):
-                g.replay()
-            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(10):
-                g.replay()
-            e1.record(stream)
+            with torch.cuda.stream(stream):  # replay on the stream the events are recorded on
+                for _ in range(3):
+                    g.replay()
+                e0.record(stream)
+                for _ in range(10):
+                    g.replay()
+                e1.record(stream)
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / (10 * L)
             b = alg_bytes(batch, nseg, h, r)

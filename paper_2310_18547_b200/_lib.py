@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libsgmv_b200.so")
+# LSG_LIB_OVERRIDE: load an experimental build of the same library (scripts/build_variant.sh)
+LIB_PATH = os.environ.get("LSG_LIB_OVERRIDE") or os.path.join(PKG, "lib", "libsgmv_b200.so")
 
 LSG_OK, LSG_EINVAL, LSG_EUNSUPPORTED, LSG_ECUDA, LSG_ENODEVICE = 0, -1, -2, -3, -4
 LSG_F16, LSG_BF16 = 0, 1

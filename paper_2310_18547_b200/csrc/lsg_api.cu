@@ -230,11 +230,11 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   else if (forced_mt == 1 || forced_mt == 8)
     pl.mt = forced_mt;
   else
-    pl.mt = s_n <= n_seg ? 1 : 8;
+    pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
   if (kernel == kKBgmv) {
     pl.row_splits = 1;
     pl.clusters = s_n;
-  } else if (pl.mt > 1 && !(g_opt_no_tile_scan.load())) {
+  } else if ((pl.mt > 1 || s_n > n_seg) && !(g_opt_no_tile_scan.load())) {
     // one cluster per row tile, mapped on the device; sum_i ceil(len_i/MT) is
     // at most (s_n + n_seg*(MT-1))/MT, and never more than s_n
     pl.tile_scan = 1;
@@ -253,12 +253,17 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   // Single-tile clusters (every segment one tile) keep only A resident ahead of
   // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
   // (s_n == n_seg: every segment is one row, so every cluster has exactly one tile)
-  pl.alias_ab =
-      pl.mode == kFused && (kernel == kKBgmv || s_n == n_seg || pl.tile_scan) && !(g_opt_no_alias.load()) ? 1 : 0;
-  auto smem_for = [&](int c) {
+  // (only when keeping B resident as well would cost co-residency: three CTAs per SM)
+  const bool single_tile = kernel == kKBgmv || s_n == n_seg || pl.tile_scan;
+  auto smem_alias = [&](int c, int alias) {
     const int nqc = (nq + c - 1) / c, ncv = (ncvt + c - 1) / c;
-    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), pl.alias_ab).total);
+    return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), alias).total);
   };
+  auto alias_for = [&](int c) {
+    return pl.mode == kFused && single_tile && !(g_opt_no_alias.load()) && smem_alias(c, 0) > kCoresidentSmem ? 1
+                                                                                                                : 0;
+  };
+  auto smem_for = [&](int c) { return smem_alias(c, alias_for(c)); };
   // Split-K cluster size.  Candidates divide the chunk / column-group counts
   // (every CTA gets the same share).  Measured on B200 (profiles/README.md):
   // a launch runs best with about 128-256 CTAs in all, and clusters of 8-16
@@ -282,6 +287,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);
+  pl.alias_ab = alias_for(c);
   pl.cluster = c;
   pl.nqc_max = (nq + c - 1) / c;
   pl.ncv_max = (ncvt + c - 1) / c;

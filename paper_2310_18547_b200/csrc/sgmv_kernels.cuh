@@ -32,7 +32,13 @@ namespace lsg {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 256;
+#ifndef LSG_MIN_BLOCKS
+#define LSG_MIN_BLOCKS 3  // co-resident CTAs per SM the register budget is sized for (measured best)
+#endif
+#ifndef LSG_THREADS
+#define LSG_THREADS 256
+#endif
+constexpr int kThreads = LSG_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int KW = 128;     // rows of A (h_in elements) per canonical reduction chunk
 constexpr int kPieces = 4;  // A arrives in up to 4 bulk copies, one mbarrier each
@@ -128,8 +134,24 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
 __device__ __forceinline__ int split_lo(int i, int n, int c) { return (i * n) / c; }
 __device__ __forceinline__ int split_owner(int q, int n, int c) { return ((q + 1) * c - 1) / n; }
 
+// s = ((0 + v[0]) + v[stride]) + ... + v[(n-1)*stride], in that order (the
+// canonical ascending-chunk sum).  Loads are batched 16 at a time so the chain
+// costs one shared-memory latency per batch instead of one per term.
+__device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) {
+  float s = 0.f;
+  for (int q0 = 0; q0 < n; q0 += 16) {
+    float t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = q0 + j < n ? v[(q0 + j) * stride] : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (q0 + j < n) s += t[j];
+  }
+  return s;
+}
+
 template <typename T, int R, int MT, int MODE>
-__global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
+__global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
   static_assert(R == 8 || R == 16 || R == 32 || R == 64, "fast path ranks");
   constexpr int VPR = R / 8;       // 16-byte vectors per A row
   constexpr int RPI = 32 / VPR;    // A rows covered by one warp instruction
@@ -312,6 +334,8 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         bulk_prefetch_l2(Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16));
     } else if (kEx && warp == b_warp && ncv > 0) {
       const T* B = Bslice;
+      if (kSh && (p.exp_flags & 64))  // experiment: queue B behind A (A is needed first)
+        for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], wphase);
       if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
       __syncwarp();
       const uint64_t pol = l2_evict_first_policy();
@@ -323,6 +347,20 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
           bulk_g2s_hint(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
                         &bars[kBarB], pol);
       }
+    }
+    // Activations of the first tile: warm L2 now, ahead of the PDL wait.  After the
+    // wait they then come from L2 instead of queueing in HBM behind the weight
+    // streams of the launches that follow.  A prefetch is only a cache hint (L2 is
+    // the coherence point), so this is safe even when the preceding kernel is still
+    // writing x or y.
+    if (first_item && warp == 2 && !(p.exp_flags & 32)) {
+      const int r0 = seg_begin + first_tile * MT, rows = min(MT, seg_end - r0);
+      if (kSh && lane < rows && nqc > 0)
+        bulk_prefetch_l2(static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + lane) * p.ldx + q0 * KW,
+                         static_cast<uint32_t>(ndl * sizeof(T)));
+      if (kEx && lane >= 16 && lane - 16 < rows && ncv > 0)
+        bulk_prefetch_l2(static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + lane - 16) * p.ldy + cv0 * 8,
+                         static_cast<uint32_t>(ncv * 16));
     }
     LSG_TRACE(2);
     if (p.exp_flags & 8) {  // experiment: weight stream only
@@ -337,6 +375,20 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
       if constexpr (kSh) cluster_wait();
       return;
+    }
+    // Cluster-window addresses this lane pushes its chunk partials to (one-round
+    // reduction, C <= RPI: lane group g sends half h to CTA (g + h) % RPI).
+    int push_dst[2] = {C, C};
+    uint32_t push_recv[2] = {0, 0}, push_bar[2] = {0, 0};
+    if (kSh && red_all && C <= RPI) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        push_dst[h] = (lane / VPR + h) % RPI;
+        if (push_dst[h] < C) {
+          push_recv[h] = mapa_u32(recv, static_cast<uint32_t>(push_dst[h]));
+          push_bar[h] = mapa_u32(&bars[kBarRed], static_cast<uint32_t>(push_dst[h]));
+        }
+      }
     }
     // x, v and y may be produced by the preceding kernel: wait for it here
     // (returns at once after the first item).
@@ -353,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       if constexpr (kSh) {
         const int nv = ndl / 8;  // 16-byte vectors per x row slice
         for (int i = tid; i < rows * nv; i += kThreads) {
-          const int m = i / nv, c = i - m * nv;
+          const int m = MT == 1 ? 0 : i / nv, c = i - m * nv;
           cp_async16(x_sm + m * ndl + c * 8,
                      static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW + c * 8);
         }
@@ -361,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
       cp_async_commit();
       if constexpr (kEx) {
         for (int i = tid; i < rows * ncv; i += kThreads) {
-          const int m = i / ncv, c = i - m * ncv;
+          const int m = MT == 1 ? 0 : i / ncv, c = i - m * ncv;
           cp_async16(y_sm + m * ncv + c,
                      static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + c) * 8);
         }
@@ -383,6 +435,10 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         if (first) cluster_wait();  // every peer's barriers are initialised
         first = false;
         LSG_TRACE(5);
+        if (p.trace != nullptr && tid == 0) {  // trace only: when did all of A land?
+          for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], wphase);
+          LSG_TRACE(12);
+        }
         // ---- shrink: per-chunk partials P_q[m, k], pushed to the reducers ----------
         const int rowoff = lane / VPR, vec = lane % VPR;
         const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
@@ -391,10 +447,9 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         // CTA or tile size computes it.
         const int nunits = nqc * rows;
         for (int u = warp; u < nunits; u += kWarps) {
-          const int ql = u / rows, m = u - ql * rows;
-          int piece = 0;  // wait for the piece holding chunk ql (no-op once it has landed)
-          while (((piece + 1) * nqc) / npieces <= ql) ++piece;
-          mbar_wait(&bars[piece], wphase);
+          const int ql = MT == 1 ? u : u / rows, m = MT == 1 ? 0 : u - ql * rows;
+          // wait for the piece holding chunk ql (no-op once it has landed)
+          mbar_wait(&bars[split_owner(ql, nqc, npieces)], wphase);
           float acc[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = 0.f;
@@ -408,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
           }
+          if (u == warp) LSG_TRACE(9);  // warp 0: FMA chain of its first unit done
 #pragma unroll
           for (int off = VPR; off < 32; off <<= 1)
 #pragma unroll
@@ -421,7 +477,11 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int o = m * R + vec * 8 + h * 4;
-            if (red_all) {
+            if (red_all && C <= RPI) {  // at most one destination per (lane, h): precomputed windows
+              if (push_dst[h] < C)
+                st_async_v4(push_recv[h] + static_cast<uint32_t>((q * MT * R + o) * 4), acc[h * 4 + 0], acc[h * 4 + 1],
+                            acc[h * 4 + 2], acc[h * 4 + 3], push_bar[h]);
+            } else if (red_all) {
               const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
               for (int dst = (g + h) % RPI; dst < C; dst += RPI) {
                 uint32_t ra, rb;
@@ -437,11 +497,10 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
                           mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
             }
           }
+          if (u == warp) LSG_TRACE(13);  // warp 0: first unit pushed
         }
-        LSG_TRACE(12);
         if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
         __syncthreads();
-        LSG_TRACE(13);
         if (kEx && alias_ab && warp == b_warp && ncv > 0) {
           // A is consumed: bring the (L2-warm) B slice into the same shared memory
           if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
@@ -457,13 +516,13 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         if (red_all) {
           for (int o = tid; o < no; o += kThreads) {
             float s = 0.f;
-            for (int q = 0; q < p.nq; ++q) s += recv[(q * MT) * R + o];
+            s = ordered_sum(recv + o, MT * R, p.nq);
             V_sm[o] = s;
           }
         } else {
           for (int o = o0 + tid; o < o1; o += kThreads) {
             float s = 0.f;
-            for (int q = 0; q < p.nq; ++q) s += recv[q * slice_max + (o - o0)];
+            s = ordered_sum(recv + (o - o0), slice_max, p.nq);
             if constexpr (MODE == kShrink) {
               const int m = o / R;
               p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
@@ -485,7 +544,6 @@ __global__ void __launch_bounds__(kThreads, 2) sgmv_fast_kernel(const __grid_con
         LSG_TRACE(8);
         cp_async_wait<0>();  // this thread's y vectors
         __syncthreads();     // V_sm and every y vector visible
-        LSG_TRACE(9);
         // ---- expand: y[m, n] += sum_k v[m, k] B[k, n] ---------------------------
         if (ncv > 0) {
           mbar_wait(&bars[kBarB], wphase);

@@ -15,7 +15,7 @@ if [[ $what == all || $what == bench ]]; then
   timeout 600 python bench.py --steps 50 --warmup 5 ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench=$?" >> $st
 fi
 if [[ $what == all || $what == ncu ]]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:lsg -c 224 --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:sgmv -c 224 --csv \
     --log-file gpurun_out/launches.csv python bench.py --profile --warmup 1 --sites 224 ${BENCH_ARGS:-} > gpurun_out/ncu_launch.log 2>&1
   echo "ncu_launch=$?" >> $st
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_fast -s 20 -c 2 \

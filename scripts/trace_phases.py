@@ -20,7 +20,7 @@ from paper_2310_18547_b200 import _lib  # noqa: E402
 from bench import segments  # noqa: E402
 
 PHASES = ["entry", "metadata", "tma_issued", "pdl_wait_done", "x_landed", "cluster_ready", "shrink_pushed",
-          "partials_in", "v_ready", "y_landed", "b_landed", "tile_done", "units_done", "cta_synced"]
+          "partials_in", "v_ready", "w0_fma_done", "b_landed", "tile_done", "a_landed", "w0_pushed"]
 
 
 def main():
@@ -33,7 +33,9 @@ def main():
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--sites", type=int, default=64)
     ap.add_argument("--graph", type=int, default=1, help="1: trace inside a CUDA-graph replay (steady state)")
+    ap.add_argument("--no-l2-staging", type=int, default=0)
     a = ap.parse_args()
+    lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, a.no_l2_staging)
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     h, r = a.hidden, a.rank
@@ -87,6 +89,17 @@ def main():
             print(f"  {i:2d} {name:15s} median {col.median().item():7.2f} us   max {col.max().item():7.2f} us")
     end = ent + rel[valid, 11] * 1e3
     print(f"first entry -> last tile_done: {(end.max() - ent.min()).item() / 1e3:.2f} us")
+    # per-CTA phase-to-phase deltas (clock64, exact; the globaltimer anchors below
+    # are quantised)
+    print("per-CTA deltas (us): median / p90 / max")
+    for a_, b_, name in ((3, 4, "wait -> x landed"), (3, 12, "wait -> A landed"), (4, 5, "x -> cluster ready"),
+                         (12, 9, "A landed -> w0 FMA done"), (9, 13, "w0 butterfly + push"),
+                         (13, 7, "w0 pushed -> partials in"), (7, 8, "reduce"), (8, 10, "v -> B landed"),
+                         (10, 11, "expand + store"), (3, 11, "wait -> tile done")):
+        ok = (t[valid, a_] != 0) & (t[valid, b_] != 0)
+        d = (rel[valid, b_] - rel[valid, a_])[ok]
+        if d.numel():
+            print(f"  {name:26s} {d.median().item():6.2f} {d.quantile(0.9).item():6.2f} {d.max().item():6.2f}")
     # absolute timeline anchored at the earliest return from griddepcontrol.wait
     # (= the previous launch's completion in a back-to-back stream)
     absu = ent.unsqueeze(1) / 1e3 + rel[valid]  # us
