@@ -93,7 +93,8 @@ def test_launch_planning_is_host_only():
     assert info.path == 0 and info.tile_rows == 1 and info.cluster >= 2
     assert info.smem_bytes <= 227 * 1024
     assert L.lsg_query_launch(C.byref(t), 1, 64, _lib.KERNEL_FUSED, C.byref(info)) == 0  # Identical
-    assert info.tile_rows == 8 and info.grid_ctas <= 148 * 2
+    # one row per cluster for every popularity (tile-scan); co-resident at 3 CTAs/SM
+    assert info.tile_rows == 1 and info.grid_ctas <= 148 * 2 and info.smem_bytes <= 75 * 1024
     t2 = _table(h_in=136)
     assert L.lsg_query_launch(C.byref(t2), 4, 4, _lib.KERNEL_FUSED, C.byref(info)) == 0
     assert info.path == 1  # h_in not a multiple of 128 -> generic kernel
