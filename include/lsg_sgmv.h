@@ -13,6 +13,7 @@
  *                         (the per-row gather formulation, one adapter slot per row)
  *   lsg_build_segments <- lorasim::plan_batch grouping             core/src/simulator.cpp:267-309,
  *                         and the per-row gather loop              sgmv.cpp:195-203
+ *   lsg_partition_segments <- Scheduler::place (request -> GPU)    core/src/scheduler.cpp:12-29
  *
  * Mapping from the reference's value types:
  *   Segments::boundaries() (sgmv.hpp:28, size_t)  -> seg_starts[n+1] int32, device memory
@@ -148,6 +149,27 @@ int lsg_gather_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
                     const int32_t* row_perm, int32_t rows, int32_t cols, lsg_stream_t stream);
 int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
                      const int32_t* row_perm, int32_t rows, int32_t cols, lsg_stream_t stream);
+
+/* Request-partitioned multi-GPU plan (host memory in and out; no device work).
+ * Replaces, for one decode step, the reference's request-level placement of
+ * requests onto GPUs (core/src/scheduler.cpp:12-29): rows are independent
+ * (sgmv.cpp:108-116, 125-134), so a batch shards with no collective.  Whole
+ * segments are placed (one adapter's weights read once); a segment larger than
+ * the per-rank byte share is cut into row ranges.  Pieces are assigned by LPT
+ * greedy on the algorithmic bytes rows*(h_in+h_out)*e + (h_in+h_out)*rank*e
+ * (cost_model.cpp:13-19, :59), largest first onto the least-loaded rank.
+ * Output: *num_pieces pieces ordered by (rank, segment, row); each rank's pieces
+ * are its local batch.  If max_pieces is too small, returns LSG_EINVAL with
+ * *num_pieces = the count needed (at most num_segments + world). */
+typedef struct lsg_piece {
+  int32_t rank;    /* owning rank */
+  int32_t seg;     /* segment index in the global batch */
+  int32_t row0;    /* first global row */
+  int32_t row1;    /* one past the last global row */
+} lsg_piece;
+int lsg_partition_segments(const int32_t* seg_starts /* host, n+1 */, int32_t num_segments, int32_t h_in,
+                           int32_t h_out, int32_t rank, int32_t elem_bytes, int32_t world, int32_t max_pieces,
+                           lsg_piece* pieces, int32_t* num_pieces);
 
 /* Tuning / test hooks. */
 typedef enum {

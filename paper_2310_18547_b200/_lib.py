@@ -24,7 +24,7 @@ EXPORTED = (
     "lsg_sgmv", "lsg_sgmv_ws", "lsg_sgmv_workspace_size", "lsg_sgmv_shrink", "lsg_sgmv_expand", "lsg_bgmv",
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
-    "lsg_last_error", "lsg_version", "lsg_set_trace",
+    "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments",
 )
 
 
@@ -47,6 +47,12 @@ class WeightTable(C.Structure):
 
 class LaunchInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("path", "cluster", "tile_rows", "row_splits", "grid_ctas", "smem_bytes")]
+
+
+class Piece(C.Structure):
+    """Mirror of ``lsg_piece``."""
+
+    _fields_ = [(n, C.c_int32) for n in ("rank", "seg", "row0", "row1")]
 
 
 class LsgError(RuntimeError):
@@ -88,6 +94,8 @@ def lib() -> C.CDLL:
         L.lsg_last_error.restype = C.c_char_p
         L.lsg_version.restype = C.c_int
         L.lsg_set_trace.argtypes = [vp, i32]
+        L.lsg_partition_segments.argtypes = [C.POINTER(i32), i32, i32, i32, i32, i32, i32, i32,
+                                             C.POINTER(Piece), C.POINTER(i32)]
         _lib = L
     return _lib
 

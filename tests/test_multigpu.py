@@ -1,0 +1,145 @@
+"""Multi-GPU host logic on CPU: the request partitioner and the TP
+expand all-gather, exercised with world_size 2 over gloo.
+
+The product path runs the CUDA kernels on every rank; on CPU the per-rank compute
+is the fp64 oracle (test infrastructure only), which is enough to prove the host
+logic: the plan covers every row exactly once, per-rank batches reassemble into
+the single-process result bit for bit, and the TP column shards gather into the
+unsharded expand.  The GPU side of the same property (partitioned kernel output
+== single-GPU kernel output, bitwise) is in tests/test_sgmv_gpu.py.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.oracle import DISTINCT, IDENTICAL, SKEWED, UNIFORM
+from paper_2310_18547_b200 import partition as part
+from paper_2310_18547_b200 import tp as tpmod
+from tests._util import oracle, random_problem, segments_for
+
+
+def _bytes(rows, h_in, h_out, r, e=2):
+    return rows * (h_in + h_out) * e + (h_in + h_out) * r * e
+
+
+@pytest.mark.parametrize("pop", [DISTINCT, UNIFORM, SKEWED, IDENTICAL])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("batch", [1, 7, 64])
+def test_plan_covers_every_row_once_and_balances(pop, world, batch):
+    bounds, _, _ = segments_for(pop, batch, 11)
+    h, r = 4096, 16
+    plan = part.partition_segments(bounds.astype(np.int32), h, h, r, world)
+    rows = np.zeros(batch, dtype=np.int64)
+    loads = np.zeros(world, dtype=np.int64)
+    for rank, seg, r0, r1 in plan:
+        assert 0 <= rank < world
+        assert bounds[seg] <= r0 < r1 <= bounds[seg + 1]  # a piece stays inside its segment
+        rows[r0:r1] += 1
+        loads[rank] += _bytes(r1 - r0, h, h, r)
+    assert (rows == 1).all()
+    assert [p[0] for p in plan] == sorted(p[0] for p in plan)  # ordered by rank
+    # no two pieces of one segment on one rank (they would read the adapter twice)
+    keys = [(p[0], p[1]) for p in plan]
+    assert len(keys) == len(set(keys))
+    total = int(loads.sum())  # split segments pay their adapter once per piece
+    biggest = max(_bytes(r1 - r0, h, h, r) for _, _, r0, r1 in plan)
+    assert loads.max() <= -(-total // world) + biggest  # LPT bound
+
+
+def test_plan_distinct_is_exactly_even():
+    plan = part.partition_segments(np.arange(65, dtype=np.int32), 4096, 4096, 16, 8)
+    counts = np.bincount([p[0] for p in plan], minlength=8)
+    assert (counts == 8).all()
+
+
+def test_plan_identical_splits_rows():
+    plan = part.partition_segments(np.array([0, 64], dtype=np.int32), 4096, 4096, 16, 4)
+    assert plan == [(0, 0, 0, 16), (1, 0, 16, 32), (2, 0, 32, 48), (3, 0, 48, 64)]
+
+
+def test_plan_rejects_bad_input():
+    with pytest.raises(RuntimeError, match="seg_starts"):
+        part.partition_segments(np.array([1, 4], dtype=np.int32), 64, 64, 8, 2)
+    with pytest.raises(RuntimeError):
+        part.partition_segments(np.array([0, 4, 2], dtype=np.int32), 64, 64, 8, 2)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+
+def _partition_worker(rank, world, port, pop, batch):
+    _init(rank, world, port)
+    try:
+        h_in, h_out, r = 128, 96, 8
+        bounds, _, _ = segments_for(pop, batch, 5)
+        x, A, B = random_problem(h_in, h_out, r, bounds, 9)
+        rb = part.rank_batches(bounds.astype(np.int32), h_in, h_out, r, world)[rank]
+        o = oracle()
+        y_local = (o.lora_addon(x[rb.rows], rb.seg_starts.astype(np.uint64), A[rb.segs], B[rb.segs])
+                   if rb.num_rows else np.zeros((0, h_out)))
+        parts = [None] * world
+        dist.all_gather_object(parts, (rb, y_local))
+        if rank == 0:
+            y = part.scatter_rows_back(np.full((batch, h_out), np.nan), parts)
+            ref = o.lora_addon(x, bounds, A, B)
+            assert np.array_equal(y, ref), "partitioned result differs from the single-process oracle"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pop", [DISTINCT, SKEWED, IDENTICAL])
+def test_request_partitioned_world2_gloo_bit_exact(pop):
+    mp.spawn(_partition_worker, args=(2, _free_port(), pop, 37), nprocs=2, join=True)
+
+
+def _tp_worker(rank, world, port):
+    _init(rank, world, port)
+    try:
+        h, r = 64, 8
+        bounds, _, _ = segments_for(UNIFORM, 12, 3)
+        x, A, B = random_problem(h, h, r, bounds, 4)
+        y0 = np.random.default_rng(0).uniform(-1, 1, (12, h))
+        o = oracle()
+        # this rank's shard pool: A replicated, B column slice (fp64 CPU tensors, test stand-in)
+        a_t = torch.tensor(A)[:, None]          # [slots, layers=1, h, r]
+        b_t = torch.tensor(B)[:, None]          # [slots, layers=1, r, h]
+        b_shard = tpmod.shard_b(b_t, world, rank)
+
+        class ShardPool:  # the attributes tp_sgmv_allgather reads
+            h_out = b_shard.shape[-1]
+
+        def compute(stage, xx, pool, seg_starts, seg_slot, layer):
+            stage += torch.tensor(o.lora_addon(xx.numpy(), seg_starts.numpy().astype(np.uint64),
+                                               a_t[:, layer].numpy(), b_shard[:, layer].numpy()))
+
+        y = torch.tensor(y0)
+        tpmod.tp_sgmv_allgather(y, torch.tensor(x), ShardPool(), torch.tensor(bounds.astype(np.int64)),
+                                torch.arange(len(bounds) - 1), 0, compute=compute)
+        ref = y0 + o.lora_addon(x, bounds, A, B)
+        assert np.array_equal(y.numpy(), ref), f"rank {rank}: gathered TP output differs"
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_expand_allgather_world2_gloo_bit_exact():
+    mp.spawn(_tp_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+def test_tp_column_ranges():
+    assert tpmod.column_range(8192, 8, 3) == (3072, 4096)
+    with pytest.raises(ValueError):
+        tpmod.column_range(100, 8, 0)
