@@ -115,13 +115,15 @@ def workload_name(a):
     return f"{model}-lora h={a.hidden} r={a.rank} {shape} {a.kernel} ({a.dtype})"
 
 
-def bounds_for(a):
+def bounds_for(a, world=1):
+    """Segment boundaries of the (global) batch: ``world`` copies of the per-GPU batch."""
     if a.segments:
         b = [0]
-        for x in a.segments.split(","):
-            b.append(b[-1] + int(x))
+        for _ in range(world):
+            for x in a.segments.split(","):
+                b.append(b[-1] + int(x))
         return b
-    return segments(a.popularity, a.batch)
+    return segments(a.popularity, a.batch * world)
 
 
 # ----------------------------------------------------------------------------------
@@ -278,10 +280,16 @@ def main():
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, int(a.no_l2_staging))
     lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
-    bounds = bounds_for(a)
+    # Request-partitioned weak scaling: the global batch is `batch` rows per GPU; the
+    # partitioner (lsg_partition_segments) hands every rank whole segments (or row
+    # ranges of dominant ones) and each rank runs its share on its own replica of
+    # the adapter pool -- no collective on the data path.
+    from paper_2310_18547_b200.partition import rank_batches
+    gbounds = bounds_for(a, world)
+    mine = rank_batches(np.array(gbounds, dtype=np.int32), h, h, r, world)[rank]
+    bounds = [int(v) for v in mine.seg_starts]
+    batch = mine.num_rows
     nseg = len(bounds) - 1
-    # Request-partitioned weak scaling: every rank owns its own batch of `batch` rows
-    # and its own replica of the adapter pool -- no collective on the data path.
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
     nslots = max(a.slots, nseg)
     pool = lsg.AdapterPool(nslots, sites, h, h, r, dtype)
@@ -426,7 +434,8 @@ def main():
         "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": a.dtype + " (fp32 accumulate)", "data": "synthetic (U[-1,1) adapters/activations, random init)",
         "config": {"workload": workload_name(a), "model": "Llama-2-7B LoRA sites (h x h)", "hidden": h, "rank": r,
-                   "batch_per_gpu": batch, "global_batch": batch * world, "segments": nseg,
+                   "batch_per_gpu": a.batch, "global_batch": a.batch * world, "segments": nseg,
+                   "global_segments": len(gbounds) - 1, "rank0_rows": batch,
                    "popularity": a.popularity, "step": f"{sites} fused SGMV launches (7 sites x 32 layers), CUDA graph",
                    "parallelism": f"request-partitioned x{world} (no collective)",
                    "kernel": a.kernel, "pool_slots": nslots, "preset": a.preset or None,
