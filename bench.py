@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also print per-(popularity,batch) lines to stderr")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graph, no extras)")
+    ap.add_argument("--profile-graph", action="store_true",
+                    help="short run for ncu --graph-profiling graph: capture the step graph, replay it twice")
     pre, _ = ap.parse_known_args()
     ap.set_defaults(**PRESETS.get(pre.preset, {}))  # a preset sets defaults; explicit flags still win
     a = ap.parse_args()
@@ -329,6 +331,14 @@ def main():
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         step()
+    if a.profile_graph:
+        with torch.cuda.stream(stream):
+            graph.replay()
+            torch.cuda.nvtx.range_push("lsg_graph")  # ncu --nvtx --nvtx-include lsg_graph/
+            graph.replay()
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        return
     for _ in range(max(3, a.warmup)):
         graph.replay()
     torch.cuda.synchronize()
@@ -380,6 +390,7 @@ def main():
     extra["us_per_launch_no_pdl"] = ms_nopdl * 1e3 / sites
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     del flush
+
 
     # e2e through the public API: pinned host x in, host y out, every launch, every step
     e2e = None

@@ -34,7 +34,9 @@ def main():
     ap.add_argument("--sites", type=int, default=64)
     ap.add_argument("--graph", type=int, default=1, help="1: trace inside a CUDA-graph replay (steady state)")
     ap.add_argument("--no-l2-staging", type=int, default=0)
+    ap.add_argument("--tile-rows", type=int, default=0)
     a = ap.parse_args()
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, a.no_l2_staging)
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
