@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cluster", type=int, default=0, help="force the split-K cluster size (0 = library heuristic)")
     ap.add_argument("--tile-rows", type=int, default=0, help="force rows per tile, 1 or 8 (0 = heuristic)")
     ap.add_argument("--no-l2-staging", action="store_true", help="keep B resident from kernel entry")
+    ap.add_argument("--l2-staging", action="store_true", help="always stage B through L2 into A's smem")
     ap.add_argument("--no-tc", action="store_true", help="long segments stay on the CUDA-core kernel")
     ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
                     help="sgmv: segmented launch; bgmv: per-row adapter slots (decode BGMV)")
@@ -279,7 +280,7 @@ def main():
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
-    lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, int(a.no_l2_staging))
+    lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, 1 if a.no_l2_staging else -1 if a.l2_staging else 0)
     lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
     # Request-partitioned weak scaling: the global batch is `batch` rows per GPU; the

@@ -177,7 +177,9 @@ typedef enum {
   LSG_OPT_FORCE_CLUSTER = 1,  /* 0 (default): auto; else split-K cluster size 1..16 */
   LSG_OPT_FORCE_GENERIC = 2,  /* 1: use the generic (any-shape) kernels */
   LSG_OPT_FORCE_TILE_ROWS = 3, /* 0 (default): auto; else rows per tile (1 or 8) */
-  LSG_OPT_NO_L2_STAGING = 4,  /* 1: keep B resident in smem from entry (no L2 prefetch + reuse of A's smem) */
+  LSG_OPT_NO_L2_STAGING = 4,  /* 1: keep B resident in smem from entry; -1: always stage B through L2 into
+                                 A's smem (single-tile launches); 0 (default): stage only when B resident
+                                 would cost co-residency */
   LSG_OPT_NO_TENSOR_CORES = 5 /* 1: long segments stay on the CUDA-core kernel (no tcgen05 path) */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);

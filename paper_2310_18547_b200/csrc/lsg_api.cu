@@ -260,8 +260,9 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), alias).total);
   };
   auto alias_for = [&](int c) {
-    return pl.mode == kFused && single_tile && !(g_opt_no_alias.load()) && smem_alias(c, 0) > kCoresidentSmem ? 1
-                                                                                                                : 0;
+    const int o = g_opt_no_alias.load();  // 1: never, -1: always (single-tile launches), 0: when co-residency needs it
+    if (pl.mode != kFused || !single_tile || o > 0) return 0;
+    return o < 0 || smem_alias(c, 0) > kCoresidentSmem ? 1 : 0;
   };
   auto smem_for = [&](int c) { return smem_alias(c, alias_for(c)); };
   // Split-K cluster size.  Candidates divide the chunk / column-group counts
@@ -473,7 +474,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       if (value != 0 && value != 1 && value != 8) return fail(LSG_EINVAL, "lsg: tile rows must be 0, 1 or 8");
       g_opt_force_tile_rows = value;
       return LSG_OK;
-    case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value > 0 ? 1 : value < 0 ? -1 : 0; return LSG_OK;
     case LSG_OPT_NO_TENSOR_CORES: g_opt_no_tc = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
