@@ -199,7 +199,9 @@ int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t 
                      int32_t kernel /* 0 fused, 1 shrink, 2 expand, 3 bgmv */,
                      lsg_launch_info* info);
 
-/* Phase tracing (profiling aid, off by default).  device_buffer holds
+/* Phase tracing (profiling aid; only in instrumented builds compiled with
+ * -DLSG_INSTRUMENT, see scripts/build_variant.sh -- production builds return
+ * LSG_EUNSUPPORTED for a non-NULL buffer).  device_buffer holds
  * 2 * max_ctas * 16 u64.  Thread 0 of every CUDA-core fast-path CTA (up to
  * max_ctas, CTA index = blockIdx.y * C + rank) writes entries [0, max_ctas):
  * clock64() at the kernel's phase boundaries in slots 0..13, %globaltimer at

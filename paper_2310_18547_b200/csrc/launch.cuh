@@ -75,9 +75,9 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cu
   return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kernel), args);
 }
 
-template <typename T, int R, int MT, int MODE>
+template <typename T, int R, int MT, int MODE, int ITEM>
 int launch_fast_inst(const FastParams& p, const Plan& pl, cudaStream_t st) {
-  auto kern = sgmv_fast_kernel<T, R, MT, MODE>;
+  auto kern = sgmv_fast_kernel<T, R, MT, MODE, ITEM>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
@@ -110,12 +110,25 @@ int launch_fast_inst(const FastParams& p, const Plan& pl, cudaStream_t st) {
   return LSG_OK;
 }
 
+template <typename T, int R, int MODE>
+int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
+  if (pl.mt == 1) {
+    if (p.row_slot != nullptr) {
+      if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemBgmv>(p, pl, st);
+      return fail(LSG_EINVAL, "lsg: BGMV indexing is fused-only");
+    }
+    return pl.tile_scan ? launch_fast_inst<T, R, 1, MODE, kItemTileScan>(p, pl, st)
+                        : launch_fast_inst<T, R, 1, MODE, kItemRowSplit>(p, pl, st);
+  }
+  return pl.tile_scan ? launch_fast_inst<T, R, 8, MODE, kItemTileScan>(p, pl, st)
+                      : launch_fast_inst<T, R, 8, MODE, kItemRowSplit>(p, pl, st);
+}
+
 template <typename T, int MODE>
 int dispatch_rank_mt(const FastParams& p, const Plan& pl, int rank, cudaStream_t st) {
-#define LSG_CASE(R)                                                            \
-  case R:                                                                      \
-    return pl.mt == 1 ? launch_fast_inst<T, R, 1, MODE>(p, pl, st)             \
-                      : launch_fast_inst<T, R, 8, MODE>(p, pl, st);
+#define LSG_CASE(R) \
+  case R:           \
+    return dispatch_item<T, R, MODE>(p, pl, st);
   switch (rank) {
     LSG_CASE(8)
     LSG_CASE(16)

@@ -249,7 +249,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int nq = t->h_in / KW, ncvt = t->h_out / 8;
   // one-round reduction (every CTA receives every chunk partial) while that
   // receive buffer stays <= 16 KB; otherwise owner-sliced with a second round
-  auto red_all_for = [&](int c) { return pl.mode == kFused && nq * pl.mt * t->rank <= 4096 ? 1 : 0; };
+  auto red_all_for = [&](int c) { return pl.mode == kFused && (pl.mt == 1 || nq * pl.mt * t->rank <= 4096) ? 1 : 0; };
   // Single-tile clusters (every segment one tile) keep only A resident ahead of
   // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
   // (s_n == n_seg: every segment is one row, so every cluster has exactly one tile)
@@ -589,6 +589,9 @@ int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
 
 int lsg_set_trace(unsigned long long* device_buffer, int32_t max_ctas) {
   if (max_ctas < 0 || (max_ctas > 0 && device_buffer == nullptr)) return fail(LSG_EINVAL, "lsg_set_trace: bad buffer");
+#ifndef LSG_INSTRUMENT
+  if (max_ctas > 0) return fail(LSG_EUNSUPPORTED, "lsg_set_trace: this build has no phase tracing (-DLSG_INSTRUMENT)");
+#endif
   g_trace = max_ctas ? device_buffer : nullptr;
   g_trace_ctas = max_ctas;
   return LSG_OK;

@@ -80,9 +80,21 @@ struct FastParams {
 
 // Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
 // globaltimer at entry, slot 15: SM id).  Off unless lsg_set_trace() installed a buffer.
+// Phase tracing and the LSG_EXP experiment switches exist only in instrumented
+// builds (-DLSG_INSTRUMENT, scripts/build_variant.sh).  Production code is kept
+// lean on purpose: every CTA runs each phase's code once per launch, so code size
+// is instruction-fetch latency on the critical path (measured: dropping the
+// instrumentation alone took the headline launch from 4.49 to 4.11 us).
+#ifdef LSG_INSTRUMENT
+#define LSG_TRACE_ON (p.trace != nullptr)
+#define LSG_EXP_FLAGS p.exp_flags
+#else
+#define LSG_TRACE_ON false
+#define LSG_EXP_FLAGS 0
+#endif
 #define LSG_TRACE(i)                                                                                   \
   do {                                                                                                 \
-    if (p.trace != nullptr && threadIdx.x == 0) {                                                      \
+    if (LSG_TRACE_ON && threadIdx.x == 0) {                                                      \
       const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                            \
       if (cta_ < p.trace_ctas) p.trace[cta_ * 16 + (i)] = clock64();                                   \
     }                                                                                                  \
@@ -150,7 +162,11 @@ __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) 
   return s;
 }
 
-template <typename T, int R, int MT, int MODE>
+// How a cluster finds its work item (compile-time, so each instantiation carries
+// only its own decode path -- see the code-size note at LSG_INSTRUMENT).
+enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2 };
+
+template <typename T, int R, int MT, int MODE, int ITEM>
 __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
   static_assert(R == 8 || R == 16 || R == 32 || R == 64, "fast path ranks");
   constexpr int VPR = R / 8;       // 16-byte vectors per A row
@@ -164,7 +180,9 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   const int C = static_cast<int>(gridDim.x);
   const int crank = static_cast<int>(blockIdx.x);  // cluster dims (C,1,1), grid.x == C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int red_all = MODE == kFused ? p.red_all : 0;
+  // one-row tiles always use the one-round reduction (compile-time: the owner-sliced
+  // path is not even emitted into those instantiations)
+  const int red_all = MODE == kFused ? (MT == 1 ? 1 : p.red_all) : 0;
   const int alias_ab = MODE == kFused ? p.alias_ab : 0;
   const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all, alias_ab);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -175,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   float* recv = reinterpret_cast<float*>(smem + L.recv);
   float* V_sm = reinterpret_cast<float*>(smem + L.v);
 
-  if (p.trace != nullptr && tid == 0 && blockIdx.y * gridDim.x + blockIdx.x < p.trace_ctas) {
+  if (LSG_TRACE_ON && tid == 0 && blockIdx.y * gridDim.x + blockIdx.x < p.trace_ctas) {
     unsigned long long gt;
     uint32_t smid;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   bool first_item = true;
   for (int item = blockIdx.y;; item += gridDim.y, wphase ^= 1u) {
     int slot, seg_begin, seg_end, first_tile, tile_step;
-    if (p.row_slot != nullptr) {
+    if constexpr (ITEM == kItemBgmv) {
       const int row = item;
       if (row >= p.s_n) return;
       slot = p.row_slot[row];
@@ -215,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
       seg_end = row + 1;
       first_tile = 0;
       tile_step = 1;
-    } else if (p.tile_scan) {
+    } else if constexpr (ITEM == kItemTileScan) {
       // Tile t: walk the segments' tile counts ceil(len/MT) with a warp prefix
       // sum (32 segments per step) until t falls inside one.
       __shared__ int s_seg, s_tile;
@@ -271,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
       slot = p.seg_slot[s];
       if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return;  // tensor-core kernels'
     }
-    const bool last_item = !p.tile_scan;  // bgmv / row-split: one item per cluster
+    constexpr bool last_item = ITEM != kItemTileScan;  // bgmv / row-split: one item per cluster
     const int ntiles = (seg_end - seg_begin + MT - 1) / MT;
     if (first_tile >= ntiles) {
       if (last_item) return;
@@ -295,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     const int q0 = split_lo(crank, p.nq, C), nqc = split_lo(crank + 1, p.nq, C) - q0;
     const int cv0 = split_lo(crank, p.ncvt, C), ncv = split_lo(crank + 1, p.ncvt, C) - cv0;
     const int ndl = nqc * KW;  // this CTA's slice of h_in (x_sm row stride)
-    const int npieces = (p.exp_flags & 2) ? min(1, nqc) : min(kPieces, nqc);
+    const int npieces = (LSG_EXP_FLAGS & 2) ? min(1, nqc) : min(kPieces, nqc);
     const int slice_max = slice_floats(MT, R, C);
 
     if (first) {
@@ -310,14 +328,14 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     // arrives in kPieces chunk-aligned pieces with their own barriers so the
     // shrink starts on the first piece; B follows on one barrier.  Warp 0 issues
     // A, warp 1 issues B (one row per lane).
-    const int a_warp = (p.exp_flags & 4) ? 1 : 0, b_warp = (p.exp_flags & 4) ? 0 : (kSh ? 1 : 0);
+    const int a_warp = (LSG_EXP_FLAGS & 4) ? 1 : 0, b_warp = (LSG_EXP_FLAGS & 4) ? 0 : (kSh ? 1 : 0);
     if (kSh && warp == a_warp && nqc > 0) {
       const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
       if (lane < npieces) {
         const int c0 = (lane * nqc) / npieces, c1 = ((lane + 1) * nqc) / npieces;
         const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
         mbar_arrive_expect_tx(&bars[lane], bytes);
-        if (p.exp_flags & 1)
+        if (LSG_EXP_FLAGS & 1)
           bulk_g2s(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane]);
         else
           bulk_g2s_hint(A_sm + c0 * KW * R, A + c0 * KW * R, bytes, &bars[lane], l2_evict_first_policy());
@@ -334,13 +352,13 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         bulk_prefetch_l2(Bslice + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16));
     } else if (kEx && warp == b_warp && ncv > 0) {
       const T* B = Bslice;
-      if (kSh && (p.exp_flags & 64))  // experiment: queue B behind A (A is needed first)
+      if (kSh && (LSG_EXP_FLAGS & 64))  // experiment: queue B behind A (A is needed first)
         for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], wphase);
       if (lane == 0) mbar_arrive_expect_tx(&bars[kBarB], static_cast<uint32_t>(R * ncv * 16));
       __syncwarp();
       const uint64_t pol = l2_evict_first_policy();
       for (int k = lane; k < R; k += 32) {
-        if (p.exp_flags & 1)
+        if (LSG_EXP_FLAGS & 1)
           bulk_g2s(B_sm + k * ncv, B + static_cast<int64_t>(k) * p.h_out, static_cast<uint32_t>(ncv * 16),
                    &bars[kBarB]);
         else
@@ -353,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     // streams of the launches that follow.  A prefetch is only a cache hint (L2 is
     // the coherence point), so this is safe even when the preceding kernel is still
     // writing x or y.
-    if (first_item && warp == 2 && !(p.exp_flags & 32)) {
+    if (first_item && warp == 2 && !(LSG_EXP_FLAGS & 32)) {
       const int r0 = seg_begin + first_tile * MT, rows = min(MT, seg_end - r0);
       if (kSh && lane < rows && nqc > 0)
         bulk_prefetch_l2(static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + lane) * p.ldx + q0 * KW,
@@ -363,13 +381,13 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
                          static_cast<uint32_t>(ncv * 16));
     }
     LSG_TRACE(2);
-    if (p.exp_flags & 8) {  // experiment: weight stream only
+    if (LSG_EXP_FLAGS & 8) {  // experiment: weight stream only
       for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
       if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
       if constexpr (kSh) cluster_wait();
       return;
     }
-    if (p.exp_flags & 16) {  // experiment: weights + activations, no compute
+    if (LSG_EXP_FLAGS & 16) {  // experiment: weights + activations, no compute
       pdl_wait();
       for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], 0);
       if (kEx && ncv > 0) mbar_wait(&bars[kBarB], 0);
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     // reduction, C <= RPI: lane group g sends half h to CTA (g + h) % RPI).
     int push_dst[2] = {C, C};
     uint32_t push_recv[2] = {0, 0}, push_bar[2] = {0, 0};
-    if (kSh && red_all && C <= RPI) {
+    if (kSh && red_all && (RPI >= 16 || C <= RPI)) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         push_dst[h] = (lane / VPR + h) % RPI;
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         if (first) cluster_wait();  // every peer's barriers are initialised
         first = false;
         LSG_TRACE(5);
-        if (p.trace != nullptr && tid == 0) {  // trace only: when did all of A land?
+        if (LSG_TRACE_ON && tid == 0) {  // trace only: when did all of A land?
           for (int i = 0; i < npieces; ++i) mbar_wait(&bars[i], wphase);
           LSG_TRACE(12);
         }
@@ -477,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int o = m * R + vec * 8 + h * 4;
-            if (red_all && C <= RPI) {  // at most one destination per (lane, h): precomputed windows
+            if (red_all && (RPI >= 16 || C <= RPI)) {  // <= one destination per (lane, h); C <= 16
               if (push_dst[h] < C)
                 st_async_v4(push_recv[h] + static_cast<uint32_t>((q * MT * R + o) * 4), acc[h * 4 + 0], acc[h * 4 + 1],
                             acc[h * 4 + 2], acc[h * 4 + 3], push_bar[h]);

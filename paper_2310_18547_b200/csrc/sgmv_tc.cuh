@@ -67,9 +67,14 @@ struct TcExpandParams {
 
 // Shrink CTAs trace into entries [trace_ctas, 1.5 trace_ctas), expand CTAs into
 // [1.5 trace_ctas, 2 trace_ctas); 16 %globaltimer stamps each.
+#ifdef LSG_INSTRUMENT
+#define LSG_TC_TRACE_ON (p.trace != nullptr)
+#else
+#define LSG_TC_TRACE_ON false  // instrumented builds only (see sgmv_kernels.cuh)
+#endif
 #define LSG_TC_TRACE(base, i)                                                                        \
   do {                                                                                               \
-    if (p.trace != nullptr && threadIdx.x == 0) {                                                    \
+    if (LSG_TC_TRACE_ON && threadIdx.x == 0) {                                                    \
       const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                          \
       if (cta_ < p.trace_ctas / 2) {                                                                 \
         unsigned long long gt_;                                                                      \

@@ -1,4 +1,7 @@
-"""Per-phase timeline of one fused SGMV launch inside a back-to-back stream.
+"""Needs an instrumented build: scripts/build_variant.sh instr -DLSG_INSTRUMENT, then
+LSG_LIB_OVERRIDE=build/variants/instr/libsgmv_b200.so.
+
+Per-phase timeline of one fused SGMV launch inside a back-to-back stream.
 
 Uses the library's phase trace (lsg_set_trace): thread 0 of every CTA stamps
 clock64 at the kernel's phase boundaries.  Prints, per phase, the median and
