@@ -273,9 +273,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # One process per GPU.  LSG_BENCH_BACKEND=gloo (test only) lets the N>1 code path
+    # run with several ranks sharing one GPU; the product path is NCCL.
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LSG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     dtype = torch.float16 if a.dtype == "fp16" else torch.bfloat16
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
@@ -362,7 +369,7 @@ def main():
             ms = t.item()
         return ms
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         ms = timed(graph.replay, a.steps)
     ms_step = ms / a.steps
     us_site = ms_step * 1e3 / sites  # per-rank device time per launch

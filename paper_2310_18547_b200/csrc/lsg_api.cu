@@ -361,7 +361,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
     if (prepare_long_segments(lp, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, ws, ws_bytes))
       skip_long = kTcMinRows;
   }
-  const Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
+  Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
+  // With the long segments on the tensor cores, the short ones have at most n_seg
+  // segments' worth of work items in practice: size the tile-scan grid by that
+  // (clusters loop over further tiles) instead of by s_n.
+  if (skip_long && pl.tile_scan) pl.clusters = std::min(pl.clusters, std::max(1, n_seg));
 
   FastParams p{};
   p.y = y;

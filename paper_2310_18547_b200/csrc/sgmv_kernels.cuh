@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   constexpr int kBarB = kPieces, kBarRed = kPieces + 1, kBarV = kPieces + 2;
 
   extern __shared__ __align__(128) uint8_t smem[];
+  // A CTA that leaves without work still waits for the preceding grid first: with
+  // PDL a grid's completion must imply its predecessor's (the next kernel on the
+  // stream waits only for this one).
+  auto exit_after_wait = [] { pdl_wait(); };
   const int C = static_cast<int>(gridDim.x);
   const int crank = static_cast<int>(blockIdx.x);  // cluster dims (C,1,1), grid.x == C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     int slot, seg_begin, seg_end, first_tile, tile_step;
     if constexpr (ITEM == kItemBgmv) {
       const int row = item;
-      if (row >= p.s_n) return;
+      if (row >= p.s_n) return exit_after_wait();
       slot = p.row_slot[row];
       seg_begin = row;
       seg_end = row + 1;
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         }
       }
       __syncthreads();
-      if (s_seg < 0) return;  // past the last tile
+      if (s_seg < 0) return exit_after_wait();  // past the last tile
       // A later item reuses every buffer: the whole cluster finishes the previous one first.
       if (!first_item) {
         if constexpr (kSh) cluster_sync();
@@ -281,18 +285,18 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
       slot = p.seg_slot[s];
     } else {
       const int s = item / p.row_splits;
-      if (s >= p.n_seg) return;
+      if (s >= p.n_seg) return exit_after_wait();
       first_tile = item - s * p.row_splits;
       tile_step = p.row_splits;
       seg_begin = p.seg_starts[s];
       seg_end = p.seg_starts[s + 1];
       slot = p.seg_slot[s];
-      if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return;  // tensor-core kernels'
+      if (p.skip_long > 0 && seg_end - seg_begin >= p.skip_long) return exit_after_wait();  // tensor-core kernels'
     }
     constexpr bool last_item = ITEM != kItemTileScan;  // bgmv / row-split: one item per cluster
     const int ntiles = (seg_end - seg_begin + MT - 1) / MT;
     if (first_tile >= ntiles) {
-      if (last_item) return;
+      if (last_item) return exit_after_wait();
       wphase ^= 1u;  // no weights were requested for this item: keep the barrier phase
       continue;
     }
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
           for (int i = tid; i < rows * R; i += kThreads) p.v_out[static_cast<int64_t>(r0) * R + i] = 0.f;
         }
       }
-      if (last_item) return;
+      if (last_item) return exit_after_wait();
       wphase ^= 1u;  // no weights were requested for this item: keep the barrier phase
       continue;
     }
