@@ -428,6 +428,13 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
     prefetch_tmap(&p.tmap_y);
   }
   if (warp == 0) tmem_alloc<kTcNT>(tmem_slot);
+  // y_old: written only by kernels before the shrink, which all completed before
+  // the shrink triggered this launch -- staged ahead of the wait for v.
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bars[0], 4 * kTcBox);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_2d(smem + L::kY + b * kTcBox, &p.tmap_y, n0 + b * kTcKB, r0, &bars[0]);
+  }
   // ---- B block [R x 256] (weights) -> MN-major SW128 atoms: 64-col atom na, k-group kg:
   //      na*(R/8)*1024 + kg*1024 + (k%8)*128 + swizzled 16-byte chunk
   {
@@ -447,13 +454,6 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
       *reinterpret_cast<uint4*>(smem + L::kB + na * (R / 8) * 1024 + (k / 8) * 1024 + (k % 8) * 128 +
                                 ((jj ^ (k % 8)) * 16)) = vb[j];
     }
-  }
-  // y_old: written only by kernels before the shrink, which all completed before
-  // the shrink triggered this launch -- staged ahead of the wait for v.
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bars[0], 4 * kTcBox);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) tma_load_2d(smem + L::kY + b * kTcBox, &p.tmap_y, n0 + b * kTcKB, r0, &bars[0]);
   }
   fence_proxy_async_smem();
   tc_fence_before();

@@ -38,13 +38,20 @@ def main():
     ap.add_argument("--graph", type=int, default=1, help="1: trace inside a CUDA-graph replay (steady state)")
     ap.add_argument("--no-l2-staging", type=int, default=0)
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--segments", default="", help="explicit segment sizes (overrides popularity/batch)")
     a = ap.parse_args()
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, a.no_l2_staging)
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     h, r = a.hidden, a.rank
-    bounds = segments(a.popularity, a.batch)
+    if a.segments:
+        bounds = [0]
+        for v in a.segments.split(","):
+            bounds.append(bounds[-1] + int(v))
+        a.batch = bounds[-1]
+    else:
+        bounds = segments(a.popularity, a.batch)
     n = len(bounds) - 1
     pool = lsg.AdapterPool(n, a.sites, h, h, r, torch.float16)
     pool.a.uniform_(-1, 1)
