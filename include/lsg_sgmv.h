@@ -180,7 +180,9 @@ typedef enum {
   LSG_OPT_NO_L2_STAGING = 4,  /* 1: keep B resident in smem from entry; -1: always stage B through L2 into
                                  A's smem (single-tile launches); 0 (default): stage only when B resident
                                  would cost co-residency */
-  LSG_OPT_NO_TENSOR_CORES = 5 /* 1: long segments stay on the CUDA-core kernel (no tcgen05 path) */
+  LSG_OPT_NO_TENSOR_CORES = 5, /* 1: long segments stay on the CUDA-core kernel (no tcgen05 path) */
+  LSG_OPT_TC_SPLIT = 6         /* 1: rank-16 long segments use the two-kernel tensor-core path
+                                  (shrink, then expand through a workspace) instead of the fused one */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

@@ -66,3 +66,29 @@ int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cu
 }
 
 }  // namespace lsg
+
+namespace lsg {
+
+template <typename T>
+static int launch_tc_fused_inst(const TcFusedParams& p, int C, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_fused_kernel<T>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc fused smem)");
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc fused cluster)");
+    configured = true;
+  }
+  const dim3 grid(static_cast<unsigned>(C), static_cast<unsigned>(tiles), 1);
+  const int smem = static_cast<int>(tcf_layout(p.kcs_max, p.compact).total);
+  const cudaError_t e = launch_ex(kern, grid, dim3(kTcThreads), smem, C, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_fused_kernel launch");
+}
+
+int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st) {
+  return dtype == LSG_F16 ? launch_tc_fused_inst<__half>(p, C, tiles, st)
+                          : launch_tc_fused_inst<__nv_bfloat16>(p, C, tiles, st);
+}
+
+}  // namespace lsg

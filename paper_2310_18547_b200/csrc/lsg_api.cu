@@ -46,6 +46,7 @@ std::atomic<int> g_opt_force_tile_rows{0};
 std::atomic<int> g_opt_no_alias{0};
 std::atomic<int> g_opt_no_tile_scan{0};
 std::atomic<int> g_opt_no_tc{0};
+std::atomic<int> g_opt_tc_split{0};
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -81,7 +82,10 @@ int tc_nq(const lsg_weight_table* t) {
   return 0;
 }
 
+int tc_fused_c(const lsg_weight_table* t, int* compact);
+
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
+  if (tc_fused_c(t, nullptr) > 0 && !g_opt_tc_split.load()) return 0;  // the fused kernel keeps v on chip
   return tc_nq(t) > 0 && s_n >= kTcMinRows ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
@@ -126,15 +130,65 @@ bool encode_rows_map(CUtensorMap* m, int dtype, const void* base, int cols, int 
 struct LongPlan {
   TcShrinkParams sp;
   TcExpandParams ep;
+  TcFusedParams fp;
   int nq = 0, tiles = 0;
+  int fused_c = 0;  // > 0: one fused tensor-core launch with clusters of fused_c CTAs
 };
+
+// Cluster size of the fused tensor-core kernel for this shape (0: not applicable).
+// Rank 16 only; every CTA expands at most two 256-column chunks.
+// Compact form (one chunk per CTA, y staged in the x ring; two CTAs per SM) when
+// the chunks fit one per CTA of a 16-CTA cluster, else two chunks per CTA.
+int tc_fused_c(const lsg_weight_table* t, int* compact = nullptr) {
+  if (t->rank != 16 || t->h_in % kTcKB != 0 || t->h_out % kTcNT != 0) return 0;
+  const int nch = t->h_out / kTcNT, nkb = t->h_in / kTcKB;
+  for (int c : {16, 8}) {
+    const int per = (nch + c - 1) / c;
+    if (per > 2 || nkb < c) continue;
+    const int kcs_max = ((nkb + c - 1) / c) * kTcKB, cp = per == 1 ? 1 : 0;
+    if (tcf_layout(kcs_max, cp).total <= static_cast<uint32_t>(kSmemBudget)) {
+      if (compact) *compact = cp;
+      return c;
+    }
+  }
+  return 0;
+}
 bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, int64_t ldx,
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
   const int nq = tc_nq(tbl);
-  if (nq == 0 || s_n < kTcMinRows || ws == nullptr || ws_bytes < tc_workspace_bytes(tbl, s_n) || !aligned16(ws))
-    return false;
+  if (nq == 0 || s_n < kTcMinRows) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
+  int compact = 0;
+  const int fc = g_opt_tc_split.load() ? 0 : tc_fused_c(tbl, &compact);
+  if (fc > 0) {
+    TcFusedParams& fp = lp.fp;
+    fp = TcFusedParams{};
+    if (!encode_rows_map(&fp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx) ||
+        !encode_rows_map(&fp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
+      return false;
+    lp.fused_c = fc;
+    lp.tiles = std::max(1, s_n / (kTcM / 2));
+    fp.y = y;
+    fp.ldy = ldy;
+    fp.a_ptr = tbl->a_ptr;
+    fp.b_ptr = tbl->b_ptr;
+    fp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+    fp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+    fp.seg_starts = seg_starts;
+    fp.seg_slot = seg_slot;
+    fp.n_seg = n_seg;
+    fp.s_n = s_n;
+    fp.num_slots = tbl->num_slots;
+    fp.h_in = tbl->h_in;
+    fp.h_out = tbl->h_out;
+    fp.kcs_max = ((tbl->h_in / kTcKB + fc - 1) / fc) * kTcKB;
+    fp.compact = compact;
+    fp.trace = g_trace;
+    fp.trace_ctas = g_trace_ctas;
+    return true;
+  }
+  if (ws == nullptr || ws_bytes < tc_workspace_bytes(tbl, s_n) || !aligned16(ws)) return false;
   TcShrinkParams& sp = lp.sp;
   TcExpandParams& ep = lp.ep;
   sp = TcShrinkParams{};
@@ -175,6 +229,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
 }
 
 int launch_long_segments(const LongPlan& lp, int dtype, int rank, cudaStream_t cs) {
+  if (lp.fused_c > 0) return launch_tc_fused(dtype, lp.fp, lp.fused_c, lp.tiles, cs);
   const int st = launch_tc_shrink(dtype, rank, lp.sp, lp.nq, lp.tiles, cs);
   if (st != LSG_OK) return st;
   return launch_tc_expand(dtype, rank, lp.ep, lp.tiles, cs);
@@ -485,6 +540,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       return LSG_OK;
     case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value > 0 ? 1 : value < 0 ? -1 : 0; return LSG_OK;
     case LSG_OPT_NO_TENSOR_CORES: g_opt_no_tc = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_TC_SPLIT: g_opt_tc_split = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -497,6 +553,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_FORCE_TILE_ROWS: return g_opt_force_tile_rows.load();
     case LSG_OPT_NO_L2_STAGING: return g_opt_no_alias.load();
     case LSG_OPT_NO_TENSOR_CORES: return g_opt_no_tc.load();
+    case LSG_OPT_TC_SPLIT: return g_opt_tc_split.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

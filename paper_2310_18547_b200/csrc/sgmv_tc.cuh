@@ -556,3 +556,322 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
 }
 
 }  // namespace lsg
+
+namespace lsg {
+
+// ---------------------------------------------------------------------------------------
+// Fused long-segment kernel (rank 16): ONE launch per call for all long-segment tiles.
+// A cluster of C CTAs serves one 128-row tile:
+//   shrink  CTA c: D1 (TMEM, fp32 128 x 16) = x[tile, K boxes of c] . A[K boxes of c]
+//           (x by TMA through a ring, A MN-major swizzled); row partials go to the
+//           row owners (st.async DSMEM), owners add the C partials in CTA order and
+//           broadcast their rows of v to the whole cluster -- v never leaves the chip;
+//   expand  CTA c: 256-column chunks j = c, c + C of y: D2 (TMEM, the 256 columns D1
+//           used -- D1 is consumed first, so two CTAs fit one SM's TMEM) = hi.B_j + lo.B_j
+//           (v split into 16-bit hi + lo), epilogue adds y_old (TMA-staged while the
+//           shrink runs) and stores the tile (TMA store; per-row stores on a
+//           segment's last, partial tile).
+// Canonical arithmetic for these rows: v = sum over CTAs c (ascending) of the MMA
+// partial over c's K boxes (C and the box split depend only on the shape);
+// y = rn(fp32(hi.B + lo.B) + y_old).
+// ---------------------------------------------------------------------------------------
+constexpr int kTcfStages = 4;  // x ring depth
+struct TcFusedParams {
+  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 128, SW128
+  CUtensorMap tmap_y;  // y [s_n, h_out], box 64 x 128, SW128
+  void* y;
+  int64_t ldy;
+  const void* const* a_ptr;
+  const void* const* b_ptr;
+  int64_t a_off, b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  int32_t n_seg, s_n, num_slots, h_in, h_out;
+  int32_t kcs_max;  // max K columns per CTA (multiple of 64)
+  int32_t compact;  // 1: one 256-column chunk per CTA, y staged in the x ring after the shrink (2 CTAs/SM)
+  unsigned long long* trace;
+  int32_t trace_ctas;
+};
+
+// Shared-memory plan (offsets from the 1024-aligned base), R = 16.
+struct TcfLayout {
+  uint32_t ring, y0, a, b, vhi, vlo, recv, vfull, bars, total;
+};
+__host__ __device__ inline TcfLayout tcf_layout(int kcs_max, int compact) {
+  TcfLayout L{};
+  L.ring = 0;                              // x ring; after the shrink: y staging of chunk 1 (or 0 if compact)
+  L.y0 = kTcfStages * kTcBox;              // y staging of chunk 0 (4 boxes, SW128)
+  L.a = compact ? L.y0 : L.y0 + 4 * kTcBox;  // A slice, kcs_max rows x 32 B (MN-major SW32)
+  L.b = L.a + static_cast<uint32_t>(kcs_max) * 32;  // B chunks: (1 or 2) x (16 x 256) MN-major SW128 atoms
+  L.vhi = L.b + (compact ? 1 : 2) * 16 * kTcNT * 2;
+  L.vlo = L.vhi + kTcM * 16 * 2;
+  L.recv = L.vlo + kTcM * 16 * 2;          // [C][128/C][16] fp32 row partials = 8 KB for any C
+  L.vfull = L.recv + kTcM * 16 * 4;        // [128][16] fp32 v of the tile
+  L.bars = L.vfull + kTcM * 16 * 4;
+  L.total = L.bars + 256 + 1024;           // + alignment slack
+  return L;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __grid_constant__ TcFusedParams p) {
+  constexpr int R = 16;
+  constexpr int fmt = std::is_same<T, __half>::value ? 0 : 1;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const TcfLayout L = tcf_layout(p.kcs_max, p.compact);
+  const int C = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  // bars: [0,4) full[s], [4,8) empty[s], 8 D1, 9 recv, 10 vfull, 11 y0, 12 y1, 13 D2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  float* recv = reinterpret_cast<float*>(smem + L.recv);
+  float* vfull = reinterpret_cast<float*>(smem + L.vfull);
+
+  LSG_TC_TRACE(0, 0);
+  pdl_launch_dependents();  // the next kernel only stages weights before its own wait
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  __syncthreads();
+  if (s_seg < 0) {  // past the last tile (the grid is an upper bound): keep the PDL chain
+    pdl_wait();
+    return;
+  }
+  const int slot = p.seg_slot[s_seg];
+  if (slot < 0 || slot >= p.num_slots) {  // no adapter: rows untouched
+    pdl_wait();
+    return;
+  }
+  const int seg_end = p.seg_starts[s_seg + 1];
+  const int r0 = p.seg_starts[s_seg] + s_tile * kTcM;
+  const int rows = min(kTcM, seg_end - r0);
+  const int nkb = p.h_in / kTcKB, kb0 = (c * nkb) / C, nk = ((c + 1) * nkb) / C - kb0;
+  const int nch = p.h_out / kTcNT, nmine = c < nch ? (nch - 1 - c) / C + 1 : 0;  // <= 2 (host checks)
+  const int rpo = kTcM / C;
+
+  if (tid == 0) {
+    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+    prefetch_tmap(&p.tmap_x);
+    prefetch_tmap(&p.tmap_y);
+  }
+  if (warp == 0) tmem_alloc<kTcNT>(tmem_slot);
+  // ---- weights (independent of the preceding kernel) --------------------------------
+  {  // A rows [kb0*64, (kb0+nk)*64) -> MN-major SW32: row k at k*32, 16-byte chunk c ^ swz<32>(k)
+    const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(kb0) * kTcKB * R;
+    const int total = nk * kTcKB * 2;  // 16-byte chunks
+    for (int base = 0; base < total; base += 8 * kTcThreads) {
+      uint4 va[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = base + j * kTcThreads + tid;
+        if (i < total) va[j] = ldg_nc_v4(A + static_cast<int64_t>(i) * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = base + j * kTcThreads + tid;
+        if (i < total) {
+          const int k = i >> 1, cc = i & 1;
+          *reinterpret_cast<uint4*>(smem + L.a + k * 32 + ((cc ^ swz<32>(k)) * 16)) = va[j];
+        }
+      }
+    }
+  }
+  for (int i = 0; i < nmine; ++i) {  // B chunk j -> MN-major SW128 atoms (as the two-kernel expand)
+    const int n0 = (c + i * C) * kTcNT;
+    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
+    constexpr int per = R * (kTcNT / 8) / kTcThreads;  // 4
+    uint4 vb[per];
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int e = j * kTcThreads + tid, k = e / (kTcNT / 8), cc = e - k * (kTcNT / 8);
+      vb[j] = ldg_nc_v4(B + static_cast<int64_t>(k) * p.h_out + cc * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      const int e = j * kTcThreads + tid, k = e / (kTcNT / 8), cc = e - k * (kTcNT / 8);
+      const int na = cc / 8, jj = cc % 8;
+      *reinterpret_cast<uint4*>(smem + L.b + i * (R * kTcNT * 2) + na * (R / 8) * 1024 + (k / 8) * 1024 +
+                                (k % 8) * 128 + ((jj ^ (k % 8)) * 16)) = vb[j];
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  cluster_arrive_relaxed();  // barrier inits -> the cluster (waited on before the first push)
+  LSG_TC_TRACE(0, 1);
+
+  pdl_wait();  // x and y_old may come from the preceding kernel
+  LSG_TC_TRACE(0, 2);
+  if (warp == 1 && lane == 0) {  // TMA producer: y chunk 0, the x ring, then y chunk 1
+    if (nmine > 0 && !p.compact) {
+      mbar_arrive_expect_tx(&bars[11], 4 * kTcBox);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        tma_load_2d(smem + L.y0 + b * kTcBox, &p.tmap_y, c * kTcNT + b * kTcKB, r0, &bars[11]);
+    }
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kTcfStages;
+      if (kb >= kTcfStages) mbar_wait(&bars[4 + s], ((kb / kTcfStages) - 1) & 1);
+      mbar_arrive_expect_tx(&bars[s], kTcBox);
+      tma_load_2d(smem + L.ring + s * kTcBox, &p.tmap_x, (kb0 + kb) * kTcKB, r0, &bars[s]);
+    }
+    const int ring_chunk = p.compact ? 0 : 1;  // the chunk staged in the ring once the shrink is done
+    if (nmine > ring_chunk) {
+      mbar_wait(&bars[8], 0);  // every shrink MMA has read its x box: the ring is free
+      mbar_arrive_expect_tx(&bars[11 + ring_chunk], 4 * kTcBox);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        tma_load_2d(smem + L.ring + b * kTcBox, &p.tmap_y, (c + ring_chunk * C) * kTcNT + b * kTcKB, r0,
+                    &bars[11 + ring_chunk]);
+    }
+  } else if (warp == 0 && lane == 0) {  // MMA issuer (shrink)
+    const uint32_t idesc = umma_idesc(fmt, kTcM, R);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kTcfStages;
+      mbar_wait(&bars[s], (kb / kTcfStages) & 1);
+      tc_fence_after();
+      const uint32_t xa = smem_u32(smem + L.ring + s * kTcBox);
+      const uint32_t aa = smem_u32(smem + L.a) + kb * kTcKB * 32;
+#pragma unroll
+      for (int ks = 0; ks < kTcKB / 16; ++ks) {
+        const uint64_t ad = umma_desc(xa + ks * 32, 16, 1024, kSw128);          // x: K-major SW128
+        const uint64_t bd = umma_desc(aa + ks * 16 * 32, 16, 8 * 32, kSw32);     // A: MN-major SW32
+        umma_f16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+      }
+      umma_commit(&bars[4 + s]);
+    }
+    umma_commit(&bars[8]);  // D1 complete (and the ring free)
+  }
+  __syncwarp();
+
+  // ---- cluster reduction of v: row partials -> owners -> every CTA ---------------------
+  cluster_wait();  // peers' barriers initialised
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bars[9], static_cast<uint32_t>(C * rpo * R * 4));
+    mbar_arrive_expect_tx(&bars[10], static_cast<uint32_t>(kTcM * R * 4));
+  }
+  mbar_wait(&bars[8], 0);
+  LSG_TC_TRACE(0, 3);
+  tc_fence_after();
+  {
+    const int m = tid;  // row of the tile = TMEM lane
+    const int owner = m / rpo, ml = m - owner * rpo;
+    float v[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16), v);
+    const uint32_t ra = mapa_u32(recv + (c * rpo + ml) * R, static_cast<uint32_t>(owner));
+    const uint32_t rb = mapa_u32(&bars[9], static_cast<uint32_t>(owner));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_async_v4(ra + j * 16, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3], rb);
+  }
+  mbar_wait(&bars[9], 0);
+  for (int qd = tid; qd < rpo * R / 4; qd += kTcThreads) {  // my rows' v, 4 columns per thread
+    const int ml = qd / (R / 4), k4 = (qd - ml * (R / 4)) * 4;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int cc = 0; cc < C; ++cc)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[e] += recv[(cc * rpo + ml) * R + k4 + e];
+    const float* lv = vfull + (c * rpo + ml) * R + k4;
+    for (int d = 0; d < C; ++d)
+      st_async_v4(mapa_u32(lv, static_cast<uint32_t>(d)), s[0], s[1], s[2], s[3],
+                  mapa_u32(&bars[10], static_cast<uint32_t>(d)));
+  }
+  mbar_wait(&bars[10], 0);
+  LSG_TC_TRACE(0, 4);
+  {  // v -> 16-bit hi + lo, K-major interleave (m,k) at (m/8)*256 + (k/8)*128 + (m%8)*16 + (k%8)*2
+    const int m = tid;
+#pragma unroll
+    for (int kg = 0; kg < R / 8; ++kg) {
+      float f[8], hf[8], lo[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = vfull[m * R + kg * 8 + e];
+      const uint4 hi = Cvt<T>::pack8(f);
+      Cvt<T>::unpack8(hi, hf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) lo[e] = f[e] - hf[e];
+      const uint32_t off = (m / 8) * (R / 8) * 128 + kg * 128 + (m % 8) * 16;
+      *reinterpret_cast<uint4*>(smem + L.vhi + off) = hi;
+      *reinterpret_cast<uint4*>(smem + L.vlo + off) = Cvt<T>::pack8(lo);
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+
+  // ---- expand: my 256-column chunks ----------------------------------------------------
+  for (int i = 0; i < nmine; ++i) {
+    const int n0 = (c + i * C) * kTcNT;
+    uint8_t* ybuf = smem + (i == 0 && !p.compact ? L.y0 : L.ring);
+    if (warp == 0 && lane == 0) {
+      tc_fence_after();
+      const uint32_t idesc = umma_idesc(fmt, kTcM, kTcNT);
+      const uint32_t bs = smem_u32(smem + L.b + i * (R * kTcNT * 2));
+      const uint64_t bd = umma_desc(bs, (R / 8) * 1024, 1024, kSw128);  // B: MN-major SW128
+      const uint64_t ah = umma_desc(smem_u32(smem + L.vhi), 128, (R / 8) * 128, kSwNone);
+      const uint64_t al = umma_desc(smem_u32(smem + L.vlo), 128, (R / 8) * 128, kSwNone);
+      umma_f16(tmem, ah, bd, idesc, 0u);
+      umma_f16(tmem, al, bd, idesc, 1u);
+      umma_commit(&bars[13]);
+    }
+    __syncwarp();
+    mbar_wait(&bars[11 + i], 0);
+    mbar_wait(&bars[13], i & 1);
+    LSG_TC_TRACE(0, 5 + i);
+    tc_fence_after();
+    const int m = tid;
+    uint8_t* yrow = ybuf + m * 128;  // + box * kTcBox + swizzled chunk
+#pragma unroll 4
+    for (int cc = 0; cc < kTcNT / 16; ++cc) {
+      float acc[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cc * 16, acc);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = (cc % 4) * 2 + h;
+        uint4* ptr = reinterpret_cast<uint4*>(yrow + (cc / 4) * kTcBox + ((j ^ (m & 7)) * 16));
+        float f[8];
+        Cvt<T>::unpack8(*ptr, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = acc[h * 8 + e] + f[e];
+        *ptr = Cvt<T>::pack8(f);
+      }
+    }
+    tc_fence_before();  // D2 reads done before the next chunk's MMA overwrites it
+    if (rows == kTcM) {
+      fence_proxy_async_smem();  // epilogue writes -> visible to the TMA store
+      __syncthreads();
+      if (tid == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) tma_store_2d(&p.tmap_y, ybuf + b * kTcBox, n0 + b * kTcKB, r0);
+        bulk_commit_group();
+      }
+    } else {
+      if (m < rows) {  // last tile of a segment: only the segment's rows
+        T* yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + n0;
+#pragma unroll 4
+        for (int e = 0; e < kTcNT / 8; ++e) {
+          const int b = e / 8, j = e % 8;
+          st_global_v4(yg + e * 8, *reinterpret_cast<const uint4*>(yrow + b * kTcBox + ((j ^ (m & 7)) * 16)));
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) bulk_wait_group0();  // TMA stores have read their staging before exit
+  LSG_TC_TRACE(0, 7);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<kTcNT>(tmem);
+  }
+}
+
+}  // namespace lsg

@@ -18,6 +18,10 @@ SHRINK = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "partials_in",
 EXPAND = ["entry", "weights_staged", "pdl_wait_done", "y_landed", "d2_ready", "end"]
 
 
+FUSED = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "v_ready", "chunk0_ready", "chunk1_ready",
+         "end"]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--segments", default="2048," + ",".join(["1"] * 31))
@@ -25,7 +29,9 @@ def main():
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--sites", type=int, default=16)
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--split", type=int, default=0, help="1: two-kernel path (LSG_OPT_TC_SPLIT)")
     a = ap.parse_args()
+    lsg.set_option(_lib.LSG_OPT_TC_SPLIT, a.split)
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lens = [int(v) for v in a.segments.split(",")]
     bounds = [0]
@@ -63,9 +69,10 @@ def main():
     torch.cuda.synchronize()
     allt = buf.view(2 * ctas, 16).cpu().double()
     t0 = None
-    for name, phases, part in (("shrink", SHRINK, allt[ctas:ctas + ctas // 2]),
-                               ("expand", EXPAND, allt[ctas + ctas // 2:])):
-        tv = part[part[:, 5] != 0]
+    groups = ((("shrink", SHRINK, allt[ctas:ctas + ctas // 2]), ("expand", EXPAND, allt[ctas + ctas // 2:]))
+              if a.split else (("fused", FUSED, allt[ctas:ctas + ctas // 2]),))
+    for name, phases, part in groups:
+        tv = part[part[:, len(phases) - 1] != 0]
         if not tv.numel():
             print(f"{name}: no traced CTAs")
             continue
