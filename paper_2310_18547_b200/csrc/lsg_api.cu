@@ -298,7 +298,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     pl.clusters = static_cast<int>(std::min<int64_t>(bound, s_n));
   } else {
     const int tiles_per_seg = (s_n + pl.mt * n_seg - 1) / (pl.mt * n_seg);
-    pl.row_splits = std::max(1, tiles_per_seg);
+    pl.row_splits = pl.mt == 1 ? 1 : std::max(1, tiles_per_seg);  // the MT=1 kernel assumes 1
     pl.clusters = n_seg * pl.row_splits;
   }
   const int nq = t->h_in / KW, ncvt = t->h_out / 8;

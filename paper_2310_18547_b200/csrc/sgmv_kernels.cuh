@@ -150,6 +150,7 @@ __device__ __forceinline__ int split_owner(int q, int n, int c) { return ((q + 1
 // canonical ascending-chunk sum).  Loads are batched 16 at a time so the chain
 // costs one shared-memory latency per batch instead of one per term.
 __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) {
+  __builtin_assume(n > 0);
   float s = 0.f;
   for (int q0 = 0; q0 < n; q0 += 16) {
     float t[16];
@@ -284,10 +285,12 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
       seg_end = p.seg_starts[s + 1];
       slot = p.seg_slot[s];
     } else {
-      const int s = item / p.row_splits;
+      // one-row tiles only take this path when s_n <= n_seg, where the planner
+      // always sets row_splits = 1 (compile-time: no division on the entry path)
+      const int s = MT == 1 ? item : item / p.row_splits;
       if (s >= p.n_seg) return exit_after_wait();
-      first_tile = item - s * p.row_splits;
-      tile_step = p.row_splits;
+      first_tile = MT == 1 ? 0 : item - s * p.row_splits;
+      tile_step = MT == 1 ? 1 : p.row_splits;
       seg_begin = p.seg_starts[s];
       seg_end = p.seg_starts[s + 1];
       slot = p.seg_slot[s];
@@ -536,10 +539,10 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         mbar_wait(&bars[kBarRed], phase);
         LSG_TRACE(7);
         if (red_all) {
-          for (int o = tid; o < no; o += kThreads) {
-            float s = 0.f;
-            s = ordered_sum(recv + o, MT * R, p.nq);
-            V_sm[o] = s;
+          if constexpr (MT * R <= kThreads) {  // one output per thread at most
+            if (tid < no) V_sm[tid] = ordered_sum(recv + tid, MT * R, p.nq);
+          } else {
+            for (int o = tid; o < no; o += kThreads) V_sm[o] = ordered_sum(recv + o, MT * R, p.nq);
           }
         } else {
           for (int o = o0 + tid; o < o1; o += kThreads) {
