@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--l2-staging", action="store_true", help="always stage B through L2 into A's smem")
     ap.add_argument("--no-tc", action="store_true", help="long segments stay on the CUDA-core kernel")
     ap.add_argument("--tc-split", action="store_true", help="two-kernel tensor-core path for rank-16 long segments")
+    ap.add_argument("--no-row-mode", action="store_true", help="segment-major decode for one-row tiles")
     ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
                     help="sgmv: segmented launch; bgmv: per-row adapter slots (decode BGMV)")
     ap.add_argument("--slots", type=int, default=0, help="adapter-pool slots (0 = one per segment)")
@@ -291,6 +292,7 @@ def main():
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, 1 if a.no_l2_staging else -1 if a.l2_staging else 0)
     lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, int(a.tc_split))
+    lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, int(a.no_row_mode))
     h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
     # Request-partitioned weak scaling: the global batch is `batch` rows per GPU; the
     # partitioner (lsg_partition_segments) hands every rank whole segments (or row

@@ -181,8 +181,10 @@ typedef enum {
                                  A's smem (single-tile launches); 0 (default): stage only when B resident
                                  would cost co-residency */
   LSG_OPT_NO_TENSOR_CORES = 5, /* 1: long segments stay on the CUDA-core kernel (no tcgen05 path) */
-  LSG_OPT_TC_SPLIT = 6         /* 1: rank-16 long segments use the two-kernel tensor-core path
+  LSG_OPT_TC_SPLIT = 6,        /* 1: rank-16 long segments use the two-kernel tensor-core path
                                   (shrink, then expand through a workspace) instead of the fused one */
+  LSG_OPT_NO_ROW_MODE = 7      /* 1: one-row tiles use the segment-major decode (row split / tile scan)
+                                  instead of one cluster per row with a segment search */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

@@ -30,6 +30,7 @@ struct Plan {
   int red_all = 0;
   int alias_ab = 0;
   int tile_scan = 0;
+  int row_mode = 0;  // one cluster per row, segment found by search (one-row tiles, no long-segment skip)
 };
 
 // Set by the API layer; read at launch.
@@ -119,6 +120,7 @@ int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
       if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemBgmv>(p, pl, st);
       return fail(LSG_EINVAL, "lsg: BGMV indexing is fused-only");
     }
+    if (pl.row_mode) return launch_fast_inst<T, R, 1, MODE, kItemRow>(p, pl, st);
     return pl.tile_scan ? launch_fast_inst<T, R, 1, MODE, kItemTileScan>(p, pl, st)
                         : launch_fast_inst<T, R, 1, MODE, kItemRowSplit>(p, pl, st);
   }

@@ -47,6 +47,7 @@ std::atomic<int> g_opt_no_alias{0};
 std::atomic<int> g_opt_no_tile_scan{0};
 std::atomic<int> g_opt_no_tc{0};
 std::atomic<int> g_opt_tc_split{0};
+std::atomic<int> g_opt_no_row_mode{0};
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -419,6 +420,13 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
       skip_long = kTcMinRows;
   }
   Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
+  // One-row tiles without a long-segment split: one cluster per row, exact grid.
+  if (pl.mt == 1 && kernel != kKBgmv && !skip_long && !g_opt_no_row_mode.load()) {
+    pl.row_mode = 1;
+    pl.tile_scan = 0;
+    pl.row_splits = 1;
+    pl.clusters = s_n;
+  }
   // With the long segments on the tensor cores, the short ones have at most n_seg
   // segments' worth of work items in practice: size the tile-scan grid by that
   // (clusters loop over further tiles) instead of by s_n.
@@ -541,6 +549,7 @@ int lsg_set_option(int32_t option, int32_t value) {
     case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value > 0 ? 1 : value < 0 ? -1 : 0; return LSG_OK;
     case LSG_OPT_NO_TENSOR_CORES: g_opt_no_tc = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_TC_SPLIT: g_opt_tc_split = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_NO_ROW_MODE: g_opt_no_row_mode = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -554,6 +563,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_NO_L2_STAGING: return g_opt_no_alias.load();
     case LSG_OPT_NO_TENSOR_CORES: return g_opt_no_tc.load();
     case LSG_OPT_TC_SPLIT: return g_opt_tc_split.load();
+    case LSG_OPT_NO_ROW_MODE: return g_opt_no_row_mode.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

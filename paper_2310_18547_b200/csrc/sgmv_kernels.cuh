@@ -165,7 +165,7 @@ __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) 
 
 // How a cluster finds its work item (compile-time, so each instantiation carries
 // only its own decode path -- see the code-size note at LSG_INSTRUMENT).
-enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2 };
+enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3 };
 
 template <typename T, int R, int MT, int MODE, int ITEM>
 __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
@@ -230,10 +230,34 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   bool first_item = true;
   for (int item = blockIdx.y;; item += gridDim.y, wphase ^= 1u) {
     int slot, seg_begin, seg_end, first_tile, tile_step;
-    if constexpr (ITEM == kItemBgmv) {
+    if constexpr (ITEM == kItemBgmv || ITEM == kItemRow) {
       const int row = item;
       if (row >= p.s_n) return exit_after_wait();
-      slot = p.row_slot[row];
+      if constexpr (ITEM == kItemBgmv) {
+        slot = p.row_slot[row];
+      } else {
+        // One cluster per row (one-row tiles, any popularity): the row's segment is
+        // the last s < n_seg with seg_starts[s] <= row.  Every warp finds it itself
+        // (ballots over 128 boundaries per step; starts are non-decreasing, so the
+        // first step with a start > row ends the search).
+        int seg = -1;
+        for (int c0 = 0; c0 < p.n_seg; c0 += 128) {
+          unsigned le[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int sg = c0 + j * 32 + lane;
+            le[j] = __ballot_sync(0xffffffffu, sg < p.n_seg && p.seg_starts[sg] <= row);
+          }
+          bool done = false;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (le[j]) seg = c0 + j * 32 + 31 - __clz(le[j]);
+            done = done || le[j] != 0xffffffffu;
+          }
+          if (done) break;
+        }
+        slot = seg >= 0 ? p.seg_slot[seg] : -1;
+      }
       seg_begin = row;
       seg_end = row + 1;
       first_tile = 0;
