@@ -35,7 +35,7 @@ def lsg():
 def _reset_options(lsg):
     yield
     for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
-                lsg.LSG_OPT_NO_TENSOR_CORES):
+                lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE):
         lsg.set_option(opt, 0)
 
 
@@ -458,3 +458,24 @@ def test_tp_column_shards_equal_unsharded_bitwise(lsg, tp):
     tpmod.tp_sgmv_allgather(y, p.x, tpmod.tp_pool(p.pool.a, p.pool.b, 1, 0), p.seg_starts, p.seg_slot, 0)
     torch.cuda.synchronize()
     assert torch.equal(y, base)
+
+
+@pytest.mark.parametrize("row_mode", [0, 1])
+def test_empty_segments_anywhere(lsg, row_mode):
+    """Empty segments (equal boundaries) at the start, middle and end: the row-mode
+    segment search and the segment-major decode give the same, correct rows."""
+    lens = [0, 3, 0, 0, 2, 1, 0, 4, 0]
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 31)
+    lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, 1 - row_mode)
+    try:
+        p = Problem(lsg, x, A, B, bounds, torch.float16)
+        y = p.run()
+        keep = [s for s in range(len(lens)) if lens[s] > 0]  # the reference's Segments are non-empty
+        cb = np.concatenate([[0], np.cumsum([lens[s] for s in keep])]).astype(np.uint64)
+        ref = oracle().lora_addon(p.xd, cb, p.Ad[keep], p.Bd[keep])
+        assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(torch.float16)
+        lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, row_mode)
+        assert torch.equal(p.run(), y)
+    finally:
+        lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, 0)
