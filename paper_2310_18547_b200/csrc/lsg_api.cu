@@ -85,9 +85,26 @@ int tc_nq(const lsg_weight_table* t) {
 
 int tc_fused_c(const lsg_weight_table* t, int* compact);
 
+int tc_min_rows();
+// Upper bound on the 128-row tiles of the segments with >= tc_min_rows() rows:
+// sum ceil(len / 128) <= s_n / 128 + (number of such segments).
+int tc_tile_bound(int s_n, int n_seg) {
+  return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows()));
+}
+
+// Rows from which a segment takes the tensor-core path (LSG_TC_MIN_ROWS: experiments only).
+int tc_min_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("LSG_TC_MIN_ROWS");
+    const int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : kTcMinRows;
+  }();
+  return v;
+}
+
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
   if (tc_fused_c(t, nullptr) > 0 && !g_opt_tc_split.load()) return 0;  // the fused kernel keeps v on chip
-  return tc_nq(t) > 0 && s_n >= kTcMinRows ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
+  return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
 // Library-owned workspace of lsg_sgmv(): grown (never during stream capture)
@@ -158,7 +175,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
   const int nq = tc_nq(tbl);
-  if (nq == 0 || s_n < kTcMinRows) return false;
+  if (nq == 0 || s_n < tc_min_rows()) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
   int compact = 0;
   const int fc = g_opt_tc_split.load() ? 0 : tc_fused_c(tbl, &compact);
@@ -169,7 +186,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
         !encode_rows_map(&fp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
       return false;
     lp.fused_c = fc;
-    lp.tiles = std::max(1, s_n / (kTcM / 2));
+    lp.tiles = tc_tile_bound(s_n, n_seg);
     fp.y = y;
     fp.ldy = ldy;
     fp.a_ptr = tbl->a_ptr;
@@ -185,6 +202,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     fp.h_out = tbl->h_out;
     fp.kcs_max = ((tbl->h_in / kTcKB + fc - 1) / fc) * kTcKB;
     fp.compact = compact;
+    fp.min_rows = tc_min_rows();
     fp.trace = g_trace;
     fp.trace_ctas = g_trace_ctas;
     return true;
@@ -198,7 +216,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
       !encode_rows_map(&ep.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
     return false;
   // tiles of long segments: sum ceil(len/128) over len >= 128 is at most s_n/64
-  const int tiles = std::max(1, s_n / (kTcM / 2));
+  const int tiles = tc_tile_bound(s_n, n_seg);
   lp.nq = nq;
   lp.tiles = tiles;
   sp.v = static_cast<float*>(ws);
@@ -211,6 +229,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   sp.num_slots = tbl->num_slots;
   sp.h_in = tbl->h_in;
   sp.kcs = tbl->h_in / nq;
+  sp.min_rows = tc_min_rows();
   sp.trace = g_trace;
   sp.trace_ctas = g_trace_ctas;
   ep.y = y;
@@ -224,6 +243,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   ep.s_n = s_n;
   ep.num_slots = tbl->num_slots;
   ep.h_out = tbl->h_out;
+  ep.min_rows = tc_min_rows();
   ep.trace = g_trace;
   ep.trace_ctas = g_trace_ctas;
   return true;
@@ -411,13 +431,13 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   // expand may stage y_old before waiting for v.
   int skip_long = 0;
   LongPlan lp;
-  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= kTcMinRows && tc_nq(tbl) > 0) {
+  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= tc_min_rows() && tc_nq(tbl) > 0) {
     if (library_ws) {
       ws_bytes = tc_workspace_bytes(tbl, s_n);
       ws = library_workspace(ws_bytes, cs);
     }
     if (prepare_long_segments(lp, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, ws, ws_bytes))
-      skip_long = kTcMinRows;
+      skip_long = tc_min_rows();
   }
   Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
   // One-row tiles without a long-segment split: one cluster per row, exact grid.

@@ -47,6 +47,7 @@ struct TcShrinkParams {
   const int32_t* seg_starts;
   const int32_t* seg_slot;
   int32_t n_seg, s_n, num_slots, h_in, kcs;
+  int32_t min_rows;  // segments with at least this many rows are this kernel's
   unsigned long long* trace;  // lsg_set_trace: %globaltimer stamps, entries [trace_ctas, 2 trace_ctas)
   int32_t trace_ctas;
 };
@@ -61,6 +62,7 @@ struct TcExpandParams {
   const int32_t* seg_starts;
   const int32_t* seg_slot;
   int32_t n_seg, s_n, num_slots, h_out;
+  int32_t min_rows;
   unsigned long long* trace;
   int32_t trace_ctas;
 };
@@ -181,7 +183,7 @@ __device__ __forceinline__ int swz(int k) {
 // ceil(len / 128) over the segments with len >= kTcMinRows, 32 segments per step.
 // Call from one full warp; seg = -1 past the last tile.
 __device__ __forceinline__ void tc_tile_of(const int32_t* seg_starts, int n_seg, int t, int lane, int& seg,
-                                           int& tin) {
+                                           int& tin, int min_rows) {
   int base = 0;
   seg = -1;
   tin = 0;
@@ -190,7 +192,7 @@ __device__ __forceinline__ void tc_tile_of(const int32_t* seg_starts, int n_seg,
     int nt = 0;
     if (sg < n_seg) {
       const int len = seg_starts[sg + 1] - seg_starts[sg];
-      nt = len >= kTcMinRows ? (len + kTcM - 1) / kTcM : 0;
+      nt = len >= min_rows ? (len + kTcM - 1) / kTcM : 0;
     }
     int incl = nt;
 #pragma unroll
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_shrink_kernel(const __grid
   __shared__ int s_seg, s_tile;
   if (warp == 0) {
     int seg, tin;
-    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin, p.min_rows);
     if (lane == 0) {
       s_seg = seg;
       s_tile = tin;
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
   __shared__ int s_seg, s_tile;
   if (warp == 0) {
     int seg, tin;
-    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin, p.min_rows);
     if (lane == 0) {
       s_seg = seg;
       s_tile = tin;
@@ -589,6 +591,7 @@ struct TcFusedParams {
   int32_t n_seg, s_n, num_slots, h_in, h_out;
   int32_t kcs_max;  // max K columns per CTA (multiple of 64)
   int32_t compact;  // 1: one 256-column chunk per CTA, y staged in the x ring after the shrink (2 CTAs/SM)
+  int32_t min_rows;
   unsigned long long* trace;
   int32_t trace_ctas;
 };
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __gr
   __shared__ int s_seg, s_tile;
   if (warp == 0) {
     int seg, tin;
-    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin);
+    tc_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, seg, tin, p.min_rows);
     if (lane == 0) {
       s_seg = seg;
       s_tile = tin;
