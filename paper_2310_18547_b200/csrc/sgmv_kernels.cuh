@@ -178,10 +178,12 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   constexpr int kBarB = kPieces, kBarRed = kPieces + 1, kBarV = kPieces + 2;
 
   extern __shared__ __align__(128) uint8_t smem[];
-  // A CTA that leaves without work still waits for the preceding grid first: with
-  // PDL a grid's completion must imply its predecessor's (the next kernel on the
-  // stream waits only for this one).
-  auto exit_after_wait = [] { pdl_wait(); };
+  // A CTA that leaves without work: with PDL a grid's completion must imply its
+  // predecessor's (the next kernel on the stream waits only for this one), so the
+  // first cluster always waits before leaving; the others leave at once.
+  auto exit_after_wait = [] {
+    if (blockIdx.y == 0) pdl_wait();
+  };
   const int C = static_cast<int>(gridDim.x);
   const int crank = static_cast<int>(blockIdx.x);  // cluster dims (C,1,1), grid.x == C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

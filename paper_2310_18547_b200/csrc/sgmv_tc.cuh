@@ -267,13 +267,17 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_shrink_kernel(const __grid
     }
   }
   __syncthreads();
+  // CTAs without work leave at once (freeing their SM for the next grid) except the
+  // first cluster, which always waits for the preceding grid: this grid's completion
+  // (and its trigger, which the expand relies on for staging y_old early) then still
+  // implies the predecessor's.
   if (s_seg < 0) {  // past the last tile (the grid is an upper bound), whole cluster
-    pdl_wait();       // (the expand relies on every shrink CTA having waited, see below)
+    if (blockIdx.y == 0) pdl_wait();
     return;
   }
   const int slot = p.seg_slot[s_seg];
   if (slot < 0 || slot >= p.num_slots) {  // no adapter: the expand leaves y untouched
-    pdl_wait();
+    if (blockIdx.y == 0) pdl_wait();
     return;
   }
   const int seg_end = p.seg_starts[s_seg + 1];
@@ -416,9 +420,16 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
     }
   }
   __syncthreads();
-  if (s_seg < 0) return;
+  // (as in the shrink: only the first tile's CTAs wait before leaving without work)
+  if (s_seg < 0) {
+    if (blockIdx.y == 0) pdl_wait();
+    return;
+  }
   const int slot = p.seg_slot[s_seg];
-  if (slot < 0 || slot >= p.num_slots) return;  // no adapter: y untouched
+  if (slot < 0 || slot >= p.num_slots) {  // no adapter: y untouched
+    if (blockIdx.y == 0) pdl_wait();
+    return;
+  }
   const int seg_end = p.seg_starts[s_seg + 1];
   const int r0 = p.seg_starts[s_seg] + s_tile * kTcM;
   const int rows = min(kTcM, seg_end - r0);
@@ -642,13 +653,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __gr
     }
   }
   __syncthreads();
-  if (s_seg < 0) {  // past the last tile (the grid is an upper bound): keep the PDL chain
-    pdl_wait();
+  // CTAs without work leave at once, except the first tile's cluster, which waits for
+  // the preceding grid so this grid's completion still implies the predecessor's.
+  if (s_seg < 0) {  // past the last tile (the grid is an upper bound)
+    if (blockIdx.y == 0) pdl_wait();
     return;
   }
   const int slot = p.seg_slot[s_seg];
   if (slot < 0 || slot >= p.num_slots) {  // no adapter: rows untouched
-    pdl_wait();
+    if (blockIdx.y == 0) pdl_wait();
     return;
   }
   const int seg_end = p.seg_starts[s_seg + 1];
