@@ -213,6 +213,17 @@ def test_long_segments_tensor_core_path(lsg, dtype, shape, lens):
         if n < 128:
             assert torch.equal(got[a:b], cc[a:b]), s
     assert torch.equal(p.run(), got)  # run-to-run deterministic
+    if r == 16:  # rank 16 runs the fused kernel by default: the two-kernel form must agree too
+        lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, 1)
+        try:
+            split = p.run()
+        finally:
+            lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, 0)
+        assert row_norm_err(split.double().cpu().numpy(), p.reference()) <= tol(dtype)
+        for s, n in enumerate(lens):
+            a, b = int(bounds[s]), int(bounds[s + 1])
+            if n < 128:
+                assert torch.equal(split[a:b], got[a:b]), s
 
 
 def test_long_segment_no_adapter_slot_untouched(lsg):
