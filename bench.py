@@ -402,6 +402,35 @@ def main():
     extra["us_per_launch_no_pdl"] = ms_nopdl * 1e3 / sites
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     del flush
+    # Grouped launches (lsg_sgmv_multi): per layer q/k/v in one launch, o, gate/up in
+    # one launch, down -- 4 launches for the 7 sites, same bytes and results.
+    if a.kernel == "sgmv" and sites % SITES_PER_LAYER == 0:
+        groups = []
+        for l in range(sites // SITES_PER_LAYER):
+            b0 = l * SITES_PER_LAYER
+            groups += [[b0, b0 + 1, b0 + 2], [b0 + 3], [b0 + 4, b0 + 5], [b0 + 6]]
+
+        views = {s_: pool.layer_view(s_) for g in groups if len(g) > 1 for s_ in g}  # before capture
+
+        def step_grouped():
+            for g in groups:
+                if len(g) == 1:
+                    launch(g[0])
+                else:  # the sites' weights are layers g[i] of the one bench pool (same slots)
+                    lsg.sgmv_multi([ys[s_] for s_ in g], [xs[s_] for s_ in g],
+                                   [views[s_] for s_ in g], seg_starts, seg_slot, 0)
+
+        with torch.cuda.stream(stream):
+            step_grouped()
+        torch.cuda.synchronize()
+        graph_g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_g, stream=stream):
+            step_grouped()
+        with torch.cuda.stream(stream):
+            graph_g.replay()
+        kg = max(3, a.steps // 2)
+        extra["grouped_us_per_site"] = timed(graph_g.replay, kg) * 1e3 / (kg * sites)
+        extra["grouped_launches_per_layer"] = 4
 
 
     # e2e through the public API: every step copies that step's activations in from

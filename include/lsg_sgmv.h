@@ -7,6 +7,7 @@
  *
  *   lsg_sgmv           <- lorasim::lora_addon(const Batch&)        core/include/lorasim/sgmv.hpp:72-73,
  *                         core/src/sgmv.cpp:138-141 (fused, accumulates into y)
+ *   lsg_sgmv_multi     <- lora_addon over several projection sites sharing one Batch's segments
  *   lsg_sgmv_shrink    <- lorasim::sgmv_shrink(const Batch&)       sgmv.hpp:64-66, sgmv.cpp:105-119
  *   lsg_sgmv_expand    <- lorasim::sgmv_expand(v, segs, models)    sgmv.hpp:68-70, sgmv.cpp:121-136
  *   lsg_bgmv           <- lorasim::gather_bmm_oracle(const Batch&) sgmv.hpp:81-83, sgmv.cpp:186-217
@@ -107,6 +108,24 @@ int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weig
                 const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
                 int32_t total_rows, int32_t layer, void* workspace, size_t workspace_bytes,
                 lsg_stream_t stream);
+
+/* Grouped fused call: up to 8 LoRA sites that share one segment plan (e.g. the
+ * q / k / v projections of a layer: same requests, same adapters, each site with
+ * its own pool, x and y) in ONE launch -- one cluster per (site, row), so the
+ * sites' weight streams overlap and the per-launch critical path is paid once.
+ * Same results as calling lsg_sgmv per site (the sites must share h_in, h_out,
+ * rank, dtype, slot count and layer strides).  Falls back to one launch per site
+ * when a site needs another path (long segments, generic shapes). */
+typedef struct lsg_sgmv_site {
+  void* y;
+  int64_t ldy;
+  const void* x;
+  int64_t ldx;
+  const lsg_weight_table* tbl;
+} lsg_sgmv_site;
+int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
+                   const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
+                   lsg_stream_t stream);
 
 /* Shrink only: v[s_n, rank] (fp32, row stride rank) = x . A per segment (overwrite). */
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,

@@ -24,7 +24,7 @@ EXPORTED = (
     "lsg_sgmv", "lsg_sgmv_ws", "lsg_sgmv_workspace_size", "lsg_sgmv_shrink", "lsg_sgmv_expand", "lsg_bgmv",
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
-    "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments",
+    "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments", "lsg_sgmv_multi",
 )
 
 
@@ -47,6 +47,13 @@ class WeightTable(C.Structure):
 
 class LaunchInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("path", "cluster", "tile_rows", "row_splits", "grid_ctas", "smem_bytes")]
+
+
+class Site(C.Structure):
+    """Mirror of ``lsg_sgmv_site``."""
+
+    _fields_ = [("y", C.c_void_p), ("ldy", C.c_int64), ("x", C.c_void_p), ("ldx", C.c_int64),
+                ("tbl", C.POINTER(WeightTable))]
 
 
 class Piece(C.Structure):
@@ -76,6 +83,7 @@ def lib() -> C.CDLL:
         tp = C.POINTER(WeightTable)
         L.lsg_sgmv.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp]
         L.lsg_sgmv_ws.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
+        L.lsg_sgmv_multi.argtypes = [C.POINTER(Site), i32, vp, vp, i32, i32, i32, vp]
         L.lsg_sgmv_workspace_size.argtypes = [tp, i32]
         L.lsg_sgmv_workspace_size.restype = C.c_size_t
         L.lsg_sgmv_shrink.argtypes = [vp, vp, i64, tp, vp, vp, i32, i32, i32, vp]

@@ -31,6 +31,7 @@ struct Plan {
   int alias_ab = 0;
   int tile_scan = 0;
   int row_mode = 0;  // one cluster per row, segment found by search (one-row tiles, no long-segment skip)
+  int multi = 0;     // grouped launch over several sites (row mode, fused)
 };
 
 // Set by the API layer; read at launch.
@@ -119,6 +120,10 @@ int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
     if (p.row_slot != nullptr) {
       if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemBgmv>(p, pl, st);
       return fail(LSG_EINVAL, "lsg: BGMV indexing is fused-only");
+    }
+    if (pl.multi) {
+      if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemRowMulti>(p, pl, st);
+      return fail(LSG_EINVAL, "lsg: grouped launches are fused-only");
     }
     if (pl.row_mode) return launch_fast_inst<T, R, 1, MODE, kItemRow>(p, pl, st);
     return pl.tile_scan ? launch_fast_inst<T, R, 1, MODE, kItemTileScan>(p, pl, st)

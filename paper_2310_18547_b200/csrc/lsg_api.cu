@@ -376,7 +376,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
 int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_out, const float* v_in,
         const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
         const int32_t* row_slot, int32_t n_seg, int32_t s_n, int32_t layer, lsg_stream_t stream,
-        void* ws = nullptr, size_t ws_bytes = 0, bool library_ws = false) {
+        void* ws = nullptr, size_t ws_bytes = 0, bool library_ws = false, const lsg_sgmv_site* sites = nullptr,
+        int n_sites = 0) {
   int st = validate_table(tbl);
   if (st != LSG_OK) return st;
   if (s_n < 0) return fail(LSG_EINVAL, "lsg: total_rows must be >= 0");
@@ -447,6 +448,10 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
     pl.row_splits = 1;
     pl.clusters = s_n;
   }
+  if (n_sites > 1) {  // grouped launch (lsg_sgmv_multi checked eligibility): one cluster per (site, row)
+    pl.multi = 1;
+    pl.clusters = n_sites * s_n;
+  }
   // With the long segments on the tensor cores, the short ones have at most n_seg
   // segments' worth of work items in practice: size the tile-scan grid by that
   // (clusters loop over further tiles) instead of by s_n.
@@ -482,6 +487,10 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.skip_long = skip_long;
   p.trace = g_trace;
   p.trace_ctas = g_trace_ctas;
+  p.n_sites = n_sites > 1 ? n_sites : 0;
+  for (int i = 0; i < p.n_sites; ++i)
+    p.sites[i] = SiteParams{sites[i].y, sites[i].x, sites[i].tbl->a_ptr, sites[i].tbl->b_ptr, sites[i].ldx,
+                            sites[i].ldy};
   static const int exp_flags = [] {
     const char* e = std::getenv("LSG_EXP");
     return e ? std::atoi(e) : 0;
@@ -532,6 +541,42 @@ int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weig
                 lsg_stream_t stream) {
   return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
              num_segments, total_rows, layer, stream, workspace, workspace_bytes, false);
+}
+
+int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
+                   const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
+                   lsg_stream_t stream) {
+  if (sites == nullptr || num_sites < 1 || num_sites > kMaxSites)
+    return fail(LSG_EINVAL, "lsg_sgmv_multi: need 1..8 sites");
+  const lsg_weight_table* t0 = sites[0].tbl;
+  for (int i = 0; i < num_sites; ++i) {
+    const lsg_weight_table* t = sites[i].tbl;
+    const int st = validate_table(t);
+    if (st != LSG_OK) return st;
+    if (t->h_in != t0->h_in || t->h_out != t0->h_out || t->rank != t0->rank || t->dtype != t0->dtype ||
+        t->num_slots != t0->num_slots || t->num_layers != t0->num_layers ||
+        t->a_layer_stride != t0->a_layer_stride || t->b_layer_stride != t0->b_layer_stride)
+      return fail(LSG_EINVAL, "lsg_sgmv_multi: sites must share shape, dtype, slot count and layer strides");
+  }
+  // One grouped launch when every site takes the one-row fast path without long
+  // segments; otherwise the sites run one after another (same results).
+  bool grouped = num_sites > 1 && total_rows > 0 && num_segments > 0 && fast_shape_ok(t0) &&
+                 !g_opt_force_generic.load() && !g_opt_no_row_mode.load() && g_opt_force_tile_rows.load() != 8 &&
+                 (g_opt_no_tc.load() || total_rows < tc_min_rows() || tc_nq(t0) == 0);
+  for (int i = 0; grouped && i < num_sites; ++i)
+    grouped = sites[i].x != nullptr && sites[i].y != nullptr && aligned16(sites[i].x) && aligned16(sites[i].y) &&
+              sites[i].ldx % 8 == 0 && sites[i].ldy % 8 == 0 && sites[i].ldx >= t0->h_in &&
+              sites[i].ldy >= t0->h_out;
+  if (!grouped) {
+    for (int i = 0; i < num_sites; ++i) {
+      const int st = run(kKFused, sites[i].y, sites[i].ldy, sites[i].x, sites[i].ldx, nullptr, nullptr, sites[i].tbl,
+                         seg_starts, seg_slot, nullptr, num_segments, total_rows, layer, stream, nullptr, 0, true);
+      if (st != LSG_OK) return st;
+    }
+    return LSG_OK;
+  }
+  return run(kKFused, sites[0].y, sites[0].ldy, sites[0].x, sites[0].ldx, nullptr, nullptr, t0, seg_starts,
+             seg_slot, nullptr, num_segments, total_rows, layer, stream, nullptr, 0, true, sites, num_sites);
 }
 
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,

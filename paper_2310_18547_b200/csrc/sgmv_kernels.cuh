@@ -45,6 +45,17 @@ constexpr int kPieces = 4;  // A arrives in up to 4 bulk copies, one mbarrier ea
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 
+// One LoRA site of a grouped launch (lsg_sgmv_multi): its activations and pool.
+struct SiteParams {
+  void* y;
+  const void* x;
+  const void* const* a_ptr;
+  const void* const* b_ptr;
+  int64_t ldx;
+  int64_t ldy;
+};
+constexpr int kMaxSites = 8;
+
 struct FastParams {
   void* y;
   const void* x;
@@ -76,6 +87,8 @@ struct FastParams {
   int32_t alias_ab;   // 1: single-tile clusters; B is prefetched into L2 and later loaded over A's smem
   int32_t tile_scan;  // 1: cluster blockIdx.y = global tile index, mapped to (segment, tile) on device
   int32_t skip_long;  // >0: segments with at least this many rows belong to the tensor-core kernel
+  int32_t n_sites;    // grouped launch: sites[0, n_sites) share the segment plan (kItemRowMulti)
+  SiteParams sites[kMaxSites];
 };
 
 // Phase trace: thread 0 of each CTA stamps clock64 at kernel phases (slot 14:
@@ -165,7 +178,7 @@ __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) 
 
 // How a cluster finds its work item (compile-time, so each instantiation carries
 // only its own decode path -- see the code-size note at LSG_INSTRUMENT).
-enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3 };
+enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3, kItemRowMulti = 4 };
 
 template <typename T, int R, int MT, int MODE, int ITEM>
 __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
@@ -230,10 +243,27 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
   uint32_t wphase = 0;  // weight barriers: flips every item
   bool first = true;    // first tile this CTA computes (cluster barrier-init wait)
   bool first_item = true;
+  // The site this cluster works for (grouped launches pick theirs below).
+  const void* s_x = p.x;
+  void* s_y = p.y;
+  const void* const* s_a = p.a_ptr;
+  const void* const* s_b = p.b_ptr;
+  int64_t s_ldx = p.ldx, s_ldy = p.ldy;
   for (int item = blockIdx.y;; item += gridDim.y, wphase ^= 1u) {
     int slot, seg_begin, seg_end, first_tile, tile_step;
-    if constexpr (ITEM == kItemBgmv || ITEM == kItemRow) {
-      const int row = item;
+    if constexpr (ITEM == kItemBgmv || ITEM == kItemRow || ITEM == kItemRowMulti) {
+      int row = item;
+      if constexpr (ITEM == kItemRowMulti) {  // cluster y = site * s_n + row
+        const int g = item / p.s_n;
+        if (g >= p.n_sites) return exit_after_wait();
+        row = item - g * p.s_n;
+        s_x = p.sites[g].x;
+        s_y = p.sites[g].y;
+        s_a = p.sites[g].a_ptr;
+        s_b = p.sites[g].b_ptr;
+        s_ldx = p.sites[g].ldx;
+        s_ldy = p.sites[g].ldy;
+      }
       if (row >= p.s_n) return exit_after_wait();
       if constexpr (ITEM == kItemBgmv) {
         slot = p.row_slot[row];
@@ -363,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     // A, warp 1 issues B (one row per lane).
     const int a_warp = (LSG_EXP_FLAGS & 4) ? 1 : 0, b_warp = (LSG_EXP_FLAGS & 4) ? 0 : (kSh ? 1 : 0);
     if (kSh && warp == a_warp && nqc > 0) {
-      const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
+      const T* A = static_cast<const T*>(s_a[slot]) + p.a_off + static_cast<int64_t>(q0) * KW * R;
       if (lane < npieces) {
         const int c0 = (lane * nqc) / npieces, c1 = ((lane + 1) * nqc) / npieces;
         const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * KW * R * sizeof(T));
@@ -376,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     }
     const T* Bslice = nullptr;
     if (kEx && warp == b_warp && ncv > 0) {
-      const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + cv0 * 8;
+      const T* B = static_cast<const T*>(s_b[slot]) + p.b_off + cv0 * 8;
       Bslice = B;
     }
     if (kEx && warp == b_warp && ncv > 0 && alias_ab) {
@@ -407,10 +437,10 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
     if (first_item && warp == 2 && !(LSG_EXP_FLAGS & 32)) {
       const int r0 = seg_begin + first_tile * MT, rows = min(MT, seg_end - r0);
       if (kSh && lane < rows && nqc > 0)
-        bulk_prefetch_l2(static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + lane) * p.ldx + q0 * KW,
+        bulk_prefetch_l2(static_cast<const T*>(s_x) + static_cast<int64_t>(r0 + lane) * s_ldx + q0 * KW,
                          static_cast<uint32_t>(ndl * sizeof(T)));
       if (kEx && lane >= 16 && lane - 16 < rows && ncv > 0)
-        bulk_prefetch_l2(static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + lane - 16) * p.ldy + cv0 * 8,
+        bulk_prefetch_l2(static_cast<const T*>(s_y) + static_cast<int64_t>(r0 + lane - 16) * s_ldy + cv0 * 8,
                          static_cast<uint32_t>(ncv * 16));
     }
     LSG_TRACE(2);
@@ -458,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         for (int i = tid; i < rows * nv; i += kThreads) {
           const int m = MT == 1 ? 0 : i / nv, c = i - m * nv;
           cp_async16(x_sm + m * ndl + c * 8,
-                     static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + m) * p.ldx + q0 * KW + c * 8);
+                     static_cast<const T*>(s_x) + static_cast<int64_t>(r0 + m) * s_ldx + q0 * KW + c * 8);
         }
       }
       cp_async_commit();
@@ -466,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         for (int i = tid; i < rows * ncv; i += kThreads) {
           const int m = MT == 1 ? 0 : i / ncv, c = i - m * ncv;
           cp_async16(y_sm + m * ncv + c,
-                     static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + c) * 8);
+                     static_cast<const T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + c) * 8);
         }
       }
       cp_async_commit();
@@ -616,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
             Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = acc[j] + yo[j];
-            st_global_v4(static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + (cv0 + cv) * 8,
+            st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
                          Cvt<T>::pack8(acc));
           }
         }

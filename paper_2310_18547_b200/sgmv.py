@@ -69,6 +69,23 @@ class AdapterPool:
         self.a[slot].copy_(a_layers, non_blocking=True)
         self.b[slot].copy_(b_layers, non_blocking=True)
 
+    def layer_view(self, layer: int) -> "AdapterPool":
+        """A one-layer pool whose layer 0 is ``layer`` of this one (same slots, same
+        storage; only the device pointer table is new).  Lets sites that live in
+        different layers of one pool share a grouped call's layer index."""
+        if not 0 <= layer < self.num_layers:
+            raise ValueError("layer out of range")
+        v = AdapterPool.__new__(AdapterPool)
+        v.num_slots, v.num_layers = self.num_slots, 1
+        v.h_in, v.h_out, v.rank, v.dtype = self.h_in, self.h_out, self.rank, self.dtype
+        v.a, v.b = self.a[:, layer:layer + 1], self.b[:, layer:layer + 1]
+        es = self.a.element_size()
+        v.a_ptrs = self.a_ptrs + layer * self.h_in * self.rank * es
+        v.b_ptrs = self.b_ptrs + layer * self.rank * self.h_out * es
+        v.table = WeightTable(v.a_ptrs.data_ptr(), v.b_ptrs.data_ptr(), self.h_in * self.rank, self.rank * self.h_out,
+                              self.num_slots, 1, self.h_in, self.h_out, self.rank, _DTYPES[self.dtype])
+        return v
+
     @property
     def slot_bytes_per_layer(self) -> int:
         return (self.h_in * self.rank + self.rank * self.h_out) * self.a.element_size()
@@ -96,6 +113,24 @@ def sgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.
     _lib.call("lsg_sgmv_ws", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
               _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws) if ws is not None else None, wsb, _stream())
     return y
+
+
+def sgmv_multi(ys, xs, pools, seg_starts: torch.Tensor, seg_slot: torch.Tensor, layer: int,
+               num_segments: int | None = None):
+    """Grouped fused call: ``ys[i] += xs[i] . A_i . B_i`` for up to 8 sites sharing one
+    segment plan (e.g. q / k / v of a layer), in one launch (lsg_sgmv_multi)."""
+    if not (len(ys) == len(xs) == len(pools)) or not 1 <= len(ys) <= 8:
+        raise ValueError("sgmv_multi needs 1..8 sites with one y, x and pool each")
+    for y, x, pool in zip(ys, xs, pools):
+        _rows_check(x, y, pool)
+    _check_i32(seg_starts, "seg_starts")
+    _check_i32(seg_slot, "seg_slot")
+    n = seg_slot.numel() if num_segments is None else num_segments
+    sites = (_lib.Site * len(ys))(*[_lib.Site(y.data_ptr(), y.stride(0), x.data_ptr(), x.stride(0),
+                                              C.pointer(pool.table)) for y, x, pool in zip(ys, xs, pools)])
+    _lib.call("lsg_sgmv_multi", sites, len(ys), _ptr(seg_starts), _ptr(seg_slot), n, xs[0].shape[0], layer,
+              _stream())
+    return ys
 
 
 def sgmv_workspace_size(pool: AdapterPool, rows: int) -> int:
@@ -182,6 +217,6 @@ def query_launch(pool: AdapterPool, num_segments: int, total_rows: int, kernel: 
     return {f: getattr(info, f) for f, _ in LaunchInfo._fields_}
 
 
-__all__ = ["AdapterPool", "sgmv", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
+__all__ = ["AdapterPool", "sgmv", "sgmv_multi", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
            "scatter_rows", "set_option", "get_option", "query_launch", "KERNEL_FUSED", "KERNEL_SHRINK",
            "KERNEL_EXPAND", "KERNEL_BGMV"]

@@ -490,3 +490,38 @@ def test_empty_segments_anywhere(lsg, row_mode):
         assert torch.equal(p.run(), y)
     finally:
         lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, 0)
+
+
+@pytest.mark.parametrize("pop", [DISTINCT, SKEWED, IDENTICAL])
+@pytest.mark.parametrize("nsites", [2, 3, 8])
+def test_grouped_sites_equal_per_site_calls_bitwise(lsg, pop, nsites):
+    """lsg_sgmv_multi (one launch for several sites sharing the segment plan) is bitwise
+    the per-site lsg_sgmv calls; each site uses its own pool, x and y."""
+    bounds, _, _ = segments_for(pop, 48, 40 + nsites)
+    probs = []
+    for i in range(nsites):
+        x, A, B = random_problem(4096, 4096, 16, bounds, 60 + i)
+        y0 = oracle().rng(70 + i).fill_pm1(48 * 4096).reshape(48, 4096)
+        probs.append(Problem(lsg, x, A, B, bounds, torch.float16, y0=y0))
+    ref = [p.run() for p in probs]
+    ys = [p.y0.clone() for p in probs]
+    lsg.sgmv_multi(ys, [p.x for p in probs], [p.pool for p in probs], probs[0].seg_starts, probs[0].seg_slot, 0)
+    torch.cuda.synchronize()
+    for i in range(nsites):
+        assert torch.equal(ys[i], ref[i]), i
+
+
+def test_grouped_sites_fall_back_with_long_segments(lsg):
+    """A long (tensor-core) segment makes the grouped call run site by site: same results."""
+    bounds = np.array([0, 200, 203, 210], dtype=np.uint64)
+    probs = []
+    for i in range(3):
+        x, A, B = random_problem(4096, 4096, 16, bounds, 80 + i)
+        probs.append(Problem(lsg, x, A, B, bounds, torch.bfloat16))
+    ref = [p.run() for p in probs]
+    ys = [p.y0.clone() for p in probs]
+    lsg.sgmv_multi(ys, [p.x for p in probs], [p.pool for p in probs], probs[0].seg_starts, probs[0].seg_slot, 0)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert torch.equal(ys[i], ref[i]), i
+        assert row_norm_err(ys[i].double().cpu().numpy(), probs[i].reference()) <= tol(torch.bfloat16)
