@@ -48,6 +48,7 @@ std::atomic<int> g_opt_no_tile_scan{0};
 std::atomic<int> g_opt_no_tc{0};
 std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
+std::atomic<int> g_opt_no_rank64_tiles{0};  // experiments: LSG_NO_RANK64_TILES=1
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -305,6 +306,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     pl.mt = 1;
   else if (forced_mt == 1 || forced_mt == 8)
     pl.mt = forced_mt;
+  else if (t->rank == 64 && s_n > n_seg && !g_opt_no_rank64_tiles.load())
+    pl.mt = 8;  // rank 64 with shared adapters: one weight read per 8-row tile (c3, profiles/README.md)
   else
     pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
   if (kernel == kKBgmv) {
@@ -353,14 +356,17 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::gcd(nq, ncvt));
   const int64_t est_clusters = long_on_tc ? n_seg : pl.clusters;
   int c = 0, c_small = 0;
-  for (int cand = 1; cand <= kMaxCluster; ++cand) {
-    if (span % cand != 0 && cand != kMaxCluster) continue;
+  // Multi-row tiles carry MT rows of compute per CTA: clusters above 8 measured slower
+  // (rank 64, c3: C = 16 27.3 us vs C = 8 16.7 us).
+  const int c_cap = pl.mt > 1 ? 8 : kMaxCluster;
+  for (int cand = 1; cand <= c_cap; ++cand) {
+    if (span % cand != 0 && cand != c_cap) continue;
     if (smem_for(cand) > kSmemBudget) continue;
     if (c_small == 0) c_small = cand;
     const int64_t limit = (pl.tile_scan || cand <= 4) ? 256 : 148;
     if (est_clusters * cand <= limit) c = cand;
   }
-  if (c == 0) c = c_small > 0 ? c_small : kMaxCluster;
+  if (c == 0) c = c_small > 0 ? c_small : c_cap;
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);
@@ -511,6 +517,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
 }  // namespace
 
 bool pdl_enabled() { return g_opt_pdl.load() != 0; }
+static const bool g_rank64_env = [] {
+  const char* e = std::getenv("LSG_NO_RANK64_TILES");
+  if (e && std::atoi(e)) g_opt_no_rank64_tiles = 1;
+  return true;
+}();
 
 int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st) {
   return dtype == LSG_F16 ? dispatch_generic<__half>(g, mode, rows, smem, st)

@@ -181,7 +181,8 @@ __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) 
 enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3, kItemRowMulti = 4 };
 
 template <typename T, int R, int MT, int MODE, int ITEM>
-__global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(const __grid_constant__ FastParams p) {
+__global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
+    sgmv_fast_kernel(const __grid_constant__ FastParams p) {
   static_assert(R == 8 || R == 16 || R == 32 || R == 64, "fast path ranks");
   constexpr int VPR = R / 8;       // 16-byte vectors per A row
   constexpr int RPI = 32 / VPR;    // A rows covered by one warp instruction
@@ -526,6 +527,61 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         // Work unit = (chunk, row): every warp takes units until none are left.  A
         // unit's arithmetic depends only on its chunk and row, never on which warp,
         // CTA or tile size computes it.
+        if constexpr (MT > 1) {
+          // Multi-row tiles: unit = one chunk for ALL rows of the tile -- each A vector
+          // is read and converted once and feeds MT independent per-row chains (the same
+          // per-lane chain per row as a one-row unit, so results are unchanged).
+          for (int ql = warp; ql < nqc; ql += kWarps) {
+            mbar_wait(&bars[split_owner(ql, nqc, npieces)], wphase);
+            float acc[MT][8];
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
+            const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
+            const T* xc = x_sm + ql * KW + rowoff;
+#pragma unroll 4
+            for (int it = 0; it < ITER; ++it) {
+              float a[8];
+              Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
+#pragma unroll
+              for (int m = 0; m < MT; ++m) {
+                const float xm = Cvt<T>::to_f(xc[m * ndl + it * RPI]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(xm, a[j], acc[m][j]);
+              }
+            }
+            const int q = q0 + ql;
+            const int g = lane / VPR;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              if (m >= rows) break;  // warp-uniform
+#pragma unroll
+              for (int off = VPR; off < 32; off <<= 1)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int o = m * R + vec * 8 + h * 4;
+                if (red_all) {
+                  const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
+                  for (int dst = (g + h) % RPI; dst < C; dst += RPI)
+                    st_async_v4(mapa_u32(recv + q * MT * R + o, static_cast<uint32_t>(dst)), acc[m][h * 4 + 0],
+                                acc[m][h * 4 + 1], acc[m][h * 4 + 2], acc[m][h * 4 + 3],
+                                mapa_u32(&bars[kBarRed], static_cast<uint32_t>(dst)));
+                  (void)local;
+                  (void)lbar;
+                } else if (g == h) {
+                  const int owner = split_owner(o / 4, no / 4, C);
+                  const int jl = o - split_lo(owner, no / 4, C) * 4;
+                  st_async_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[m][h * 4 + 0],
+                              acc[m][h * 4 + 1], acc[m][h * 4 + 2], acc[m][h * 4 + 3],
+                              mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
+                }
+              }
+            }
+          }
+        } else {
         const int nunits = nqc * rows;
         for (int u = warp; u < nunits; u += kWarps) {
           const int ql = MT == 1 ? u : u / rows, m = MT == 1 ? 0 : u - ql * rows;
@@ -580,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
           }
           if (u == warp) LSG_TRACE(13);  // warp 0: first unit pushed
         }
+        }  // MT == 1
         if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
         __syncthreads();
         if (kEx && alias_ab && warp == b_warp && ncv > 0) {
@@ -629,6 +686,43 @@ __global__ void __launch_bounds__(kThreads, LSG_MIN_BLOCKS) sgmv_fast_kernel(con
         if (ncv > 0) {
           mbar_wait(&bars[kBarB], wphase);
           LSG_TRACE(10);
+          if constexpr (MT > 1) {
+            // Multi-row tiles: item = (column vector, pair of rows); each B vector is
+            // read and converted once for both rows (same per-element chain over k).
+            constexpr int RG = 2;
+            const int ngr = (rows + RG - 1) / RG;
+            for (int i = tid; i < ngr * ncv; i += kThreads) {
+              const int gr = i / ncv, cv = i - gr * ncv;
+              float acc[RG][8];
+#pragma unroll
+              for (int r = 0; r < RG; ++r)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+#pragma unroll 8
+              for (int k = 0; k < R; ++k) {
+                float b[8];
+                Cvt<T>::unpack8(B_sm[k * ncv + cv], b);
+#pragma unroll
+                for (int r = 0; r < RG; ++r) {
+                  const float vk = V_sm[(gr * RG + r) * R + k];
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) acc[r][j] = fmaf(vk, b[j], acc[r][j]);
+                }
+              }
+#pragma unroll
+              for (int r = 0; r < RG; ++r) {
+                const int m = gr * RG + r;
+                if (m < rows) {
+                  float yo[8];
+                  Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) acc[r][j] = acc[r][j] + yo[j];
+                  st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
+                               Cvt<T>::pack8(acc[r]));
+                }
+              }
+            }
+          } else
           for (int i = tid; i < rows * ncv; i += kThreads) {
             const int m = i / ncv, cv = i - m * ncv;
             float acc[8];

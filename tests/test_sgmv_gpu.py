@@ -525,3 +525,22 @@ def test_grouped_sites_fall_back_with_long_segments(lsg):
     for i in range(3):
         assert torch.equal(ys[i], ref[i]), i
         assert row_norm_err(ys[i].double().cpu().numpy(), probs[i].reference()) <= tol(torch.bfloat16)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("pop", [UNIFORM, SKEWED])
+def test_rank64_multirow_tiles_bitwise_one_row(lsg, dtype, pop):
+    """Rank 64 with shared adapters runs 8-row tiles (one weight read per tile): bitwise
+    the one-row-per-cluster result, for every cluster size."""
+    bounds, _, _ = segments_for(pop, 64, 91)
+    x, A, B = random_problem(5120, 5120, 64, bounds, 92)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    base = p.run()
+    assert row_norm_err(base.double().cpu().numpy(), p.reference()) <= tol(dtype)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 1)
+    assert torch.equal(p.run(), base)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 8)
+    for c in (4, 8, 16):
+        lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
+        assert torch.equal(p.run(), base), c
+        assert torch.equal(p.run("two_launch"), base), c
