@@ -202,8 +202,9 @@ typedef enum {
   LSG_OPT_NO_TENSOR_CORES = 5, /* 1: long segments stay on the CUDA-core kernel (no tcgen05 path) */
   LSG_OPT_TC_SPLIT = 6,        /* 1: rank-16 long segments use the two-kernel tensor-core path
                                   (shrink, then expand through a workspace) instead of the fused one */
-  LSG_OPT_NO_ROW_MODE = 7      /* 1: one-row tiles use the segment-major decode (row split / tile scan)
+  LSG_OPT_NO_ROW_MODE = 7,     /* 1: one-row tiles use the segment-major decode (row split / tile scan)
                                   instead of one cluster per row with a segment search */
+  LSG_OPT_NO_MULTIROW_TILES = 8 /* 1: rank 64 keeps one-row tiles even when rows share adapters */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

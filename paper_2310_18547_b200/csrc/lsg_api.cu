@@ -48,7 +48,7 @@ std::atomic<int> g_opt_no_tile_scan{0};
 std::atomic<int> g_opt_no_tc{0};
 std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
-std::atomic<int> g_opt_no_rank64_tiles{0};  // experiments: LSG_NO_RANK64_TILES=1
+std::atomic<int> g_opt_no_rank64_tiles{0};
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -517,11 +517,7 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
 }  // namespace
 
 bool pdl_enabled() { return g_opt_pdl.load() != 0; }
-static const bool g_rank64_env = [] {
-  const char* e = std::getenv("LSG_NO_RANK64_TILES");
-  if (e && std::atoi(e)) g_opt_no_rank64_tiles = 1;
-  return true;
-}();
+
 
 int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st) {
   return dtype == LSG_F16 ? dispatch_generic<__half>(g, mode, rows, smem, st)
@@ -626,6 +622,7 @@ int lsg_set_option(int32_t option, int32_t value) {
     case LSG_OPT_NO_TENSOR_CORES: g_opt_no_tc = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_TC_SPLIT: g_opt_tc_split = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_NO_ROW_MODE: g_opt_no_row_mode = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_NO_MULTIROW_TILES: g_opt_no_rank64_tiles = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -640,6 +637,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_NO_TENSOR_CORES: return g_opt_no_tc.load();
     case LSG_OPT_TC_SPLIT: return g_opt_tc_split.load();
     case LSG_OPT_NO_ROW_MODE: return g_opt_no_row_mode.load();
+    case LSG_OPT_NO_MULTIROW_TILES: return g_opt_no_rank64_tiles.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
