@@ -9,13 +9,13 @@ namespace lsg {
 template <typename T, int R>
 static int launch_tc_shrink_inst(const TcShrinkParams& p, int nq, int tiles, cudaStream_t st) {
   auto kern = sgmv_tc_shrink_kernel<T, R>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc shrink smem)");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc shrink cluster)");
-    configured = true;
+    mark_configured(configured);
   }
   const dim3 grid(static_cast<unsigned>(nq), static_cast<unsigned>(tiles), 1);
   const int smem = static_cast<int>(tc_shrink_smem(R, p.kcs));
@@ -26,12 +26,12 @@ static int launch_tc_shrink_inst(const TcShrinkParams& p, int nq, int tiles, cud
 template <typename T, int R>
 static int launch_tc_expand_inst(const TcExpandParams& p, int tiles, cudaStream_t st) {
   auto kern = sgmv_tc_expand_kernel<T, R>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
     const cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcExpandLayout<R>::kTotal);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc expand smem)");
-    configured = true;
+    mark_configured(configured);
   }
   const dim3 grid(static_cast<unsigned>(p.h_out / kTcNT), static_cast<unsigned>(tiles), 1);
   const cudaError_t e =
@@ -72,13 +72,13 @@ namespace lsg {
 template <typename T>
 static int launch_tc_fused_inst(const TcFusedParams& p, int C, int tiles, cudaStream_t st) {
   auto kern = sgmv_tc_fused_kernel<T>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc fused smem)");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc fused cluster)");
-    configured = true;
+    mark_configured(configured);
   }
   const dim3 grid(static_cast<unsigned>(C), static_cast<unsigned>(tiles), 1);
   const int smem = static_cast<int>(tcf_layout(p.kcs_max, p.compact).total);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include <string>
 
@@ -33,6 +34,22 @@ struct Plan {
   int row_mode = 0;  // one cluster per row, segment found by search (one-row tiles, no long-segment skip)
   int multi = 0;     // grouped launch over several sites (row mode, fused)
 };
+
+// Function attributes (max dynamic smem, non-portable clusters) are per device:
+// a launcher configures its kernel once for every device it runs on.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline bool configured_on_device(const std::atomic<unsigned long long>& mask) {
+  const int d = current_device();
+  return d < 64 && (mask.load() >> d & 1ull);
+}
+inline void mark_configured(std::atomic<unsigned long long>& mask) {
+  const int d = current_device();
+  if (d < 64) mask.fetch_or(1ull << d);
+}
 
 // Set by the API layer; read at launch.
 bool pdl_enabled();
@@ -82,13 +99,13 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cu
 template <typename T, int R, int MT, int MODE, int ITEM>
 int launch_fast_inst(const FastParams& p, const Plan& pl, cudaStream_t st) {
   auto kern = sgmv_fast_kernel<T, R, MT, MODE, ITEM>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(max dynamic smem)");
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(non-portable cluster)");
-    configured = true;
+    mark_configured(configured);
   }
   int clusters = pl.clusters;
   if (pl.tile_scan) {

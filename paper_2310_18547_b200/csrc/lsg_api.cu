@@ -687,12 +687,12 @@ int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_
   int n_pow2 = 1;
   while (n_pow2 < total_rows) n_pow2 <<= 1;
   const int smem = n_pow2 * static_cast<int>(sizeof(uint64_t));
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(build_segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kBuilderMaxRows * 8);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(builder smem)");
-    configured = true;
+    mark_configured(configured);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1);
