@@ -8,6 +8,7 @@
  *   lsg_sgmv           <- lorasim::lora_addon(const Batch&)        core/include/lorasim/sgmv.hpp:72-73,
  *                         core/src/sgmv.cpp:138-141 (fused, accumulates into y)
  *   lsg_sgmv_multi     <- lora_addon over several projection sites sharing one Batch's segments
+ *   lsg_dense_lora     <- lorasim::dense_projection(const Batch&, w)  sgmv.cpp:143-155 (LoRA in the GEMM epilogue)
  *   lsg_sgmv_shrink    <- lorasim::sgmv_shrink(const Batch&)       sgmv.hpp:64-66, sgmv.cpp:105-119
  *   lsg_sgmv_expand    <- lorasim::sgmv_expand(v, segs, models)    sgmv.hpp:68-70, sgmv.cpp:121-136
  *   lsg_bgmv           <- lorasim::gather_bmm_oracle(const Batch&) sgmv.hpp:81-83, sgmv.cpp:186-217
@@ -126,6 +127,19 @@ typedef struct lsg_sgmv_site {
 int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
                    const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
                    lsg_stream_t stream);
+
+/* Dense projection with the LoRA add in the GEMM epilogue (decode shapes):
+ *   y[s_n, h_out] = x[s_n, h_in] . W[h_in, h_out] + x . A_slot(s) . B_slot(s)   (overwrite)
+ * <- lorasim::dense_projection(const Batch&, const Matrix& w), sgmv.cpp:143-155.
+ * W is row-major [h_in, h_out] (row stride ldw), same dtype as the pool.  The shrink
+ * writes v (fp32, [s_n, rank]) into the caller's workspace; one tcgen05 GEMM launch
+ * then computes x.W per 64-column tile and adds v . B in its epilogue.  Rank 16,
+ * s_n <= 64, h_in % 64 == 0, h_out % 64 == 0 (else LSG_EUNSUPPORTED). */
+size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows);
+int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
+                   const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
+                   int32_t num_segments, int32_t total_rows, int32_t layer, void* workspace,
+                   size_t workspace_bytes, lsg_stream_t stream);
 
 /* Shrink only: v[s_n, rank] (fp32, row stride rank) = x . A per segment (overwrite). */
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,

@@ -25,6 +25,7 @@ EXPORTED = (
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
     "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments", "lsg_sgmv_multi",
+    "lsg_dense_lora", "lsg_dense_lora_workspace_size",
 )
 
 
@@ -84,6 +85,9 @@ def lib() -> C.CDLL:
         L.lsg_sgmv.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp]
         L.lsg_sgmv_ws.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
         L.lsg_sgmv_multi.argtypes = [C.POINTER(Site), i32, vp, vp, i32, i32, i32, vp]
+        L.lsg_dense_lora.argtypes = [vp, i64, vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
+        L.lsg_dense_lora_workspace_size.argtypes = [tp, i32]
+        L.lsg_dense_lora_workspace_size.restype = C.c_size_t
         L.lsg_sgmv_workspace_size.argtypes = [tp, i32]
         L.lsg_sgmv_workspace_size.restype = C.c_size_t
         L.lsg_sgmv_shrink.argtypes = [vp, vp, i64, tp, vp, vp, i32, i32, i32, vp]

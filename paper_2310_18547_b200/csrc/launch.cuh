@@ -67,6 +67,8 @@ int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int t
 int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st);
 struct TcFusedParams;
 int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st);
+struct DenseLoraParams;
+int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st);
 
 template <typename K>
 cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cudaStream_t st,

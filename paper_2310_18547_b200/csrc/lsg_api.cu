@@ -586,6 +586,63 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
              seg_slot, nullptr, num_segments, total_rows, layer, stream, nullptr, 0, true, sites, num_sites);
 }
 
+size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
+  if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
+  return static_cast<size_t>(total_rows) * tbl->rank * sizeof(float);
+}
+
+int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
+                   const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
+                   int32_t num_segments, int32_t total_rows, int32_t layer, void* workspace,
+                   size_t workspace_bytes, lsg_stream_t stream) {
+  int st = validate_table(tbl);
+  if (st != LSG_OK) return st;
+  if (total_rows < 0 || num_segments < 0) return fail(LSG_EINVAL, "lsg_dense_lora: negative sizes");
+  if (layer < 0 || layer >= tbl->num_layers) return fail(LSG_EINVAL, "lsg: layer index out of range");
+  if (total_rows == 0) return LSG_OK;
+  if (x == nullptr || y == nullptr || w == nullptr || seg_starts == nullptr || seg_slot == nullptr)
+    return fail(LSG_EINVAL, "lsg_dense_lora: NULL pointer");
+  if (ldx < tbl->h_in || ldy < tbl->h_out || ldw < tbl->h_out) return fail(LSG_EINVAL, "lsg_dense_lora: bad strides");
+  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % kTcKB != 0 || tbl->h_out % kDlN != 0 ||
+      !aligned16(x) || !aligned16(y) || !aligned16(w) || ldx % 8 != 0 || ldy % 8 != 0 || ldw % 8 != 0 ||
+      tbl->b_layer_stride % 8 != 0 || encode_tiled_fn() == nullptr)
+    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 64, h_out % 64, 16-byte rows");
+  if (workspace == nullptr || workspace_bytes < lsg_dense_lora_workspace_size(tbl, total_rows) || !aligned16(workspace))
+    return fail(LSG_EINVAL, "lsg_dense_lora: workspace too small");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  float* v = static_cast<float*>(workspace);
+  st = run(kKShrink, nullptr, 0, x, ldx, v, nullptr, tbl, seg_starts, seg_slot, nullptr, num_segments, total_rows,
+           layer, stream);
+  if (st != LSG_OK) return st;
+  DenseLoraParams p{};
+  if (!encode_rows_map(&p.tmap_x, tbl->dtype, x, tbl->h_in, total_rows, ldx)) return fail(LSG_ECUDA, "tensor map x");
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_out), static_cast<cuuint64_t>(tbl->h_in)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kDlN), static_cast<cuuint32_t>(kTcKB)};
+    const cuuint32_t estr[2] = {1, 1};
+    if (encode_tiled_fn()(&p.tmap_w,
+                          tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          const_cast<void*>(w), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(LSG_ECUDA, "tensor map W");
+  }
+  p.y = y;
+  p.ldy = ldy;
+  p.v = v;
+  p.b_ptr = tbl->b_ptr;
+  p.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+  p.seg_starts = seg_starts;
+  p.seg_slot = seg_slot;
+  p.n_seg = num_segments;
+  p.s_n = total_rows;
+  p.num_slots = tbl->num_slots;
+  p.h_in = tbl->h_in;
+  p.h_out = tbl->h_out;
+  return launch_dense_lora(tbl->dtype, p, cs);
+}
+
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,
                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
                     int32_t total_rows, int32_t layer, lsg_stream_t stream) {

@@ -891,3 +891,162 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __gr
 }
 
 }  // namespace lsg
+
+namespace lsg {
+
+// ---------------------------------------------------------------------------------------
+// Dense projection with the LoRA add in the GEMM epilogue, decode shape
+// (s_n <= 64 rows): y = x . W + v . B_seg(row)   (reference dense_projection,
+// sgmv.cpp:143-155: x.W + lora_addon).  v = x . A comes from the shrink kernel.
+// One CTA per 64-column tile of y: x (K-major) and W (MN-major) stream through a TMA
+// ring into tcgen05.mma (D = x . W, fp32 in TMEM, M = 128 with rows >= s_n zero);
+// every row's B slice for the tile is staged by cp.async at kernel entry (weights,
+// ahead of the PDL wait); the epilogue adds sum_k v[m,k] B[k,n] (fp32 chain over k)
+// to D and rounds once.
+// ---------------------------------------------------------------------------------------
+constexpr int kDlN = 64;       // columns per CTA
+constexpr int kDlMaxRows = 64;  // decode rows per launch
+constexpr int kDlStages = 3;
+constexpr int kDlStage = kTcBox + kTcKB * kDlN * 2;  // x box 16 KB + W box 8 KB
+
+struct DenseLoraParams {
+  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 128, SW128
+  CUtensorMap tmap_w;  // W [h_in, h_out] row-major, box 64 (N) x 64 (K), SW128
+  void* y;
+  int64_t ldy;
+  const float* v;      // [s_n, R] fp32
+  const void* const* b_ptr;
+  int64_t b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  int32_t n_seg, s_n, num_slots, h_in, h_out;
+};
+
+template <int R>
+__host__ __device__ constexpr uint32_t dl_smem() {
+  return kDlStages * kDlStage + kDlMaxRows * R * kDlN * 2 + 256 + 1024;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_constant__ DenseLoraParams p) {
+  constexpr int fmt = std::is_same<T, __half>::value ? 0 : 1;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* Bsm = smem + kDlStages * kDlStage;  // [row][k][64 cols] 16-bit
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Bsm + kDlMaxRows * R * kDlN * 2);  // full[4], empty[4], D
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = static_cast<int>(blockIdx.x) * kDlN;
+  const int nkb = p.h_in / kTcKB;
+
+  if (tid == 0) {
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+    prefetch_tmap(&p.tmap_x);
+    prefetch_tmap(&p.tmap_w);
+  }
+  if (warp == 0) tmem_alloc<kDlN>(tmem_slot);
+  // Row m's adapter slot: the last segment s with seg_starts[s] <= m (thread m < s_n).
+  const int m = tid;
+  int slot = -1;
+  if (m < p.s_n) {
+    int lo = 0, hi = p.n_seg;  // first s with seg_starts[s + 1] > m
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (p.seg_starts[mid + 1] > m) hi = mid; else lo = mid + 1;
+    }
+    slot = lo < p.n_seg ? p.seg_slot[lo] : -1;
+    if (slot >= p.num_slots) slot = -1;
+  }
+  if (slot >= 0) {  // this row's B[:, n0 : n0 + 64] (weights: before the PDL wait)
+    const T* B = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+#pragma unroll
+      for (int c = 0; c < kDlN / 8; ++c)
+        cp_async16(Bsm + ((m * R + k) * kDlN + c * 8) * 2, B + static_cast<int64_t>(k) * p.h_out + c * 8);
+  }
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  pdl_wait();  // x and v come from the preceding kernels
+  pdl_launch_dependents();
+  if (warp == 1 && lane == 0) {  // TMA producer: x box + W box per K step
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDlStages;
+      if (kb >= kDlStages) mbar_wait(&bars[4 + s], ((kb / kDlStages) - 1) & 1);
+      mbar_arrive_expect_tx(&bars[s], kDlStage);
+      uint8_t* st = smem + s * kDlStage;
+      tma_load_2d(st, &p.tmap_x, kb * kTcKB, 0, &bars[s]);
+      tma_load_2d(st + kTcBox, &p.tmap_w, n0, kb * kTcKB, &bars[s]);
+    }
+  } else if (warp == 0 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = umma_idesc(fmt, kTcM, kDlN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDlStages;
+      mbar_wait(&bars[s], (kb / kDlStages) & 1);
+      tc_fence_after();
+      const uint32_t xa = smem_u32(smem + s * kDlStage), wa = xa + kTcBox;
+#pragma unroll
+      for (int ks = 0; ks < kTcKB / 16; ++ks) {
+        const uint64_t ad = umma_desc(xa + ks * 32, 16, 1024, kSw128);            // x: K-major SW128
+        const uint64_t bd = umma_desc(wa + ks * 2 * 1024, 8 * 1024, 1024, kSw128);  // W: MN-major SW128
+        umma_f16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+      }
+      umma_commit(&bars[4 + s]);
+    }
+    umma_commit(&bars[8]);
+  }
+  __syncwarp();
+  // v[m, :] and this row's B slice while the MMAs run
+  float v[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = 0.f;
+  if (slot >= 0) {
+#pragma unroll
+    for (int k = 0; k < R; k += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p.v + static_cast<int64_t>(m) * R + k);
+      v[k] = q.x, v[k + 1] = q.y, v[k + 2] = q.z, v[k + 3] = q.w;
+    }
+  }
+  cp_async_wait<0>();
+  mbar_wait(&bars[8], 0);
+  tc_fence_after();
+#pragma unroll
+  for (int c = 0; c < kDlN / 16; ++c) {
+    float acc[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, acc);  // all threads (aligned)
+    if (m < p.s_n) {
+      float lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) lo[j] = 0.f;
+      if (slot >= 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float b[16];
+          const uint4* br = reinterpret_cast<const uint4*>(Bsm + ((m * R + k) * kDlN + c * 16) * 2);
+          Cvt<T>::unpack8(br[0], b);
+          Cvt<T>::unpack8(br[1], b + 8);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) lo[j] = fmaf(v[k], b[j], lo[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = acc[j] + lo[j];
+      T* yr = static_cast<T*>(p.y) + static_cast<int64_t>(m) * p.ldy + n0 + c * 16;
+      st_global_v4(yr, Cvt<T>::pack8(acc));
+      st_global_v4(yr + 8, Cvt<T>::pack8(acc + 8));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<kDlN>(tmem);
+  }
+}
+
+}  // namespace lsg

@@ -133,6 +133,24 @@ def sgmv_multi(ys, xs, pools, seg_starts: torch.Tensor, seg_slot: torch.Tensor, 
     return ys
 
 
+def dense_lora(y: torch.Tensor, x: torch.Tensor, w: torch.Tensor, pool: AdapterPool, seg_starts: torch.Tensor,
+               seg_slot: torch.Tensor, layer: int, num_segments: int | None = None) -> torch.Tensor:
+    """``y = x . W + x . A_slot . B_slot`` (overwrite): the dense projection with the LoRA add
+    in the GEMM epilogue (lsg_dense_lora; rank 16, <= 64 rows).  W is ``[h_in, h_out]``."""
+    _rows_check(x, y, pool)
+    _check_i32(seg_starts, "seg_starts")
+    _check_i32(seg_slot, "seg_slot")
+    if w.dtype != pool.dtype or not w.is_cuda or w.dim() != 2 or w.stride(1) != 1 or \
+            tuple(w.shape) != (pool.h_in, pool.h_out):
+        raise ValueError(f"w must be a CUDA [{pool.h_in}, {pool.h_out}] {pool.dtype} tensor with unit column stride")
+    n = seg_slot.numel() if num_segments is None else num_segments
+    wsb = int(_lib.lib().lsg_dense_lora_workspace_size(C.byref(pool.table), x.shape[0]))
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=x.device)
+    _lib.call("lsg_dense_lora", _ptr(y), y.stride(0), _ptr(x), x.stride(0), _ptr(w), w.stride(0), C.byref(pool.table),
+              _ptr(seg_starts), _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws), ws.numel(), _stream())
+    return y
+
+
 def sgmv_workspace_size(pool: AdapterPool, rows: int) -> int:
     """Bytes of workspace a fused call over ``rows`` rows may use (0: none)."""
     return int(_lib.lib().lsg_sgmv_workspace_size(C.byref(pool.table), rows))
@@ -217,6 +235,6 @@ def query_launch(pool: AdapterPool, num_segments: int, total_rows: int, kernel: 
     return {f: getattr(info, f) for f, _ in LaunchInfo._fields_}
 
 
-__all__ = ["AdapterPool", "sgmv", "sgmv_multi", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
+__all__ = ["AdapterPool", "sgmv", "sgmv_multi", "dense_lora", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
            "scatter_rows", "set_option", "get_option", "query_launch", "KERNEL_FUSED", "KERNEL_SHRINK",
            "KERNEL_EXPAND", "KERNEL_BGMV"]

@@ -544,3 +544,37 @@ def test_rank64_multirow_tiles_bitwise_one_row(lsg, dtype, pop):
         lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
         assert torch.equal(p.run(), base), c
         assert torch.equal(p.run("two_launch"), base), c
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("pop,batch", [(DISTINCT, 64), (UNIFORM, 37), (IDENTICAL, 8)])
+def test_dense_lora_matches_oracle_dense_projection(lsg, dtype, pop, batch):
+    """lsg_dense_lora = dense_projection (sgmv.cpp:143-155): x.W + lora_addon, LoRA in the
+    GEMM epilogue; checked against the fp64 oracle and against cuBLAS + the SGMV kernel."""
+    h_in, h_out, r = 4096, 2048, 16
+    bounds, _, _ = segments_for(pop, batch, 44)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 45)
+    W = oracle().rng(46).fill_pm1(h_in * h_out).reshape(h_in, h_out) * 0.05
+    p = Problem(lsg, x, A, B, bounds, dtype, layers=2, layer=1)
+    Wq = torch.tensor(W, dtype=torch.float64).to(dtype).cuda()
+    y = torch.full((batch, h_out), float("nan"), dtype=dtype, device="cuda")
+    lsg.dense_lora(y, p.x, Wq, p.pool, p.seg_starts, p.seg_slot, 1)
+    torch.cuda.synchronize()
+    ref = p.xd @ Wq.double().cpu().numpy() + oracle().lora_addon(p.xd, p.bounds, p.Ad, p.Bd)
+    err = row_norm_err(y.double().cpu().numpy(), ref)
+    assert err <= tol(dtype), err
+    y2 = (p.x.float() @ Wq.float()).to(dtype)  # cuBLAS GEMM, then the SGMV kernel adds the LoRA
+    lsg.sgmv(y2, p.x, p.pool, p.seg_starts, p.seg_slot, 1)
+    torch.cuda.synchronize()
+    assert row_norm_err(y.double().cpu().numpy(), y2.double().cpu().numpy()) <= 2 * tol(dtype)
+
+
+def test_dense_lora_rejects_unsupported(lsg):
+    pool = lsg.AdapterPool(2, 1, 4096, 4096, 32, torch.float16)
+    x = torch.zeros(4, 4096, dtype=torch.float16, device="cuda")
+    y = torch.zeros_like(x)
+    w = torch.zeros(4096, 4096, dtype=torch.float16, device="cuda")
+    ss = torch.tensor([0, 4], dtype=torch.int32, device="cuda")
+    sl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with pytest.raises(RuntimeError, match="rank 16"):
+        lsg.dense_lora(y, x, w, pool, ss, sl, 0)
