@@ -134,7 +134,8 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
  * W is row-major [h_in, h_out] (row stride ldw), same dtype as the pool.  The shrink
  * writes v (fp32, [s_n, rank]) into the caller's workspace; one tcgen05 GEMM launch
  * then computes x.W per 64-column tile and adds v . B in its epilogue.  Rank 16,
- * s_n <= 64, h_in % 64 == 0, h_out % 64 == 0 (else LSG_EUNSUPPORTED). */
+ * s_n <= 64, h_in % 256 == 0, h_out % 64 == 0 (else LSG_EUNSUPPORTED).  A cluster of 4 CTAs
+ * splits K per 64-column tile; the partial products are summed over DSMEM in CTA order. */
 size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows);
 int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
                    const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
