@@ -603,10 +603,10 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
   if (x == nullptr || y == nullptr || w == nullptr || seg_starts == nullptr || seg_slot == nullptr)
     return fail(LSG_EINVAL, "lsg_dense_lora: NULL pointer");
   if (ldx < tbl->h_in || ldy < tbl->h_out || ldw < tbl->h_out) return fail(LSG_EINVAL, "lsg_dense_lora: bad strides");
-  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % kTcKB != 0 || tbl->h_out % kDlN != 0 ||
+  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % (kTcKB * kDlKS) != 0 || tbl->h_out % kDlN != 0 ||
       !aligned16(x) || !aligned16(y) || !aligned16(w) || ldx % 8 != 0 || ldy % 8 != 0 || ldw % 8 != 0 ||
       tbl->b_layer_stride % 8 != 0 || encode_tiled_fn() == nullptr)
-    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 64, h_out % 64, 16-byte rows");
+    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 256, h_out % 64, 16-byte rows");
   if (workspace == nullptr || workspace_bytes < lsg_dense_lora_workspace_size(tbl, total_rows) || !aligned16(workspace))
     return fail(LSG_EINVAL, "lsg_dense_lora: workspace too small");
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
