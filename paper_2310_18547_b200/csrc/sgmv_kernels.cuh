@@ -658,20 +658,21 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
             for (int o = tid; o < no; o += kThreads) V_sm[o] = ordered_sum(recv + o, MT * R, p.nq);
           }
         } else {
-          for (int o = o0 + tid; o < o1; o += kThreads) {
-            float s = 0.f;
-            s = ordered_sum(recv + (o - o0), slice_max, p.nq);
-            if constexpr (MODE == kShrink) {
+          if constexpr (MODE == kShrink) {
+            for (int o = o0 + tid; o < o1; o += kThreads) {
+              const float s = ordered_sum(recv + (o - o0), slice_max, p.nq);
               const int m = o / R;
               p.v_out[static_cast<int64_t>(r0 + m) * R + (o - m * R)] = s;
-            } else {
-              const uint32_t local = smem_u32(V_sm + o), lbar = smem_u32(&bars[kBarV]);
-              for (int dst = 0; dst < C; ++dst) {
-                uint32_t ra, rb;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lbar), "r"(dst));
-                st_async_f32(ra, s, rb);
-              }
+            }
+          } else {
+            // my slice of v, 4 outputs per thread, broadcast to every CTA as 16-byte pushes
+            for (int o = o0 + 4 * tid; o < o1; o += 4 * kThreads) {
+              float s4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) s4[e] = ordered_sum(recv + (o - o0) + e, slice_max, p.nq);
+              for (int dst = 0; dst < C; ++dst)
+                st_async_v4(mapa_u32(V_sm + o, static_cast<uint32_t>(dst)), s4[0], s4[1], s4[2], s4[3],
+                            mapa_u32(&bars[kBarV], static_cast<uint32_t>(dst)));
             }
           }
           if constexpr (MODE == kFused) mbar_wait(&bars[kBarV], phase);
