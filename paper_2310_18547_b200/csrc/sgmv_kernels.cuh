@@ -551,15 +551,19 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
                 for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(xm, a[j], acc[m][j]);
               }
             }
+            if (ql == warp) LSG_TRACE(9);  // warp 0: FMA chains of its first unit done
             const int q = q0 + ql;
             const int g = lane / VPR;
+            // butterflies of all rows level by level (independent shuffle chains interleave)
+#pragma unroll
+            for (int off = VPR; off < 32; off <<= 1)
+#pragma unroll
+              for (int m = 0; m < MT; ++m)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
               if (m >= rows) break;  // warp-uniform
-#pragma unroll
-              for (int off = VPR; off < 32; off <<= 1)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int o = m * R + vec * 8 + h * 4;
@@ -580,6 +584,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
                 }
               }
             }
+            if (ql == warp) LSG_TRACE(13);  // warp 0: first unit pushed
           }
         } else {
         const int nunits = nqc * rows;
