@@ -328,7 +328,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int nq = t->h_in / KW, ncvt = t->h_out / 8;
   // one-round reduction (every CTA receives every chunk partial) while that
   // receive buffer stays <= 16 KB; otherwise owner-sliced with a second round
-  auto red_all_for = [&](int c) { return pl.mode == kFused && (pl.mt == 1 || nq * pl.mt * t->rank <= 4096) ? 1 : 0; };
+  auto red_all_for = [&](int) { return pl.mode == kFused && pl.mt == 1 ? 1 : 0; };  // must match the kernel
   // Single-tile clusters (every segment one tile) keep only A resident ahead of
   // the PDL wait and prefetch B into L2, so two launches' CTAs fit per SM.
   // (s_n == n_seg: every segment is one row, so every cluster has exactly one tile)

@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // one-row tiles always use the one-round reduction (compile-time: the owner-sliced
   // path is not even emitted into those instantiations)
-  const int red_all = MODE == kFused ? (MT == 1 ? 1 : p.red_all) : 0;
+  // (multi-row tiles always use the owner-sliced two-round reduction: compile-time too)
+  constexpr int red_all = MODE == kFused && MT == 1 ? 1 : 0;
   const int alias_ab = MODE == kFused ? p.alias_ab : 0;
   const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all, alias_ab);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
               for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
             const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
             const T* xc = x_sm + ql * KW + rowoff;
-#pragma unroll 4
+#pragma unroll 2  // code size: the multi-row body is large (instruction fetch is on the critical path)
             for (int it = 0; it < ITER; ++it) {
               float a[8];
               Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
@@ -704,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
               for (int r = 0; r < RG; ++r)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
-#pragma unroll 8
+#pragma unroll 4
               for (int k = 0; k < R; ++k) {
                 float b[8];
                 Cvt<T>::unpack8(B_sm[k * ncv + cv], b);
