@@ -578,3 +578,33 @@ def test_dense_lora_rejects_unsupported(lsg):
     sl = torch.zeros(1, dtype=torch.int32, device="cuda")
     with pytest.raises(RuntimeError, match="rank 16"):
         lsg.dense_lora(y, x, w, pool, ss, sl, 0)
+
+
+@pytest.mark.parametrize("lens", [[1] * 64, [3, 0, 5, 1, 7], [200, 1, 1, 30, 129], [1000]])
+def test_pdl_chain_of_dependent_launches(lsg, lens):
+    """With programmatic dependent launch, each launch of a chain reads the y its predecessor
+    wrote (y_a -> y_b -> y_a ...): 12 dependent launches (long segments take the tensor-core
+    kernels, whose CTAs without work leave early) equal the same chain without PDL, bit for bit."""
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    nseg, rows = len(lens), int(bounds[-1])
+    g = oracle().rng(123)
+    pool = lsg.AdapterPool(nseg, 12, 4096, 4096, 16, torch.float16)
+    pool.a.copy_(torch.tensor(g.fill_pm1(pool.a.numel()).reshape(pool.a.shape) * 0.01).half())
+    pool.b.copy_(torch.tensor(g.fill_pm1(pool.b.numel()).reshape(pool.b.shape) * 0.05).half())
+    x = torch.tensor(g.fill_pm1(rows * 4096).reshape(rows, 4096)).half().cuda()
+    ss = torch.tensor(bounds.astype(np.int64), dtype=torch.int32, device="cuda")
+    sl = torch.arange(nseg, dtype=torch.int32, device="cuda")
+    out = []
+    for pdl in (0, 1):
+        lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+        bufs = [x.clone(), torch.zeros_like(x)]
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for layer in range(12):  # launch i reads bufs[i % 2], accumulates into bufs[(i + 1) % 2]
+                lsg.sgmv(bufs[(layer + 1) % 2], bufs[layer % 2], pool, ss, sl, layer)
+        torch.cuda.synchronize()
+        out.append([b.clone() for b in bufs])
+    lsg.set_option(lsg.LSG_OPT_PDL, 0)
+    for a, b in zip(*out):
+        assert torch.isfinite(a.float()).all()
+        assert torch.equal(a, b)
