@@ -162,6 +162,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tmap, const void
 }
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Wait only until the bulk stores have READ their shared-memory source (the global writes
+// complete asynchronously and are covered by the grid's completion): enough before a CTA
+// exits or reuses the staging.
+__device__ __forceinline__ void bulk_wait_group_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(kTcThreads) sgmv_tc_expand_kernel(const __grid
 #pragma unroll
       for (int b = 0; b < 4; ++b) tma_store_2d(&p.tmap_y, smem + L::kY + b * kTcBox, n0 + b * kTcKB, r0);
       bulk_commit_group();
-      bulk_wait_group0();
+      bulk_wait_group_read0();
     }
   } else if (m < rows) {  // last tile of a segment: only the segment's rows
     T* yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0 + m) * p.ldy + n0;
@@ -880,7 +886,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __gr
       __syncthreads();
     }
   }
-  if (tid == 0) bulk_wait_group0();  // TMA stores have read their staging before exit
+  if (tid == 0) bulk_wait_group_read0();  // TMA stores have read their staging before exit
   LSG_TC_TRACE(0, 7);
   tc_fence_before();
   __syncthreads();
