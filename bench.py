@@ -429,7 +429,7 @@ def main():
         with torch.cuda.stream(stream):
             graph_g.replay()
         kg = max(3, a.steps // 2)
-        extra["grouped_us_per_site"] = timed(graph_g.replay, kg) * 1e3 / (kg * sites)
+        extra["grouped_us_per_site"] = timed(graph_g.replay, kg) * 1e3 / (kg * sites * world)  # as `value`
         extra["grouped_launches_per_layer"] = 4
 
 
