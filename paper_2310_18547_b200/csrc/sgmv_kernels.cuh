@@ -694,9 +694,9 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
           mbar_wait(&bars[kBarB], wphase);
           LSG_TRACE(10);
           if constexpr (MT > 1) {
-            // Multi-row tiles: item = (column vector, pair of rows); each B vector is
-            // read and converted once for both rows (same per-element chain over k).
-            constexpr int RG = 2;
+            // Multi-row tiles: item = (column vector, 4 rows); each B vector is
+            // read and converted once for the 4 rows (same per-element chain over k).
+            constexpr int RG = 4;
             const int ngr = (rows + RG - 1) / RG;
             for (int i = tid; i < ngr * ncv; i += kThreads) {
               const int gr = i / ncv, cv = i - gr * ncv;
