@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from paper_2310_18547_b200.adapters import SlotTable
-from tests._util import TOL, oracle, random_problem, row_norm_err
+from tests._util import TOL, oracle, row_norm_err
 
 
 def test_slot_table_lru_and_pinning():

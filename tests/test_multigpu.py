@@ -10,7 +10,6 @@ unsharded expand.  The GPU side of the same property (partitioned kernel output
 """
 from __future__ import annotations
 
-import os
 import socket
 
 import numpy as np
