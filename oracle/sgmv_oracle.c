@@ -214,7 +214,7 @@ int orc_lora_addon(const double* x, size_t h_in, const size_t* bounds, size_t ns
                    const double* A, const double* B, size_t rank, size_t h_out, double* y) {
   if (nseg == 0) return 0;
   const size_t rows = bounds[nseg];
-  double* v = (double*)malloc(sizeof(double) * (rows * rank ? rows * rank : 1));
+  double* v = (double*)malloc(sizeof(double) * (rows * rank != 0 ? rows * rank : 1));
   int st = orc_sgmv_shrink(x, h_in, bounds, nseg, A, rank, v);
   if (!st) st = orc_sgmv_expand(v, rank, bounds, nseg, B, h_out, y);
   free(v);
