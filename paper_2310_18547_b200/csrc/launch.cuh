@@ -148,6 +148,10 @@ int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
     return pl.tile_scan ? launch_fast_inst<T, R, 1, MODE, kItemTileScan>(p, pl, st)
                         : launch_fast_inst<T, R, 1, MODE, kItemRowSplit>(p, pl, st);
   }
+  if (pl.mt == 4) {  // rank-64 fused launches with shared adapters (tile scan)
+    if constexpr (R == 64 && MODE == kFused) return launch_fast_inst<T, R, 4, MODE, kItemTileScan>(p, pl, st);
+    return fail(LSG_EINVAL, "lsg: 4-row tiles are rank-64 fused only");
+  }
   return pl.tile_scan ? launch_fast_inst<T, R, 8, MODE, kItemTileScan>(p, pl, st)
                       : launch_fast_inst<T, R, 8, MODE, kItemRowSplit>(p, pl, st);
 }

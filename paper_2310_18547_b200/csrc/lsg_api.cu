@@ -50,6 +50,7 @@ std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
 std::atomic<int> g_opt_no_rank64_tiles{0};
 
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -307,7 +308,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   else if (forced_mt == 1 || forced_mt == 8)
     pl.mt = forced_mt;
   else if (t->rank == 64 && s_n > n_seg && !g_opt_no_rank64_tiles.load())
-    pl.mt = 8;  // rank 64 with shared adapters: one weight read per 8-row tile (c3, profiles/README.md)
+    pl.mt = kernel == kKFused ? 4 : 8;  // rank 64, shared adapters: one weight read per tile (c3: 4 rows, C = 4)
   else
     pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
   if (kernel == kKBgmv) {
@@ -356,9 +357,9 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::gcd(nq, ncvt));
   const int64_t est_clusters = long_on_tc ? n_seg : pl.clusters;
   int c = 0, c_small = 0;
-  // Multi-row tiles carry MT rows of compute per CTA: clusters above 8 measured slower
-  // (rank 64, c3: C = 16 27.3 us vs C = 8 16.7 us).
-  const int c_cap = pl.mt > 1 ? 8 : kMaxCluster;
+  // Multi-row tiles carry MT rows of compute per CTA: clusters above MT measured slower
+  // (rank 64, c3: MT = 8 C = 16 27.3 us vs C = 8 16.0 us; MT = 4 C = 8 23.4 us vs C = 4 14.8 us).
+  const int c_cap = pl.mt > 1 ? pl.mt : kMaxCluster;
   for (int cand = 1; cand <= c_cap; ++cand) {
     if (span % cand != 0 && cand != c_cap) continue;
     if (smem_for(cand) > kSmemBudget) continue;
