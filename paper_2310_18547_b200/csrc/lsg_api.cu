@@ -367,7 +367,12 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     const int64_t limit = (pl.tile_scan || cand <= 4) ? 256 : 148;
     if (est_clusters * cand <= limit) c = cand;
   }
-  if (c == 0) c = c_small > 0 ? c_small : c_cap;
+  if (c == 0) c = c_small;
+  // nothing within the cap fits shared memory (e.g. rank 64 at h = 8192): the smallest
+  // larger cluster that does
+  for (int cand = c_cap + 1; c == 0 && cand <= kMaxCluster; ++cand)
+    if ((span % cand == 0 || cand == kMaxCluster) && smem_for(cand) <= kSmemBudget) c = cand;
+  if (c == 0) c = kMaxCluster;
   const int forced = g_opt_force_cluster.load();
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);

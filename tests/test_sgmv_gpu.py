@@ -527,6 +527,19 @@ def test_grouped_sites_fall_back_with_long_segments(lsg):
         assert row_norm_err(ys[i].double().cpu().numpy(), probs[i].reference()) <= tol(torch.bfloat16)
 
 
+@pytest.mark.parametrize("h", [4096, 8192])
+def test_rank64_multirow_tiles_large_hidden(lsg, h):
+    """Multi-row rank-64 tiles at h = 8192 need a cluster above the tile-row cap to fit
+    shared memory: still correct and bitwise the one-row result."""
+    bounds, _, _ = segments_for(UNIFORM, 32, 93)
+    x, A, B = random_problem(h, h, 64, bounds, 94)
+    p = Problem(lsg, x, A, B, bounds, torch.bfloat16)
+    base = p.run()
+    assert row_norm_err(base.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 1)
+    assert torch.equal(p.run(), base)
+
+
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("pop", [UNIFORM, SKEWED])
 def test_rank64_multirow_tiles_bitwise_one_row(lsg, dtype, pop):
