@@ -35,13 +35,16 @@ namespace cg = cooperative_groups;
 #ifndef LSG_MIN_BLOCKS
 #define LSG_MIN_BLOCKS 3  // co-resident CTAs per SM the register budget is sized for (measured best)
 #endif
+#ifndef LSG_PIECES
+#define LSG_PIECES 4
+#endif
 #ifndef LSG_THREADS
 #define LSG_THREADS 256
 #endif
 constexpr int kThreads = LSG_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int KW = 128;     // rows of A (h_in elements) per canonical reduction chunk
-constexpr int kPieces = 4;  // A arrives in up to 4 bulk copies, one mbarrier each
+constexpr int kPieces = LSG_PIECES;  // A arrives in up to kPieces bulk copies, one mbarrier each
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 
