@@ -303,6 +303,10 @@ def main():
     bounds = [int(v) for v in mine.seg_starts]
     batch = mine.num_rows
     nseg = len(bounds) - 1
+    # The serving engine knows its step's segment lengths: a decode-only step (no segment
+    # of >= 128 rows) skips the tensor-core pass (LSG_OPT_TC_MIN_ROWS, include/lsg_sgmv.h).
+    if max(np.diff(bounds), default=0) < 128:
+        lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, batch + 1)
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
     nslots = max(a.slots, nseg)
     pool = lsg.AdapterPool(nslots, sites, h, h, r, dtype)

@@ -94,14 +94,11 @@ int tc_tile_bound(int s_n, int n_seg) {
   return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows()));
 }
 
-// Rows from which a segment takes the tensor-core path (LSG_TC_MIN_ROWS: experiments only).
+// Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default).
+std::atomic<int> g_opt_tc_min_rows{0};
 int tc_min_rows() {
-  static const int v = [] {
-    const char* e = std::getenv("LSG_TC_MIN_ROWS");
-    const int x = e ? std::atoi(e) : 0;
-    return x > 0 ? x : kTcMinRows;
-  }();
-  return v;
+  const int x = g_opt_tc_min_rows.load();
+  return x > 0 ? x : kTcMinRows;
 }
 
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
@@ -686,6 +683,10 @@ int lsg_set_option(int32_t option, int32_t value) {
     case LSG_OPT_TC_SPLIT: g_opt_tc_split = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_NO_ROW_MODE: g_opt_no_row_mode = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_NO_MULTIROW_TILES: g_opt_no_rank64_tiles = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_TC_MIN_ROWS:
+      if (value < 0) return fail(LSG_EINVAL, "lsg: tensor-core row threshold must be >= 0");
+      g_opt_tc_min_rows = value;
+      return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -701,6 +702,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_TC_SPLIT: return g_opt_tc_split.load();
     case LSG_OPT_NO_ROW_MODE: return g_opt_no_row_mode.load();
     case LSG_OPT_NO_MULTIROW_TILES: return g_opt_no_rank64_tiles.load();
+    case LSG_OPT_TC_MIN_ROWS: return g_opt_tc_min_rows.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

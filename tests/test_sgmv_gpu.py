@@ -35,7 +35,8 @@ def lsg():
 def _reset_options(lsg):
     yield
     for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
-                lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE):
+                lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE,
+                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES):
         lsg.set_option(opt, 0)
 
 
@@ -621,3 +622,23 @@ def test_pdl_chain_of_dependent_launches(lsg, lens):
     for a, b in zip(*out):
         assert torch.isfinite(a.float()).all()
         assert torch.equal(a, b)
+
+
+def test_tc_row_threshold_option(lsg):
+    """LSG_OPT_TC_MIN_ROWS moves the tensor-core threshold: above the batch size every segment
+    stays on the CUDA-core kernel (bitwise the no-tensor-core run); results stay in tolerance."""
+    bounds = np.array([0, 200, 203, 260], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 95)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    ref = p.reference()
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 1)
+    cc = p.run()
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 0)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, 261)
+    assert torch.equal(p.run(), cc)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, 50)  # the 57-row segment joins the tensor cores
+    y = p.run()
+    assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(torch.float16)
+    assert torch.equal(y[200:203], cc[200:203])  # the 3-row segment is untouched by the change
+    with pytest.raises(RuntimeError):
+        lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, -1)
