@@ -192,7 +192,11 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
   constexpr int ITER = KW / RPI;   // per-lane FMA chain length per chunk
   constexpr bool kSh = MODE != kExpand;
   constexpr bool kEx = MODE != kShrink;
-  constexpr int kBarB = kPieces, kBarRed = kPieces + 1, kBarV = kPieces + 2;
+  constexpr int kBarB = kPieces, kBarRed = kPieces + 1, kBarV = kPieces + 2, kBarX = kPieces + 3,
+                kBarY = kPieces + 4;
+  // One-row fused tiles move x / y_old with one bulk copy each (mbarrier-completed)
+  // instead of per-thread cp.async + a block barrier.
+  constexpr bool kActBulk = MT == 1 && MODE == kFused;
 
   extern __shared__ __align__(128) uint8_t smem[];
   // A CTA that leaves without work: with PDL a grid's completion must imply its
@@ -236,6 +240,10 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
     for (int i = 0; i <= kBarB; ++i) mbar_init(&bars[i], 1);
     mbar_init(&bars[kBarRed], 1);  // completed by the bytes the cluster pushes (st.async complete_tx)
     mbar_init(&bars[kBarV], 1);
+    if constexpr (kActBulk) {
+      mbar_init(&bars[kBarX], 1);
+      mbar_init(&bars[kBarY], 1);
+    }
     fence_mbar_init();
   }
 
@@ -488,7 +496,18 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
       const int o0 = split_lo(crank, no / 4, C) * 4, o1 = split_lo(crank + 1, no / 4, C) * 4;
       // Activations go through cp.async (LDGSTS), not the TMA queue the weights
       // occupy, so they land about one memory latency after the wait.
-      if constexpr (kSh) {
+      if constexpr (kActBulk) {
+        if (tid == 0 && nqc > 0) {
+          mbar_arrive_expect_tx(&bars[kBarX], static_cast<uint32_t>(ndl * sizeof(T)));
+          bulk_g2s(x_sm, static_cast<const T*>(s_x) + static_cast<int64_t>(r0) * s_ldx + q0 * KW,
+                   static_cast<uint32_t>(ndl * sizeof(T)), &bars[kBarX]);
+        }
+        if (tid == 32 && ncv > 0) {
+          mbar_arrive_expect_tx(&bars[kBarY], static_cast<uint32_t>(ncv * 16));
+          bulk_g2s(y_sm, static_cast<const T*>(s_y) + static_cast<int64_t>(r0) * s_ldy + cv0 * 8,
+                   static_cast<uint32_t>(ncv * 16), &bars[kBarY]);
+        }
+      } else if constexpr (kSh) {
         const int nv = ndl / 8;  // 16-byte vectors per x row slice
         for (int i = tid; i < rows * nv; i += kThreads) {
           const int m = MT == 1 ? 0 : i / nv, c = i - m * nv;
@@ -497,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
         }
       }
       cp_async_commit();
-      if constexpr (kEx) {
+      if constexpr (kEx && !kActBulk) {
         for (int i = tid; i < rows * ncv; i += kThreads) {
           const int m = MT == 1 ? 0 : i / ncv, c = i - m * ncv;
           cp_async16(y_sm + m * ncv + c,
@@ -515,8 +534,12 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
       if constexpr (MODE == kExpand) {
         for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
       } else {
-        cp_async_wait<1>();  // this thread's x vectors
-        __syncthreads();     // everyone's
+        if constexpr (kActBulk) {
+          if (nqc > 0) mbar_wait(&bars[kBarX], phase);
+        } else {
+          cp_async_wait<1>();  // this thread's x vectors
+          __syncthreads();     // everyone's
+        }
         LSG_TRACE(4);
         if (first) cluster_wait();  // every peer's barriers are initialised
         first = false;
@@ -690,10 +713,11 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
 
       if constexpr (kEx) {
         LSG_TRACE(8);
-        cp_async_wait<0>();  // this thread's y vectors
+        if constexpr (!kActBulk) cp_async_wait<0>();  // this thread's y vectors
         __syncthreads();     // V_sm and every y vector visible
         // ---- expand: y[m, n] += sum_k v[m, k] B[k, n] ---------------------------
         if (ncv > 0) {
+          if constexpr (kActBulk) mbar_wait(&bars[kBarY], phase);
           mbar_wait(&bars[kBarB], wphase);
           LSG_TRACE(10);
           if constexpr (MT > 1) {
