@@ -142,3 +142,32 @@ def test_tp_column_ranges():
     assert tpmod.column_range(8192, 8, 3) == (3072, 4096)
     with pytest.raises(ValueError):
         tpmod.column_range(100, 8, 0)
+
+
+def test_plan_more_ranks_than_rows_and_empty_segments():
+    # 3 rows over 8 ranks: every row placed once, idle ranks get nothing
+    plan = part.partition_segments(np.array([0, 1, 3], dtype=np.int32), 64, 64, 8, 8)
+    rows = sorted(r for _, _, r0, r1 in plan for r in range(r0, r1))
+    assert rows == [0, 1, 2]
+    # empty segments are skipped; an all-empty batch gives an empty plan
+    plan = part.partition_segments(np.array([0, 0, 2, 2, 5], dtype=np.int32), 64, 64, 8, 2)
+    assert {p[1] for p in plan} == {1, 3}  # (segment 3 may be split across the two ranks)
+    assert part.partition_segments(np.array([0, 0, 0], dtype=np.int32), 64, 64, 8, 2) == []
+    rbs = part.rank_batches(np.array([0, 0, 0], dtype=np.int32), 64, 64, 8, 2)
+    assert all(rb.num_rows == 0 and rb.seg_starts.tolist() == [0] for rb in rbs)
+
+
+def test_adapter_pool_layer_view_pointer_table_cpu():
+    """layer_view(l) is a one-layer pool over the same storage: slot s's base pointer is
+    slot s's layer-l block of the parent (checked on CPU tensors; no kernel runs)."""
+    from paper_2310_18547_b200.sgmv import AdapterPool
+    pool = AdapterPool(3, 5, 64, 32, 8, torch.float16, device="cpu")
+    v = pool.layer_view(2)
+    es = 2
+    for s in range(3):
+        assert int(v.a_ptrs[s]) == pool.a[s, 2].data_ptr()
+        assert int(v.b_ptrs[s]) == pool.b[s, 2].data_ptr()
+        assert int(v.a_ptrs[s]) - int(pool.a_ptrs[s]) == 2 * 64 * 8 * es
+    assert v.num_layers == 1 and v.table.num_layers == 1 and v.table.num_slots == 3
+    with pytest.raises(ValueError):
+        pool.layer_view(5)
