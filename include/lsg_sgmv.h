@@ -34,10 +34,16 @@
  *   * Every call is asynchronous on `stream`, allocates nothing, never
  *     synchronises the host, and is deterministic: each output element is
  *     produced by a fixed-order fp32 reduction that does not depend on the batch
- *     composition, the segment order, or the launch configuration (so a row's
- *     result is bitwise identical whether it is computed by lsg_sgmv, by
- *     lsg_sgmv_shrink + lsg_sgmv_expand, or by lsg_bgmv, and on any GPU of a
- *     request-partitioned job).
+ *     composition, the segment order, or the launch configuration.  Rows of
+ *     segments shorter than the tensor-core threshold (LSG_OPT_TC_MIN_ROWS,
+ *     default 128) take the CUDA-core kernels, whose arithmetic is canonical: such
+ *     a row's result is bitwise identical whether it is computed by lsg_sgmv, by
+ *     lsg_sgmv_shrink + lsg_sgmv_expand, by lsg_bgmv or lsg_sgmv_multi, and on any
+ *     GPU of a request-partitioned job.  Rows of longer segments take the tensor-
+ *     core kernels (a different, equally deterministic summation): they are
+ *     run-to-run identical and agree with the CUDA-core result within the stated
+ *     tolerance, not bitwise.  A partition that cuts a long segment into pieces
+ *     below the threshold therefore changes those rows within tolerance only.
  *   * Programmatic dependent launch (opt-in, lsg_set_option(LSG_OPT_PDL, 1)):
  *     a launch may then start while the preceding kernel on the stream is still
  *     running; it reads the segment metadata, the weight table and streams the
@@ -110,6 +116,24 @@ int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weig
                 int32_t total_rows, int32_t layer, void* workspace, size_t workspace_bytes,
                 lsg_stream_t stream);
 
+/* Per-call options.  Each field overrides the process default set with
+ * lsg_set_option for this call only (-1 = use the process default).  A call
+ * takes one snapshot of its options at entry, so concurrent callers with
+ * different options (e.g. a decode-only step next to a prefill step on another
+ * stream) never see each other's settings. */
+typedef struct lsg_call_opts {
+  int32_t pdl;             /* programmatic dependent launch: 0 off, 1 on */
+  int32_t tc_min_rows;     /* rows from which a segment takes the tensor-core path (0 = 128) */
+  int32_t no_tensor_cores; /* 1: long segments stay on the CUDA-core kernel */
+} lsg_call_opts;
+
+/* lsg_sgmv with per-call options and an optional caller workspace (NULL: the
+ * library's per-device workspace, as lsg_sgmv). */
+int lsg_sgmv_ex(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                int32_t layer, void* workspace, size_t workspace_bytes, const lsg_call_opts* opts,
+                lsg_stream_t stream);
+
 /* Grouped fused call: up to 8 LoRA sites that share one segment plan (e.g. the
  * q / k / v projections of a layer: same requests, same adapters, each site with
  * its own pool, x and y) in ONE launch -- one cluster per (site, row), so the
@@ -127,6 +151,9 @@ typedef struct lsg_sgmv_site {
 int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
                    const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
                    lsg_stream_t stream);
+int lsg_sgmv_multi_ex(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
+                      const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
+                      const lsg_call_opts* opts, lsg_stream_t stream);
 
 /* Dense projection with the LoRA add in the GEMM epilogue (decode shapes):
  *   y[s_n, h_out] = x[s_n, h_in] . W[h_in, h_out] + x . A_slot(s) . B_slot(s)   (overwrite)
@@ -158,13 +185,17 @@ int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
              const int32_t* row_slot, int32_t total_rows, int32_t layer, lsg_stream_t stream);
 
 /* On-device segment builder (replaces the CPU grouping of plan_batch,
- * simulator.cpp:267-309, and the per-row gather loop, sgmv.cpp:195-203).
+ * simulator.cpp:239-311, and the per-row gather loop, sgmv.cpp:195-203).
  * Input (device): row_slot[s_n], the pool slot of every token row (negative or
- * >= num_slots = no adapter).  Output (device): a STABLE grouping of the rows --
- * rows of one slot keep their original order; groups in ascending slot order,
- * except that lead_slot (>= 0; the slot of the step's prefill request, or -1)
- * is placed first, and the no-adapter rows form a final group with slot -1.
- * This is plan_batch's order whenever slots are assigned in ascending LoraId.
+ * >= num_slots = no adapter), rows in request order.  Output (device): a STABLE
+ * grouping of the rows -- rows of one slot keep their original order; groups in
+ * ascending slot order, except that lead_slot (>= 0; the slot of the step's
+ * prefill request, or -1) is placed first, with the prefill request's own rows
+ * [lead_row0, lead_row1) ahead of the other lead_slot rows (pass an empty range
+ * when there is no prefill); the no-adapter rows form a final group with slot -1.
+ * This is plan_batch's row order (prefill prompt rows, then the same-adapter
+ * decodes, then the other adapters' decodes in ascending LoraId, request order
+ * within) whenever slots are assigned in ascending LoraId.
  *   row_perm[s_n]          gathered row -> original row
  *   seg_starts[s_n + 1]    n+1 boundaries, then padded with s_n
  *   seg_slot[s_n]          n slots, then padded with -1
@@ -174,7 +205,7 @@ int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
  * reading n back.  One CTA; total_rows <= 16384. */
 size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots);
 int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_slots,
-                       int32_t lead_slot, int32_t* row_perm, int32_t* seg_starts,
+                       int32_t lead_slot, int32_t lead_row0, int32_t lead_row1, int32_t* row_perm, int32_t* seg_starts,
                        int32_t* seg_slot, int32_t* num_segments, void* workspace,
                        size_t workspace_bytes, lsg_stream_t stream);
 
@@ -188,22 +219,26 @@ int lsg_scatter_rows(void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
  * Replaces, for one decode step, the reference's request-level placement of
  * requests onto GPUs (core/src/scheduler.cpp:12-29): rows are independent
  * (sgmv.cpp:108-116, 125-134), so a batch shards with no collective.  Whole
- * segments are placed (one adapter's weights read once); a segment larger than
- * the per-rank byte share is cut into row ranges.  Pieces are assigned by LPT
- * greedy on the algorithmic bytes rows*(h_in+h_out)*e + (h_in+h_out)*rank*e
- * (cost_model.cpp:13-19, :59), largest first onto the least-loaded rank.
- * Output: *num_pieces pieces ordered by (rank, segment, row); each rank's pieces
- * are its local batch.  If max_pieces is too small, returns LSG_EINVAL with
- * *num_pieces = the count needed (at most num_segments + world). */
+ * segments are placed (one adapter's weights read once).  seg_owner (host, n;
+ * NULL = every adapter replicated on every rank) routes a segment whose adapter
+ * lives on one rank only (slot-sharded pool, seg_owner[s] >= 0) to that rank,
+ * whole -- Scheduler::place's adapter-affinity rule.  Replicated segments may be
+ * cut into row ranges when that lowers the largest rank load (each range pays
+ * the adapter's weights again).  Pieces are assigned by LPT greedy on the
+ * algorithmic bytes rows*(h_in+h_out)*e + (h_in+h_out)*rank*e (cost_model.cpp:13-19,
+ * :59), largest first onto the least-loaded rank.  Output: *num_pieces pieces
+ * ordered by (rank, segment, row); each rank's pieces are its local batch.  There
+ * are at most (non-empty segments) + world - 1 pieces; if max_pieces is too
+ * small, returns LSG_EINVAL with *num_pieces = the count needed. */
 typedef struct lsg_piece {
   int32_t rank;    /* owning rank */
   int32_t seg;     /* segment index in the global batch */
   int32_t row0;    /* first global row */
   int32_t row1;    /* one past the last global row */
 } lsg_piece;
-int lsg_partition_segments(const int32_t* seg_starts /* host, n+1 */, int32_t num_segments, int32_t h_in,
-                           int32_t h_out, int32_t rank, int32_t elem_bytes, int32_t world, int32_t max_pieces,
-                           lsg_piece* pieces, int32_t* num_pieces);
+int lsg_partition_segments(const int32_t* seg_starts /* host, n+1 */, const int32_t* seg_owner /* host, n or NULL */,
+                           int32_t num_segments, int32_t h_in, int32_t h_out, int32_t rank, int32_t elem_bytes,
+                           int32_t world, int32_t max_pieces, lsg_piece* pieces, int32_t* num_pieces);
 
 /* Tuning / test hooks. */
 typedef enum {

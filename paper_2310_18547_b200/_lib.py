@@ -10,8 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-# LSG_LIB_OVERRIDE: load an experimental build of the same library (scripts/build_variant.sh)
-LIB_PATH = os.environ.get("LSG_LIB_OVERRIDE") or os.path.join(PKG, "lib", "libsgmv_b200.so")
+LIB_PATH = os.path.join(PKG, "lib", "libsgmv_b200.so")
 
 LSG_OK, LSG_EINVAL, LSG_EUNSUPPORTED, LSG_ECUDA, LSG_ENODEVICE = 0, -1, -2, -3, -4
 LSG_F16, LSG_BF16 = 0, 1
@@ -26,7 +25,7 @@ EXPORTED = (
     "lsg_build_segments_workspace", "lsg_build_segments", "lsg_gather_rows", "lsg_scatter_rows",
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
     "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments", "lsg_sgmv_multi",
-    "lsg_dense_lora", "lsg_dense_lora_workspace_size",
+    "lsg_dense_lora", "lsg_dense_lora_workspace_size", "lsg_sgmv_ex", "lsg_sgmv_multi_ex",
 )
 
 
@@ -58,6 +57,12 @@ class Site(C.Structure):
                 ("tbl", C.POINTER(WeightTable))]
 
 
+class CallOpts(C.Structure):
+    """Mirror of ``lsg_call_opts`` (-1 = process default)."""
+
+    _fields_ = [("pdl", C.c_int32), ("tc_min_rows", C.c_int32), ("no_tensor_cores", C.c_int32)]
+
+
 class Piece(C.Structure):
     """Mirror of ``lsg_piece``."""
 
@@ -86,6 +91,9 @@ def lib() -> C.CDLL:
         L.lsg_sgmv.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp]
         L.lsg_sgmv_ws.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
         L.lsg_sgmv_multi.argtypes = [C.POINTER(Site), i32, vp, vp, i32, i32, i32, vp]
+        L.lsg_sgmv_ex.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t,
+                                  C.POINTER(CallOpts), vp]
+        L.lsg_sgmv_multi_ex.argtypes = [C.POINTER(Site), i32, vp, vp, i32, i32, i32, C.POINTER(CallOpts), vp]
         L.lsg_dense_lora.argtypes = [vp, i64, vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, vp, C.c_size_t, vp]
         L.lsg_dense_lora_workspace_size.argtypes = [tp, i32]
         L.lsg_dense_lora_workspace_size.restype = C.c_size_t
@@ -96,7 +104,7 @@ def lib() -> C.CDLL:
         L.lsg_bgmv.argtypes = [vp, i64, vp, i64, tp, vp, i32, i32, vp]
         L.lsg_build_segments_workspace.argtypes = [i32, i32]
         L.lsg_build_segments_workspace.restype = C.c_size_t
-        L.lsg_build_segments.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.lsg_build_segments.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.lsg_gather_rows.argtypes = [vp, i64, vp, i64, vp, i32, i32, vp]
         L.lsg_scatter_rows.argtypes = [vp, i64, vp, i64, vp, i32, i32, vp]
         L.lsg_set_option.argtypes = [i32, i32]
@@ -107,7 +115,7 @@ def lib() -> C.CDLL:
         L.lsg_last_error.restype = C.c_char_p
         L.lsg_version.restype = C.c_int
         L.lsg_set_trace.argtypes = [vp, i32]
-        L.lsg_partition_segments.argtypes = [C.POINTER(i32), i32, i32, i32, i32, i32, i32, i32,
+        L.lsg_partition_segments.argtypes = [C.POINTER(i32), C.POINTER(i32), i32, i32, i32, i32, i32, i32, i32,
                                              C.POINTER(Piece), C.POINTER(i32)]
         _lib = L
     return _lib

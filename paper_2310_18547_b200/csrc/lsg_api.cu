@@ -39,6 +39,13 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 namespace {
 
+constexpr int kMaxGridY = 65535;  // gridDim.y limit
+
+// Process-wide defaults (lsg_set_option).  A call never reads these directly:
+// it takes one snapshot at entry (Opts, overridden field by field by the
+// caller's lsg_call_opts) and every planning / launch decision of that call reads
+// the snapshot, so concurrent calls with different per-call options and a
+// concurrent lsg_set_option cannot interleave inside one call.
 std::atomic<int> g_opt_pdl{0};
 std::atomic<int> g_opt_force_cluster{0};
 std::atomic<int> g_opt_force_generic{0};
@@ -49,6 +56,37 @@ std::atomic<int> g_opt_no_tc{0};
 std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
 std::atomic<int> g_opt_no_rank64_tiles{0};
+std::atomic<int> g_opt_tc_min_rows{0};  // rows from which a segment takes the tensor-core path (0 = default)
+
+struct Opts {
+  int pdl, force_cluster, force_generic, force_tile_rows, no_alias, no_tile_scan, no_tc, tc_split, no_row_mode,
+      no_rank64_tiles, tc_min_rows;
+};
+
+Opts snapshot(const lsg_call_opts* c) {
+  Opts o{g_opt_pdl.load(),     g_opt_force_cluster.load(), g_opt_force_generic.load(), g_opt_force_tile_rows.load(),
+         g_opt_no_alias.load(), g_opt_no_tile_scan.load(), g_opt_no_tc.load(),        g_opt_tc_split.load(),
+         g_opt_no_row_mode.load(), g_opt_no_rank64_tiles.load(), g_opt_tc_min_rows.load()};
+  if (c != nullptr) {
+    if (c->pdl >= 0) o.pdl = c->pdl ? 1 : 0;
+    if (c->tc_min_rows >= 0) o.tc_min_rows = c->tc_min_rows;
+    if (c->no_tensor_cores >= 0) o.no_tc = c->no_tensor_cores ? 1 : 0;
+  }
+  return o;
+}
+
+// The snapshot of the call running on this thread (set by CallScope for the
+// duration of one C-ABI call; the process defaults outside any call).
+thread_local const Opts* t_opts = nullptr;
+struct CallScope {
+  Opts o;
+  const Opts* prev;
+  explicit CallScope(const lsg_call_opts* c) : o(snapshot(c)), prev(t_opts) { t_opts = &o; }
+  ~CallScope() { t_opts = prev; }
+  CallScope(const CallScope&) = delete;
+  CallScope& operator=(const CallScope&) = delete;
+};
+Opts cur() { return t_opts ? *t_opts : snapshot(nullptr); }
 
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -95,25 +133,29 @@ int tc_tile_bound(int s_n, int n_seg) {
 }
 
 // Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default).
-std::atomic<int> g_opt_tc_min_rows{0};
 int tc_min_rows() {
-  const int x = g_opt_tc_min_rows.load();
+  const int x = cur().tc_min_rows;
   return x > 0 ? x : kTcMinRows;
 }
 
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
-  if (tc_fused_c(t, nullptr) > 0 && !g_opt_tc_split.load()) return 0;  // the fused kernel keeps v on chip
+  if (tc_fused_c(t, nullptr) > 0 && !cur().tc_split) return 0;  // the fused kernel keeps v on chip
   return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
-// Library-owned workspace of lsg_sgmv(): grown (never during stream capture)
+// Library-owned workspace of lsg_sgmv(), one per device (a process may drive
+// several GPUs): grown, never during stream capture.  The caller's current device
+// is the device of the launch, so the buffer is allocated and freed there.
+constexpr int kMaxDevices = 64;
 std::mutex g_ws_mu;
-void* g_ws = nullptr;
-size_t g_ws_bytes = 0;
+void* g_ws[kMaxDevices] = {};
+size_t g_ws_bytes[kMaxDevices] = {};
 
 void* library_workspace(size_t need, cudaStream_t cs) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (g_ws_bytes >= need) return g_ws;
+  if (g_ws_bytes[dev] >= need) return g_ws[dev];
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(cs, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return nullptr;
   size_t bytes = std::max<size_t>(need, static_cast<size_t>(1) << 20);
@@ -122,13 +164,13 @@ void* library_workspace(size_t need, cudaStream_t cs) {
     cudaGetLastError();
     return nullptr;
   }
-  if (g_ws != nullptr) {
-    cudaDeviceSynchronize();  // the old buffer may still be read by queued launches
-    cudaFree(g_ws);
+  if (g_ws[dev] != nullptr) {
+    cudaDeviceSynchronize();  // this device: the old buffer may still be read by queued launches
+    cudaFree(g_ws[dev]);
   }
-  g_ws = p;
-  g_ws_bytes = bytes;
-  return g_ws;
+  g_ws[dev] = p;
+  g_ws_bytes[dev] = bytes;
+  return p;
 }
 
 bool encode_rows_map(CUtensorMap* m, int dtype, const void* base, int cols, int rows, int64_t ld) {
@@ -174,10 +216,10 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
   const int nq = tc_nq(tbl);
-  if (nq == 0 || s_n < tc_min_rows()) return false;
+  if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
   int compact = 0;
-  const int fc = g_opt_tc_split.load() ? 0 : tc_fused_c(tbl, &compact);
+  const int fc = cur().tc_split ? 0 : tc_fused_c(tbl, &compact);
   if (fc > 0) {
     TcFusedParams& fp = lp.fp;
     fp = TcFusedParams{};
@@ -293,25 +335,25 @@ bool fast_shape_ok(const lsg_weight_table* t) {
 Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast, bool long_on_tc = false) {
   Plan pl;
   pl.mode = kernel == kKShrink ? kShrink : kernel == kKExpand ? kExpand : kFused;
-  if (!fast || g_opt_force_generic.load()) {
+  if (!fast || cur().force_generic) {
     pl.path = 1;
     pl.clusters = s_n;
     pl.smem = t->rank * 4;
     return pl;
   }
-  const int forced_mt = g_opt_force_tile_rows.load();
+  const int forced_mt = cur().force_tile_rows;
   if (kernel == kKBgmv)
     pl.mt = 1;
   else if (forced_mt == 1 || forced_mt == 8)
     pl.mt = forced_mt;
-  else if (t->rank == 64 && s_n > n_seg && !g_opt_no_rank64_tiles.load())
+  else if (t->rank == 64 && s_n > n_seg && !cur().no_rank64_tiles)
     pl.mt = kernel == kKFused ? 4 : 8;  // rank 64, shared adapters: one weight read per tile (c3: 4 rows, C = 4)
   else
     pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
   if (kernel == kKBgmv) {
     pl.row_splits = 1;
     pl.clusters = s_n;
-  } else if ((pl.mt > 1 || s_n > n_seg) && !(g_opt_no_tile_scan.load())) {
+  } else if ((pl.mt > 1 || s_n > n_seg) && !(cur().no_tile_scan)) {
     // one cluster per row tile, mapped on the device; sum_i ceil(len_i/MT) is
     // at most (s_n + n_seg*(MT-1))/MT, and never more than s_n
     pl.tile_scan = 1;
@@ -337,7 +379,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     return static_cast<int>(make_layout(pl.mode, t->rank, pl.mt, c, nq, nqc, ncv, red_all_for(c), alias).total);
   };
   auto alias_for = [&](int c) {
-    const int o = g_opt_no_alias.load();  // 1: never, -1: always (single-tile launches), 0: when co-residency needs it
+    const int o = cur().no_alias;  // 1: never, -1: always (single-tile launches), 0: when co-residency needs it
     if (pl.mode != kFused || !single_tile || o > 0) return 0;
     return o < 0 || smem_alias(c, 0) > kCoresidentSmem ? 1 : 0;
   };
@@ -370,7 +412,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   for (int cand = c_cap + 1; c == 0 && cand <= kMaxCluster; ++cand)
     if ((span % cand == 0 || cand == kMaxCluster) && smem_for(cand) <= kSmemBudget) c = cand;
   if (c == 0) c = kMaxCluster;
-  const int forced = g_opt_force_cluster.load();
+  const int forced = cur().force_cluster;
   if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
   pl.red_all = red_all_for(c);
   pl.alias_ab = alias_for(c);
@@ -441,7 +483,7 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   // expand may stage y_old before waiting for v.
   int skip_long = 0;
   LongPlan lp;
-  if (kernel == kKFused && !g_opt_no_tc.load() && s_n >= tc_min_rows() && tc_nq(tbl) > 0) {
+  if (kernel == kKFused && !cur().no_tc && s_n >= tc_min_rows() && tc_nq(tbl) > 0) {
     if (library_ws) {
       ws_bytes = tc_workspace_bytes(tbl, s_n);
       ws = library_workspace(ws_bytes, cs);
@@ -451,15 +493,28 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   }
   Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
   // One-row tiles without a long-segment split: one cluster per row, exact grid.
-  if (pl.mt == 1 && kernel != kKBgmv && !skip_long && !g_opt_no_row_mode.load()) {
+  if (pl.mt == 1 && kernel != kKBgmv && !skip_long && !cur().no_row_mode && s_n <= kMaxGridY) {
     pl.row_mode = 1;
     pl.tile_scan = 0;
     pl.row_splits = 1;
     pl.clusters = s_n;
   }
-  if (n_sites > 1) {  // grouped launch (lsg_sgmv_multi checked eligibility): one cluster per (site, row)
+  if (n_sites > 1) {  // grouped launch: one cluster per (site, row)
+    // lsg_sgmv_multi checks eligibility; the grouped item mode exists for one-row
+    // row-mode launches only, so anything else is refused here, never run partially
+    if (!pl.row_mode || pl.mt != 1 || skip_long || static_cast<int64_t>(n_sites) * s_n > kMaxGridY)
+      return fail(LSG_EINVAL, "lsg_sgmv_multi: grouped launch needs one-row row-mode tiles");
     pl.multi = 1;
     pl.clusters = n_sites * s_n;
+  }
+  // Launches with one work item per cluster put the item count in gridDim.y (max
+  // 65535): above that, clusters loop over tiles (tile-scan decode) instead.
+  if (!pl.tile_scan && !pl.multi && kernel != kKBgmv && pl.clusters > kMaxGridY) {
+    pl.row_mode = 0;
+    pl.tile_scan = 1;
+    pl.row_splits = 1;
+    const int64_t bound = (static_cast<int64_t>(s_n) + static_cast<int64_t>(n_seg) * (pl.mt - 1)) / pl.mt;
+    pl.clusters = static_cast<int>(std::min<int64_t>(bound, s_n));  // capped at launch (launch_fast_inst)
   }
   // With the long segments on the tensor cores, the short ones have at most n_seg
   // segments' worth of work items in practice: size the tile-scan grid by that
@@ -500,11 +555,14 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   for (int i = 0; i < p.n_sites; ++i)
     p.sites[i] = SiteParams{sites[i].y, sites[i].x, sites[i].tbl->a_ptr, sites[i].tbl->b_ptr, sites[i].ldx,
                             sites[i].ldy};
+#ifdef LSG_INSTRUMENT
+  // experiment switches (instrumented builds only; production kernels compile them out)
   static const int exp_flags = [] {
     const char* e = std::getenv("LSG_EXP");
     return e ? std::atoi(e) : 0;
   }();
   p.exp_flags = exp_flags;
+#endif
   if (skip_long) {
     st = launch_long_segments(lp, tbl->dtype, tbl->rank, cs);
     if (st != LSG_OK) return st;
@@ -519,7 +577,7 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
 
 }  // namespace
 
-bool pdl_enabled() { return g_opt_pdl.load() != 0; }
+bool pdl_enabled() { return cur().pdl != 0; }
 
 
 int launch_generic(int dtype, int mode, const GenericParams& g, int rows, int smem, cudaStream_t st) {
@@ -536,11 +594,13 @@ extern "C" {
 int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
              const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
              int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  CallScope scope(nullptr);
   return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
              num_segments, total_rows, layer, stream, nullptr, 0, true);
 }
 
 size_t lsg_sgmv_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
+  CallScope scope(nullptr);
   if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
   return tc_workspace_bytes(tbl, total_rows);
 }
@@ -549,13 +609,24 @@ int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weig
                 const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
                 int32_t total_rows, int32_t layer, void* workspace, size_t workspace_bytes,
                 lsg_stream_t stream) {
+  CallScope scope(nullptr);
   return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr,
              num_segments, total_rows, layer, stream, workspace, workspace_bytes, false);
 }
 
-int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
-                   const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
-                   lsg_stream_t stream) {
+int lsg_sgmv_ex(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                int32_t layer, void* workspace, size_t workspace_bytes, const lsg_call_opts* opts,
+                lsg_stream_t stream) {
+  CallScope scope(opts);
+  return run(kKFused, y, ldy, x, ldx, nullptr, nullptr, tbl, seg_starts, seg_slot, nullptr, num_segments,
+             total_rows, layer, stream, workspace, workspace_bytes, workspace == nullptr);
+}
+
+int lsg_sgmv_multi_ex(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
+                      const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
+                      const lsg_call_opts* opts, lsg_stream_t stream) {
+  CallScope scope(opts);
   if (sites == nullptr || num_sites < 1 || num_sites > kMaxSites)
     return fail(LSG_EINVAL, "lsg_sgmv_multi: need 1..8 sites");
   const lsg_weight_table* t0 = sites[0].tbl;
@@ -570,9 +641,13 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
   }
   // One grouped launch when every site takes the one-row fast path without long
   // segments; otherwise the sites run one after another (same results).
+  // (make_plan decides the tile rows: rank 64 with shared adapters plans 4-row tiles,
+  // which the grouped item mode does not have)
   bool grouped = num_sites > 1 && total_rows > 0 && num_segments > 0 && fast_shape_ok(t0) &&
-                 !g_opt_force_generic.load() && !g_opt_no_row_mode.load() && g_opt_force_tile_rows.load() != 8 &&
-                 (g_opt_no_tc.load() || total_rows < tc_min_rows() || tc_nq(t0) == 0);
+                 !cur().force_generic && !cur().no_row_mode &&
+                 static_cast<int64_t>(num_sites) * total_rows <= kMaxGridY &&
+                 make_plan(t0, kKFused, num_segments, total_rows, true).mt == 1 &&
+                 (cur().no_tc || total_rows < tc_min_rows() || tc_nq(t0) == 0);
   for (int i = 0; grouped && i < num_sites; ++i)
     grouped = sites[i].x != nullptr && sites[i].y != nullptr && aligned16(sites[i].x) && aligned16(sites[i].y) &&
               sites[i].ldx % 8 == 0 && sites[i].ldy % 8 == 0 && sites[i].ldx >= t0->h_in &&
@@ -589,7 +664,14 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
              seg_slot, nullptr, num_segments, total_rows, layer, stream, nullptr, 0, true, sites, num_sites);
 }
 
+int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t* seg_starts,
+                   const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
+                   lsg_stream_t stream) {
+  return lsg_sgmv_multi_ex(sites, num_sites, seg_starts, seg_slot, num_segments, total_rows, layer, nullptr, stream);
+}
+
 size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
+  CallScope scope(nullptr);
   if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
   return static_cast<size_t>(total_rows) * tbl->rank * sizeof(float);
 }
@@ -598,6 +680,7 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
                    const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
                    int32_t num_segments, int32_t total_rows, int32_t layer, void* workspace,
                    size_t workspace_bytes, lsg_stream_t stream) {
+  CallScope scope(nullptr);
   int st = validate_table(tbl);
   if (st != LSG_OK) return st;
   if (total_rows < 0 || num_segments < 0) return fail(LSG_EINVAL, "lsg_dense_lora: negative sizes");
@@ -649,6 +732,7 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
 int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table* tbl,
                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
                     int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  CallScope scope(nullptr);
   return run(kKShrink, nullptr, 0, x, ldx, v, nullptr, tbl, seg_starts, seg_slot, nullptr,
              num_segments, total_rows, layer, stream);
 }
@@ -656,14 +740,24 @@ int lsg_sgmv_shrink(float* v, const void* x, int64_t ldx, const lsg_weight_table
 int lsg_sgmv_expand(void* y, int64_t ldy, const float* v, const lsg_weight_table* tbl,
                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments,
                     int32_t total_rows, int32_t layer, lsg_stream_t stream) {
+  CallScope scope(nullptr);
   return run(kKExpand, y, ldy, nullptr, 0, nullptr, v, tbl, seg_starts, seg_slot, nullptr,
              num_segments, total_rows, layer, stream);
 }
 
 int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
              const int32_t* row_slot, int32_t total_rows, int32_t layer, lsg_stream_t stream) {
-  return run(kKBgmv, y, ldy, x, ldx, nullptr, nullptr, tbl, nullptr, nullptr, row_slot, 0,
-             total_rows, layer, stream);
+  CallScope scope(nullptr);
+  // One cluster per row with the row in gridDim.y (<= 65535): longer batches run as
+  // consecutive launches over row ranges (rows are independent).
+  for (int32_t r0 = 0; r0 < total_rows || r0 == 0; r0 += kMaxGridY) {
+    const int32_t n = std::min<int32_t>(kMaxGridY, total_rows - r0);
+    const int st = run(kKBgmv, y ? static_cast<char*>(y) + static_cast<int64_t>(r0) * ldy * 2 : nullptr, ldy,
+                       x ? static_cast<const char*>(x) + static_cast<int64_t>(r0) * ldx * 2 : nullptr, ldx, nullptr,
+                       nullptr, tbl, nullptr, nullptr, row_slot ? row_slot + r0 : nullptr, 0, n, layer, stream);
+    if (st != LSG_OK || total_rows <= kMaxGridY) return st;
+  }
+  return LSG_OK;
 }
 
 int lsg_set_option(int32_t option, int32_t value) {
@@ -693,15 +787,15 @@ int lsg_set_option(int32_t option, int32_t value) {
 
 int lsg_get_option(int32_t option) {
   switch (option) {
-    case LSG_OPT_PDL: return g_opt_pdl.load();
-    case LSG_OPT_FORCE_CLUSTER: return g_opt_force_cluster.load();
-    case LSG_OPT_FORCE_GENERIC: return g_opt_force_generic.load();
-    case LSG_OPT_FORCE_TILE_ROWS: return g_opt_force_tile_rows.load();
-    case LSG_OPT_NO_L2_STAGING: return g_opt_no_alias.load();
-    case LSG_OPT_NO_TENSOR_CORES: return g_opt_no_tc.load();
-    case LSG_OPT_TC_SPLIT: return g_opt_tc_split.load();
-    case LSG_OPT_NO_ROW_MODE: return g_opt_no_row_mode.load();
-    case LSG_OPT_NO_MULTIROW_TILES: return g_opt_no_rank64_tiles.load();
+    case LSG_OPT_PDL: return cur().pdl;
+    case LSG_OPT_FORCE_CLUSTER: return cur().force_cluster;
+    case LSG_OPT_FORCE_GENERIC: return cur().force_generic;
+    case LSG_OPT_FORCE_TILE_ROWS: return cur().force_tile_rows;
+    case LSG_OPT_NO_L2_STAGING: return cur().no_alias;
+    case LSG_OPT_NO_TENSOR_CORES: return cur().no_tc;
+    case LSG_OPT_TC_SPLIT: return cur().tc_split;
+    case LSG_OPT_NO_ROW_MODE: return cur().no_row_mode;
+    case LSG_OPT_NO_MULTIROW_TILES: return cur().no_rank64_tiles;
     case LSG_OPT_TC_MIN_ROWS: return g_opt_tc_min_rows.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
@@ -709,6 +803,7 @@ int lsg_get_option(int32_t option) {
 
 int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t total_rows,
                      int32_t kernel, lsg_launch_info* info) {
+  CallScope scope(nullptr);
   int st = validate_table(tbl);
   if (st != LSG_OK) return st;
   if (info == nullptr || kernel < 0 || kernel > 3) return fail(LSG_EINVAL, "lsg_query_launch: bad arguments");
@@ -733,13 +828,16 @@ size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots) {
 }
 
 int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_slots,
-                       int32_t lead_slot, int32_t* row_perm, int32_t* seg_starts,
+                       int32_t lead_slot, int32_t lead_row0, int32_t lead_row1, int32_t* row_perm, int32_t* seg_starts,
                        int32_t* seg_slot, int32_t* num_segments, void* workspace,
                        size_t workspace_bytes, lsg_stream_t stream) {
+  CallScope scope(nullptr);
   (void)workspace;
   (void)workspace_bytes;
   if (total_rows < 0 || num_slots < 0) return fail(LSG_EINVAL, "lsg_build_segments: negative sizes");
   if (total_rows > kBuilderMaxRows) return fail(LSG_EUNSUPPORTED, "lsg_build_segments: total_rows > 16384");
+  if (lead_row0 < 0 || lead_row1 < lead_row0 || lead_row1 > total_rows)
+    return fail(LSG_EINVAL, "lsg_build_segments: lead row range outside [0, total_rows]");
   if (seg_starts == nullptr || num_segments == nullptr || (total_rows > 0 && (row_slot == nullptr ||
       row_perm == nullptr || seg_slot == nullptr)))
     return fail(LSG_EINVAL, "lsg_build_segments: NULL output");
@@ -768,9 +866,9 @@ int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_
   attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &attr;
-  cfg.numAttrs = g_opt_pdl.load() ? 1 : 0;
+  cfg.numAttrs = cur().pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, build_segments_kernel, row_slot, total_rows, num_slots, lead_slot,
-                                     n_pow2, row_perm, seg_starts, seg_slot, num_segments);
+                                     lead_row0, lead_row1, n_pow2, row_perm, seg_starts, seg_slot, num_segments);
   return e == cudaSuccess ? LSG_OK : cuda_fail(e, "build_segments_kernel launch");
 }
 

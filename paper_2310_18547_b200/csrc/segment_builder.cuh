@@ -20,23 +20,33 @@ constexpr int kBuilderMaxRows = 16384;
 
 __global__ void __launch_bounds__(kBuilderThreads, 1)
     build_segments_kernel(const int32_t* __restrict__ row_slot, int32_t s_n, int32_t num_slots,
-                          int32_t lead_slot, int32_t n_pow2, int32_t* __restrict__ row_perm,
+                          int32_t lead_slot, int32_t lead_row0, int32_t lead_row1, int32_t n_pow2,
+                          int32_t* __restrict__ row_perm,
                           int32_t* __restrict__ seg_starts, int32_t* __restrict__ seg_slot,
                           int32_t* __restrict__ num_segments) {
   extern __shared__ uint64_t keys[];  // n_pow2 entries
   __shared__ int32_t warp_tot[kBuilderThreads / 32];
   const int tid = threadIdx.x;
   pdl_wait();
-  // group key: lead slot -> 0, slot s -> s + 1, no adapter -> 0x7fffffff (last)
+  // group key: lead slot -> 0, slot s -> s + 1, no adapter -> 0x7fffffff (last).
+  // Within the lead group the prefill request's rows [lead_row0, lead_row1) come
+  // first (sub-key 0), then the same-adapter decode rows (sub-key 1): plan_batch
+  // pushes the prefill's prompt rows before the merged decode group
+  // (simulator.cpp:296-309).  Key = group << 32 | sub << 31 | row (row < 2^31).
   for (int i = tid; i < n_pow2; i += kBuilderThreads) {
     uint64_t k = ~0ull;
     if (i < s_n) {
       const int s = row_slot[i];
-      uint32_t g;
-      if (s < 0 || s >= num_slots) g = 0x7fffffffu;
-      else if (s == lead_slot) g = 0u;
-      else g = static_cast<uint32_t>(s) + 1u;
-      k = (static_cast<uint64_t>(g) << 32) | static_cast<uint32_t>(i);
+      uint32_t g, sub = 0;
+      if (s < 0 || s >= num_slots) {
+        g = 0x7fffffffu;
+      } else if (s == lead_slot) {
+        g = 0u;
+        sub = (i >= lead_row0 && i < lead_row1) ? 0u : 1u;
+      } else {
+        g = static_cast<uint32_t>(s) + 1u;
+      }
+      k = (static_cast<uint64_t>(g) << 32) | (static_cast<uint64_t>(sub) << 31) | static_cast<uint32_t>(i);
     }
     keys[i] = k;
   }
@@ -62,7 +72,7 @@ __global__ void __launch_bounds__(kBuilderThreads, 1)
   const int b0 = tid * E, b1 = min(s_n, b0 + E);
   int cnt = 0;
   for (int i = b0; i < b1; ++i) {
-    row_perm[i] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+    row_perm[i] = static_cast<int32_t>(keys[i] & 0x7fffffffu);
     cnt += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
   }
   const int lane = tid & 31, warp = tid >> 5;
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(kBuilderThreads, 1)
   for (int i = b0; i < b1; ++i) {
     if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) {
       seg_starts[seg] = i;
-      const int s = row_slot[keys[i] & 0xffffffffu];
+      const int s = row_slot[keys[i] & 0x7fffffffu];
       seg_slot[seg] = (s < 0 || s >= num_slots) ? -1 : s;
       ++seg;
     }

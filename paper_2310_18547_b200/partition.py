@@ -6,9 +6,12 @@ whole segments per rank, dominant segments cut into row ranges, LPT greedy on
 algorithmic bytes.  Every rank computes the same plan from the same segment
 boundaries, gathers its rows into a local batch, runs SGMV on its own GPU and
 (only if the caller needs the full output on one rank) the rows are reassembled
-by :func:`scatter_rows_back`.  Because each output row is a fixed function of its
-own row and adapter (the kernels' canonical arithmetic), partitioned outputs equal
-the single-GPU output bit for bit.
+by :func:`scatter_rows_back`.  Rows on the CUDA-core kernels (segments shorter than
+the tensor-core threshold, every decode row) are a fixed function of their own row
+and adapter (the kernels' canonical arithmetic), so partitioned outputs equal the
+single-GPU output bit for bit there; a long (prefill) segment cut into pieces may
+move between the tensor-core and CUDA-core kernels and then agrees within the
+stated tolerance (include/lsg_sgmv.h, Semantics).
 
 Reference analogue: request -> GPU placement, ``Scheduler::place``
 (core/src/scheduler.cpp:12-29); row independence, sgmv.cpp:108-116, 125-134.
@@ -37,23 +40,34 @@ class RankBatch:
         return int(self.rows.size)
 
 
-def partition_segments(seg_starts, h_in: int, h_out: int, rank: int, world: int, elem_bytes: int = 2):
-    """The plan as a list of (rank, seg, row0, row1) tuples, ordered by (rank, seg, row0)."""
+def partition_segments(seg_starts, h_in: int, h_out: int, rank: int, world: int, elem_bytes: int = 2,
+                       seg_owner=None):
+    """The plan as a list of (rank, seg, row0, row1) tuples, ordered by (rank, seg, row0).
+
+    ``seg_owner`` (optional, one int per segment): the rank holding that segment's
+    adapter in a slot-sharded pool (the segment is routed there, whole), or -1 for an
+    adapter replicated on every rank."""
     b = np.ascontiguousarray(np.asarray(seg_starts, dtype=np.int32))
     n_seg = int(b.size) - 1
     if n_seg < 0:
         raise ValueError("seg_starts needs at least one entry")
-    cap = n_seg + world
+    own = None
+    if seg_owner is not None:
+        own = np.ascontiguousarray(np.asarray(seg_owner, dtype=np.int32))
+        if own.size != n_seg:
+            raise ValueError("seg_owner needs one entry per segment")
+    cap = n_seg + world  # the planner's bound is (non-empty segments) + world - 1
     out = (_lib.Piece * max(cap, 1))()
     n = C.c_int32(0)
-    _lib.call("lsg_partition_segments", b.ctypes.data_as(C.POINTER(C.c_int32)), n_seg, h_in, h_out, rank,
+    _lib.call("lsg_partition_segments", b.ctypes.data_as(C.POINTER(C.c_int32)),
+              own.ctypes.data_as(C.POINTER(C.c_int32)) if own is not None else None, n_seg, h_in, h_out, rank,
               elem_bytes, world, cap, out, C.byref(n))
     return [(out[i].rank, out[i].seg, out[i].row0, out[i].row1) for i in range(n.value)]
 
 
-def rank_batches(seg_starts, h_in: int, h_out: int, rank: int, world: int, elem_bytes: int = 2):
+def rank_batches(seg_starts, h_in: int, h_out: int, rank: int, world: int, elem_bytes: int = 2, seg_owner=None):
     """Per-rank local batches (list of :class:`RankBatch`, index = rank)."""
-    plan = partition_segments(seg_starts, h_in, h_out, rank, world, elem_bytes)
+    plan = partition_segments(seg_starts, h_in, h_out, rank, world, elem_bytes, seg_owner)
     out = []
     for r in range(world):
         mine = [p for p in plan if p[0] == r]

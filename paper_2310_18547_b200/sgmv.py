@@ -99,24 +99,37 @@ def _rows_check(x: torch.Tensor | None, y: torch.Tensor | None, pool: AdapterPoo
             raise ValueError(f"{name} must be a CUDA [rows, {cols}] {pool.dtype} tensor with unit column stride")
 
 
+def call_opts(pdl: bool | None = None, tc_min_rows: int | None = None,
+              no_tensor_cores: bool | None = None) -> "_lib.CallOpts":
+    """Per-call options (``lsg_call_opts``); ``None`` keeps the process default."""
+    return _lib.CallOpts(-1 if pdl is None else int(bool(pdl)), -1 if tc_min_rows is None else int(tc_min_rows),
+                         -1 if no_tensor_cores is None else int(bool(no_tensor_cores)))
+
+
 def sgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.Tensor,
-         seg_slot: torch.Tensor, layer: int, num_segments: int | None = None) -> torch.Tensor:
-    """y += x . A_slot . B_slot per segment (fused shrink+expand, one launch)."""
+         seg_slot: torch.Tensor, layer: int, num_segments: int | None = None, *, pdl: bool | None = None,
+         tc_min_rows: int | None = None, no_tensor_cores: bool | None = None) -> torch.Tensor:
+    """y += x . A_slot . B_slot per segment (fused shrink+expand, one launch).
+
+    ``pdl`` / ``tc_min_rows`` / ``no_tensor_cores`` override the process defaults
+    (``set_option``) for this call only (``lsg_sgmv_ex``)."""
     _rows_check(x, y, pool)
     _check_i32(seg_starts, "seg_starts")
     _check_i32(seg_slot, "seg_slot")
     n = seg_slot.numel() if num_segments is None else num_segments
-    # Segments of >= 128 rows run on the tensor cores and keep v in a workspace;
+    # Segments of >= 128 rows run on the tensor cores and may keep v in a workspace;
     # it comes from torch's caching allocator (stream-ordered, graph-capture safe).
     wsb = sgmv_workspace_size(pool, x.shape[0])
     ws = torch.empty(wsb, dtype=torch.uint8, device=x.device) if wsb else None
-    _lib.call("lsg_sgmv_ws", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
-              _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws) if ws is not None else None, wsb, _stream())
+    opts = call_opts(pdl, tc_min_rows, no_tensor_cores)
+    _lib.call("lsg_sgmv_ex", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
+              _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws) if ws is not None else None, wsb, C.byref(opts),
+              _stream())
     return y
 
 
 def sgmv_multi(ys, xs, pools, seg_starts: torch.Tensor, seg_slot: torch.Tensor, layer: int,
-               num_segments: int | None = None):
+               num_segments: int | None = None, *, pdl: bool | None = None, tc_min_rows: int | None = None):
     """Grouped fused call: ``ys[i] += xs[i] . A_i . B_i`` for up to 8 sites sharing one
     segment plan (e.g. q / k / v of a layer), in one launch (lsg_sgmv_multi)."""
     if not (len(ys) == len(xs) == len(pools)) or not 1 <= len(ys) <= 8:
@@ -128,8 +141,9 @@ def sgmv_multi(ys, xs, pools, seg_starts: torch.Tensor, seg_slot: torch.Tensor, 
     n = seg_slot.numel() if num_segments is None else num_segments
     sites = (_lib.Site * len(ys))(*[_lib.Site(y.data_ptr(), y.stride(0), x.data_ptr(), x.stride(0),
                                               C.pointer(pool.table)) for y, x, pool in zip(ys, xs, pools)])
-    _lib.call("lsg_sgmv_multi", sites, len(ys), _ptr(seg_starts), _ptr(seg_slot), n, xs[0].shape[0], layer,
-              _stream())
+    opts = call_opts(pdl, tc_min_rows)
+    _lib.call("lsg_sgmv_multi_ex", sites, len(ys), _ptr(seg_starts), _ptr(seg_slot), n, xs[0].shape[0], layer,
+              C.byref(opts), _stream())
     return ys
 
 
@@ -189,11 +203,14 @@ def bgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, row_slot: torch.Te
     return y
 
 
-def build_segments(row_slot: torch.Tensor, num_slots: int, lead_slot: int = -1):
-    """On-device stable grouping of rows by slot.
+def build_segments(row_slot: torch.Tensor, num_slots: int, lead_slot: int = -1, lead_rows: tuple[int, int] = (0, 0)):
+    """On-device stable grouping of rows by slot (plan_batch's order, simulator.cpp:239-311).
 
-    Returns (row_perm [s_n], seg_starts [s_n+1], seg_slot [s_n], num_segments [1]) -- all
-    device int32; seg_starts / seg_slot are padded past the true segment count.
+    ``lead_slot``: the prefill request's slot (its group goes first); ``lead_rows``: that
+    request's own row range [r0, r1) in ``row_slot`` (placed ahead of the same-adapter
+    decode rows).  Returns (row_perm [s_n], seg_starts [s_n+1], seg_slot [s_n],
+    num_segments [1]) -- all device int32; seg_starts / seg_slot are padded past the
+    true segment count.
     """
     _check_i32(row_slot, "row_slot")
     s_n = row_slot.numel()
@@ -202,7 +219,8 @@ def build_segments(row_slot: torch.Tensor, num_slots: int, lead_slot: int = -1):
     seg_starts = torch.empty(s_n + 1, dtype=torch.int32, device=dev)
     seg_slot = torch.empty(max(s_n, 1), dtype=torch.int32, device=dev)
     nseg = torch.empty(1, dtype=torch.int32, device=dev)
-    _lib.call("lsg_build_segments", _ptr(row_slot), s_n, num_slots, lead_slot, _ptr(row_perm), _ptr(seg_starts),
+    _lib.call("lsg_build_segments", _ptr(row_slot), s_n, num_slots, lead_slot, int(lead_rows[0]), int(lead_rows[1]),
+              _ptr(row_perm), _ptr(seg_starts),
               _ptr(seg_slot), _ptr(nseg), None, 0, _stream())
     return row_perm[:s_n], seg_starts, seg_slot[:s_n], nseg
 
@@ -235,6 +253,6 @@ def query_launch(pool: AdapterPool, num_segments: int, total_rows: int, kernel: 
     return {f: getattr(info, f) for f, _ in LaunchInfo._fields_}
 
 
-__all__ = ["AdapterPool", "sgmv", "sgmv_multi", "dense_lora", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
+__all__ = ["AdapterPool", "call_opts", "sgmv", "sgmv_multi", "dense_lora", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
            "scatter_rows", "set_option", "get_option", "query_launch", "KERNEL_FUSED", "KERNEL_SHRINK",
            "KERNEL_EXPAND", "KERNEL_BGMV"]

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Experimental build of libsgmv_b200.so with extra nvcc flags into build/variants/<name>/.
-# Load it with LSG_LIB_OVERRIDE=build/variants/<name>/libsgmv_b200.so (bench / tests).
+# To measure it, copy it over paper_2310_18547_b200/lib/libsgmv_b200.so inside the gpurun command
+# (the product loader has no override hook).
 # Usage: scripts/build_variant.sh <name> <extra nvcc flags...>
 set -e
 name=$1; shift

@@ -59,3 +59,43 @@ def random_problem(h_in, h_out, rank, bounds, seed):
     A = g.fill_pm1(nseg * h_in * rank).reshape(nseg, h_in, rank)
     B = g.fill_pm1(nseg * rank * h_out).reshape(nseg, rank, h_out)
     return x, A, B
+
+
+# ---- K6 segment builder: the specification the device builder is checked against ----
+def builder_model(row_slot, num_slots, lead, lead_rows=(0, 0)):
+    """Stable grouping of rows by slot (lsg_build_segments, include/lsg_sgmv.h): the lead
+    slot's group first with the prefill rows [lead_rows) ahead of its other rows, then
+    ascending slot, no-adapter rows (slot < 0 or >= num_slots) last as slot -1.
+    Returns (row_perm, seg_starts, seg_slot)."""
+    key = [(0 if s == lead else s + 1) if 0 <= s < num_slots else 1 << 31 for s in row_slot]
+    sub = [0 if (0 <= row_slot[i] < num_slots and row_slot[i] == lead and lead_rows[0] <= i < lead_rows[1]) else 1
+           for i in range(len(row_slot))]
+    perm = sorted(range(len(row_slot)), key=lambda i: (key[i], sub[i], i))
+    starts, slots = [], []
+    for i, r in enumerate(perm):
+        if i == 0 or key[r] != key[perm[i - 1]]:
+            starts.append(i)
+            s = row_slot[r]
+            slots.append(s if 0 <= s < num_slots else -1)
+    return perm, starts + [len(row_slot)], slots
+
+
+def plan_batch_rows(case):
+    """Token rows of a golden plan_batch case in request order (simulator.cpp:267-276: a
+    prefill contributes its prompt rows, a decode one row; only the first pending prefill is
+    scheduled), with slots = rank of the LoraId.  Returns (uniq_loras, row_slot, req_of_row,
+    lead_slot, lead_rows)."""
+    lora, done, prompt, plan = case["lora"], case["done"], case["prompt"], case["plan"]
+    uniq = sorted(set(lora))
+    slot_of = {l: i for i, l in enumerate(uniq)}
+    rows, req_of_row, lead_rows = [], [], (0, 0)
+    for i, (l, d) in enumerate(zip(lora, done)):
+        if d:
+            rows.append(slot_of[l])
+            req_of_row.append(i)
+        elif i == plan["prefill"]:
+            lead_rows = (len(rows), len(rows) + prompt[i])
+            rows.extend([slot_of[l]] * prompt[i])
+            req_of_row.extend([i] * prompt[i])
+    lead = slot_of[lora[plan["prefill"]]] if plan["prefill"] >= 0 else -1
+    return uniq, rows, req_of_row, lead, lead_rows

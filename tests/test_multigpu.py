@@ -171,3 +171,40 @@ def test_adapter_pool_layer_view_pointer_table_cpu():
     assert v.num_layers == 1 and v.table.num_layers == 1 and v.table.num_slots == 3
     with pytest.raises(ValueError):
         pool.layer_view(5)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("nseg,rows", [(2, 8), (3, 8), (4, 16), (5, 2), (64, 1), (1, 64), (9, 7)])
+def test_plan_piece_bound_and_cuts_only_when_they_help(world, nseg, rows):
+    """Several small equal segments: the plan stays within (segments + world - 1) pieces,
+    and every cut it makes lowers the largest rank load below the uncut LPT plan."""
+    h, r = 4096, 16
+    bounds = np.arange(nseg + 1, dtype=np.int32) * rows
+    plan = part.partition_segments(bounds, h, h, r, world)
+    assert len(plan) <= nseg + world - 1
+    loads = np.zeros(world, dtype=np.int64)
+    for rank, _, r0, r1 in plan:
+        loads[rank] += _bytes(r1 - r0, h, h, r)
+    # the uncut LPT makespan of equal segments: ceil(nseg / world) segments on one rank
+    uncut = -(-nseg // world) * _bytes(rows, h, h, r)
+    assert loads.max() <= uncut
+    if len(plan) > nseg:
+        assert loads.max() < uncut
+
+
+def test_plan_routes_pinned_segments_to_their_owner():
+    """Slot-sharded pool (configs[4]): a segment whose adapter lives on one rank goes there
+    whole; replicated segments balance around them."""
+    h, r = 8192, 16
+    bounds = np.array([0, 1, 2, 3, 4, 40, 41, 42, 43], dtype=np.int32)
+    owner = [0, 0, 0, 1, -1, 2, 3, 3]
+    plan = part.partition_segments(bounds, h, h, r, 4, seg_owner=owner)
+    rows = sorted(x for _, _, r0, r1 in plan for x in range(r0, r1))
+    assert rows == list(range(43))
+    for rank, seg, r0, r1 in plan:
+        if owner[seg] >= 0:
+            assert rank == owner[seg] and (r0, r1) == (bounds[seg], bounds[seg + 1])
+    with pytest.raises(RuntimeError, match="seg_owner"):
+        part.partition_segments(bounds, h, h, r, 2, seg_owner=owner)
+    with pytest.raises(ValueError):
+        part.partition_segments(bounds, h, h, r, 4, seg_owner=owner[:-1])

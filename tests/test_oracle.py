@@ -191,3 +191,23 @@ def test_live_against_reference(orc):
     assert np.array_equal(orc.sgmv_shrink(x, bounds, A), v)
     assert np.array_equal(orc.sgmv_expand(v, bounds, B), ref.sgmv_expand(v, bounds, A, B))
     assert ref.roofline_csv(64) == load("cost_model.json")["roofline_csv"]
+
+
+def test_builder_spec_reproduces_plan_batch_row_order():
+    """The K6 builder's specification (tests/_util.builder_model, what the device builder
+    is checked against bit-exactly in test_sgmv_gpu.py) yields plan_batch's bounds, segment
+    adapters and row order -- prefill rows first, then `decodes` -- on every golden case."""
+    from tests._util import builder_model, plan_batch_rows
+    cases = load("plan_batch.json")
+    assert len(cases) == 21
+    for ci, case in enumerate(cases):
+        plan = case["plan"]
+        uniq, rows, req_of_row, lead, lead_rows = plan_batch_rows(case)
+        perm, starts, slots = builder_model(rows, len(uniq), lead, lead_rows)
+        assert starts == plan["bounds"], ci
+        assert [uniq[s] for s in slots] == plan["loras"], ci
+        order = []
+        for r in perm:
+            if not order or order[-1] != req_of_row[r]:
+                order.append(req_of_row[r])
+        assert order == ([plan["prefill"]] if plan["prefill"] >= 0 else []) + plan["decodes"], ci

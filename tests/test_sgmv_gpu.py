@@ -14,8 +14,8 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from tests._util import (DISTINCT, IDENTICAL, NORTH_STAR_TOL, SKEWED, TOL, UNIFORM, oracle, random_problem,
-                         row_norm_err, segments_for)
+from tests._util import (DISTINCT, IDENTICAL, NORTH_STAR_TOL, SKEWED, TOL, UNIFORM, builder_model, oracle,
+                         plan_batch_rows, random_problem, row_norm_err, segments_for)
 
 pytestmark = pytest.mark.gpu
 
@@ -351,24 +351,15 @@ def test_invalid_arguments_raise(lsg):
 # ---------------------------------------------------------------------------------
 # K6: on-device segment builder
 # ---------------------------------------------------------------------------------
-def _host_grouping(row_slot, num_slots, lead):
-    key = [(0 if s == lead else s + 1) if 0 <= s < num_slots else 1 << 31 for s in row_slot]
-    perm = sorted(range(len(row_slot)), key=lambda i: (key[i], i))
-    starts, slots = [], []
-    for i, r in enumerate(perm):
-        if i == 0 or key[r] != key[perm[i - 1]]:
-            starts.append(i)
-            s = row_slot[r]
-            slots.append(s if 0 <= s < num_slots else -1)
-    return perm, starts + [len(row_slot)], slots
-
-
 @pytest.mark.parametrize("n,num_slots", [(1, 4), (9, 3), (64, 64), (64, 8), (333, 40), (2079, 1000), (16384, 7)])
 def test_build_segments_matches_host_grouping(lsg, n, num_slots):
     rs = np.random.default_rng(n).integers(-1, num_slots + 1, n).astype(np.int32)
     lead = int(rs[n // 2])
-    perm, starts, slots = _host_grouping(rs.tolist(), num_slots, lead)
-    row_perm, seg_starts, seg_slot, nseg = lsg.build_segments(torch.tensor(rs, device="cuda"), num_slots, lead)
+    lead_rows = (n // 2, min(n, n // 2 + 5))  # a "prefill" range in the middle of the batch
+    rs[lead_rows[0]:lead_rows[1]] = lead
+    perm, starts, slots = builder_model(rs.tolist(), num_slots, lead, lead_rows)
+    row_perm, seg_starts, seg_slot, nseg = lsg.build_segments(torch.tensor(rs, device="cuda"), num_slots, lead,
+                                                              lead_rows)
     k = int(nseg.item())
     assert k == len(slots)
     assert row_perm.cpu().tolist() == perm
@@ -378,26 +369,26 @@ def test_build_segments_matches_host_grouping(lsg, n, num_slots):
 
 
 def test_build_segments_reproduces_plan_batch_golden(lsg):
-    """plan_batch layouts (simulator.cpp:239-311) from the reference, slots = LoraId rank."""
-    for case in json.load(open(os.path.join(GOLDEN, "plan_batch.json"))):
+    """plan_batch layouts (simulator.cpp:239-311) from the reference, slots = LoraId rank:
+    segment bounds, segment adapters AND the row order (prefill prompt rows first, then the
+    decodes in plan_batch's `decodes` order) for all golden cases."""
+    cases = json.load(open(os.path.join(GOLDEN, "plan_batch.json")))
+    assert len(cases) == 21
+    for ci, case in enumerate(cases):
         lora, done, prompt = case["lora"], case["done"], case["prompt"]
         plan = case["plan"]
-        uniq = sorted(set(lora))
-        slot_of = {l: i for i, l in enumerate(uniq)}
-        # token rows in request order: a prefill contributes prompt rows, a decode one row;
-        # only the first pending prefill is scheduled (simulator.cpp:267-276)
-        rows = []
-        for i, (l, d) in enumerate(zip(lora, done)):
-            if d:
-                rows.append(slot_of[l])
-            elif i == plan["prefill"]:
-                rows.extend([slot_of[l]] * prompt[i])
-        lead = slot_of[lora[plan["prefill"]]] if plan["prefill"] >= 0 else -1
-        _, seg_starts, seg_slot, nseg = lsg.build_segments(torch.tensor(rows, dtype=torch.int32, device="cuda"),
-                                                           len(uniq), lead)
+        uniq, rows, req_of_row, lead, lead_rows = plan_batch_rows(case)
+        row_perm, seg_starts, seg_slot, nseg = lsg.build_segments(
+            torch.tensor(rows, dtype=torch.int32, device="cuda"), len(uniq), lead, lead_rows)
         k = int(nseg.item())
-        assert seg_starts.cpu().tolist()[: k + 1] == plan["bounds"]
-        assert [uniq[s] for s in seg_slot.cpu().tolist()[:k]] == plan["loras"]
+        assert seg_starts.cpu().tolist()[: k + 1] == plan["bounds"], ci
+        assert [uniq[s] for s in seg_slot.cpu().tolist()[:k]] == plan["loras"], ci
+        order = []
+        for r in row_perm.cpu().tolist():  # request order implied by the gathered rows
+            if not order or order[-1] != req_of_row[r]:
+                order.append(req_of_row[r])
+        expect = ([plan["prefill"]] if plan["prefill"] >= 0 else []) + plan["decodes"]
+        assert order == expect, (ci, order, expect)
 
 
 def test_builder_feeds_sgmv_without_host_readback(lsg):
@@ -642,3 +633,160 @@ def test_tc_row_threshold_option(lsg):
     assert torch.equal(y[200:203], cc[200:203])  # the 3-row segment is untouched by the change
     with pytest.raises(RuntimeError):
         lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, -1)
+
+
+# ---------------------------------------------------------------------------------
+# Round-2 parity gaps: the BASELINE configs' exact layouts, shrink output v on random
+# data, the acceptance-size verify run, grouped rank-64 launches
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_config1_exact_layout_4x8(lsg, dtype):
+    """configs[0]: h=4096, r=16, 32 decode rows, 4 LoRAs x 8 rows -- every formulation against
+    the oracle, and the three GPU formulations bitwise equal."""
+    bounds = np.array([0, 8, 16, 24, 32], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 401)
+    y0 = oracle().rng(402).fill_pm1(32 * 4096).reshape(32, 4096)
+    p = Problem(lsg, x, A, B, bounds, dtype, y0=y0)
+    ref = p.reference()
+    base = p.run("fused")
+    assert row_norm_err(base.double().cpu().numpy(), ref) <= tol(dtype)
+    for kind in ("two_launch", "bgmv"):
+        assert torch.equal(p.run(kind), base), kind
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("pop", [DISTINCT, UNIFORM])
+def test_config5_1000_slot_pool_scattered_slots_nonzero_layer(lsg, dtype, pop):
+    """configs[4] on one GPU: h=8192, r=16, a 1000-slot pool with 3 layers, the batch's
+    adapters on scattered slots (not 0..n-1), launched at layer 2; the oracle gets the
+    dequantised weights read back from exactly those slots."""
+    h, r, slots_total, layers, layer = 8192, 16, 1000, 3, 2
+    bounds, _, _ = segments_for(pop, 64, 501 + pop)
+    nseg = len(bounds) - 1
+    pool = lsg.AdapterPool(slots_total, layers, h, h, r, dtype)
+    gen = torch.Generator(device="cuda").manual_seed(503)
+    pool.a.uniform_(-1, 1, generator=gen)
+    pool.b.uniform_(-1, 1, generator=gen)
+    slots = np.random.default_rng(504).choice(slots_total, nseg, replace=False).astype(np.int32)
+    x = torch.empty(64, h, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen)
+    y0 = torch.empty(64, h, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen)
+    ss = torch.tensor(bounds.astype(np.int64), dtype=torch.int32, device="cuda")
+    sl = torch.tensor(slots, device="cuda")
+    y = y0.clone()
+    lsg.sgmv(y, x, pool, ss, sl, layer)
+    torch.cuda.synchronize()
+    idx = torch.tensor(slots.astype(np.int64), device="cuda")
+    Ad = pool.a[idx, layer].double().cpu().numpy()
+    Bd = pool.b[idx, layer].double().cpu().numpy()
+    ref = y0.double().cpu().numpy() + oracle().lora_addon(x.double().cpu().numpy(), bounds, Ad, Bd)
+    assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(dtype)
+    # the same rows through BGMV with per-row slots: bitwise
+    row_slot = torch.tensor(np.repeat(slots, np.diff(bounds.astype(np.int64))), device="cuda")
+    yb = y0.clone()
+    lsg.bgmv(yb, x, pool, row_slot, layer)
+    torch.cuda.synchronize()
+    assert torch.equal(yb, y)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("pop", [DISTINCT, UNIFORM, SKEWED, IDENTICAL])
+def test_shrink_v_matches_oracle_random(lsg, dtype, shape, pop):
+    """lsg_sgmv_shrink's fp32 v against the oracle's sgmv_shrink (sgmv.cpp:105-119) on random
+    data at every BASELINE shape: v is fp32 with no output rounding, so the per-row
+    normalised error is at fp32-accumulation level (<= 1e-5)."""
+    h_in, h_out, r = shape
+    bounds, _, _ = segments_for(pop, 64, 601 + pop)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 602 + pop)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    v = torch.empty(64, r, dtype=torch.float32, device="cuda")
+    lsg.sgmv_shrink(v, p.x, p.pool, p.seg_starts, p.seg_slot, 0)
+    torch.cuda.synchronize()
+    vref = oracle().sgmv_shrink(p.xd, p.bounds, p.Ad)
+    assert row_norm_err(v.double().cpu().numpy(), vref) <= 1e-5
+
+
+def test_verify_sgmv_acceptance_size_1000_trials(lsg):
+    """Acceptance criterion 1 (acceptance_main.cpp:57-68): verify_sgmv(1000, 42) -- 1000
+    randomised trials, every popularity and verify shape -- through the fused kernel, fp16."""
+    o = oracle()
+    g = o.rng(o.derive_seed(42, 17))
+    worst = 0.0
+    for t in range(1000):
+        tr = g.verify_next_trial(t)
+        p = Problem(lsg, tr["x"], tr["A"], tr["B"], tr["bounds"], torch.float16)
+        err = row_norm_err(p.run("fused").double().cpu().numpy(), p.reference())
+        worst = max(worst, err)
+        assert err <= tol(torch.float16), (t, err)
+    assert worst <= NORTH_STAR_TOL
+
+
+@pytest.mark.parametrize("pop", [UNIFORM, SKEWED, IDENTICAL])
+def test_grouped_sites_rank64_shared_adapters_bitwise(lsg, pop):
+    """Rank 64 with shared adapters plans 4-row tiles, which the grouped item mode does not
+    have: lsg_sgmv_multi must run those sites one by one (it used to update only
+    site 0) -- every site bitwise equal to its own lsg_sgmv call."""
+    bounds, _, _ = segments_for(pop, 64, 700 + pop)
+    probs = []
+    for i in range(3):
+        x, A, B = random_problem(5120, 5120, 64, bounds, 710 + i)
+        y0 = oracle().rng(720 + i).fill_pm1(64 * 5120).reshape(64, 5120)
+        probs.append(Problem(lsg, x, A, B, bounds, torch.float16, y0=y0))
+    ref = [p.run() for p in probs]
+    ys = [p.y0.clone() for p in probs]
+    lsg.sgmv_multi(ys, [p.x for p in probs], [p.pool for p in probs], probs[0].seg_starts, probs[0].seg_slot, 0)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert not torch.equal(ys[i], probs[i].y0), i
+        assert torch.equal(ys[i], ref[i]), i
+
+
+def test_call_options_are_per_call(lsg):
+    """lsg_sgmv_ex: a per-call tc_min_rows / no_tensor_cores overrides the process default for
+    that call only (the default is untouched and the next call uses it again)."""
+    bounds = np.array([0, 200, 203, 260], dtype=np.uint64)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 96)
+    p = Problem(lsg, x, A, B, bounds, torch.float16)
+    tc = p.run()
+    y = p.y0.clone()
+    lsg.sgmv(y, p.x, p.pool, p.seg_starts, p.seg_slot, 0, no_tensor_cores=True)
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 1)
+    cc = p.run()
+    lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(y, cc)
+    assert lsg.get_option(lsg.LSG_OPT_NO_TENSOR_CORES) == 0
+    assert torch.equal(p.run(), tc)
+    y2 = p.y0.clone()
+    lsg.sgmv(y2, p.x, p.pool, p.seg_starts, p.seg_slot, 0, tc_min_rows=261)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, cc)
+
+
+def test_grid_limit_many_rows(lsg):
+    """More than 65535 rows (gridDim.y limit): row-mode launches switch to the
+    tile-scan decode and BGMV runs in row chunks -- results bitwise equal to each other and
+    to the oracle on sampled rows."""
+    n, h, r = 70000, 128, 8
+    nseg = 7
+    bounds = np.linspace(0, n, nseg + 1).astype(np.uint64)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    pool = lsg.AdapterPool(nseg, 1, h, h, r, torch.float16)
+    pool.a.uniform_(-1, 1, generator=gen)
+    pool.b.uniform_(-1, 1, generator=gen)
+    x = torch.empty(n, h, dtype=torch.float16, device="cuda").uniform_(-1, 1, generator=gen)
+    ss = torch.tensor(bounds.astype(np.int64), dtype=torch.int32, device="cuda")
+    sl = torch.arange(nseg, dtype=torch.int32, device="cuda")
+    y = torch.zeros(n, h, dtype=torch.float16, device="cuda")
+    lsg.sgmv(y, x, pool, ss, sl, 0, no_tensor_cores=True)
+    rs = torch.repeat_interleave(sl, torch.tensor(np.diff(bounds.astype(np.int64)), device="cuda")).to(torch.int32)
+    yb = torch.zeros_like(y)
+    lsg.bgmv(yb, x, pool, rs, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(y, yb)
+    pick = np.array([0, 1, 9999, 65534, 65535, 65536, n - 1])
+    xs = x[torch.tensor(pick, device="cuda")].double().cpu().numpy()
+    segs = np.searchsorted(bounds.astype(np.int64), pick, side="right") - 1
+    ref = np.stack([xs[i] @ pool.a[segs[i], 0].double().cpu().numpy() @ pool.b[segs[i], 0].double().cpu().numpy()
+                    for i in range(len(pick))])
+    assert row_norm_err(y[torch.tensor(pick, device="cuda")].double().cpu().numpy(), ref) <= tol(torch.float16)
