@@ -9,11 +9,27 @@ fused SGMV launches (one shrink+expand pair each -- the paper's "LoRA operator",
 PAPER.md:516), every launch on its own (site, layer) weights and its own x / y
 buffers, replayed from a CUDA graph.  ``value`` is microseconds per LoRA site
 (= "us/layer" in the reference's sense, cost_model.cpp:53-61), lower is better.
-Weights rotate over a 3.7 GB pool and x/y over 235 MB per step, so every launch
+Weights rotate over a 3.5 GiB pool and x/y over 224 MiB per step, so every launch
 reads HBM, not L2 (config.l2 says so).
 
 Algorithmic bytes per launch (cost_model.cpp:59):
     2 * (s_n * (h + r) + n * h * r) * 2 B  = 17,829,888 B at the headline config.
+
+The default N=1 line also carries, so that the driver's own run records them:
+  * ``sweep``    batch 1..64 x Distinct/Uniform/Skewed/Identical (the metric's "vs batch
+                 across" part), us per launch and fraction of the HBM roofline;
+  * ``configs``  the other BASELINE configs (c1, c3 SGMV and BGMV, c4 prefill 128 and
+                 2048, c5 1000-slot pool), same bookkeeping;
+  * ``roofline.traffic`` and ``configs[*].traffic``: DRAM bytes per launch of THIS build,
+                 measured by an ncu pass over one probe run (counters, never timings);
+  * ``cpu_baseline``: the reference's own lora_addon on a Batch built once
+                 (bench_sgmv.cpp:37-47), one pinned core, with the shrink/expand split.
+
+Multi-GPU (one process per GPU, request-partitioned, no collective on the data path):
+``--gpus N`` re-launches itself under torch.distributed.run when WORLD_SIZE is unset.
+``--scaling weak`` (default): 64 rows per GPU, value = max-over-ranks time per
+64-row site-equivalent of the whole job; ``--scaling strong``: 64 rows in all,
+partitioned, value = max-over-ranks time per site.
 
 --impl reference times the reference's own CPU SGMV (oracle/_ref, compiled from
 /root/reference/proj/core/src/sgmv.cpp; else the oracle/ restatement) on all
@@ -22,9 +38,14 @@ host cores for the same metric/config.
 from __future__ import annotations
 
 import argparse
+import csv
+import hashlib
+import io
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -36,24 +57,29 @@ sys.path.insert(0, ROOT)
 
 POPS = {"distinct": 0, "uniform": 1, "skewed": 2, "identical": 3}
 SITES_PER_LAYER, LAYERS = 7, 32
-
+METRIC = "SGMV us/layer (LoRA shrink+expand per projection site)"
 
 PRESETS = {
     "c1": dict(hidden=4096, rank=16, batch=32, segments="8,8,8,8"),
     "c2": dict(hidden=4096, rank=16, batch=64, popularity="distinct"),
     "c3": dict(hidden=5120, rank=64, batch=64, popularity="uniform"),
     "c3-bgmv": dict(hidden=5120, rank=64, batch=64, popularity="uniform", kernel="bgmv"),
+    "c3-skewed": dict(hidden=5120, rank=64, batch=64, popularity="skewed"),
     "c4": dict(hidden=4096, rank=16, prefill=2048, sites=32),
+    "c4-128": dict(hidden=4096, rank=16, prefill=128, sites=64),
     "c5": dict(hidden=8192, rank=16, batch=64, popularity="distinct", slots=1000, sites=32),
 }
+EXTRA_CONFIGS = ["c1", "c3", "c3-skewed", "c3-bgmv", "c4-128", "c4", "c5"]
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: 64 rows per GPU; strong: 64 rows in all, partitioned over the GPUs")
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--batch", type=int, default=64)
@@ -73,24 +99,42 @@ def parse():
     ap.add_argument("--segments", default="", help="explicit segment sizes, e.g. 8,8,8,8 (overrides popularity)")
     ap.add_argument("--prefill", type=int, default=0, help="mixed batch: one prefill segment of this many rows "
                     "plus 31 distinct decode rows (configs[3])")
-    ap.add_argument("--preset", choices=["c1", "c2", "c3", "c3-bgmv", "c4", "c5"], default="",
+    ap.add_argument("--preset", choices=sorted(PRESETS), default="",
                     help="BASELINE.json configs: c1 h4096 r16 32 rows/4 LoRAs; c2 headline; c3 h5120 r64 uniform; "
                          "c4 prefill 2048 + 31 decodes; c5 h8192 r16 1000-slot pool")
     ap.add_argument("--sites", type=int, default=SITES_PER_LAYER * LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also print per-(popularity,batch) lines to stderr")
+    ap.add_argument("--no-extras", action="store_true", help="headline only: no sweep / configs / traffic pass")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic pass")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graph, no extras)")
     ap.add_argument("--profile-graph", action="store_true",
                     help="short run for ncu --graph-profiling graph: capture the step graph, replay it twice")
-    pre, _ = ap.parse_known_args()
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
+    pre, _ = ap.parse_known_args(argv)
     ap.set_defaults(**PRESETS.get(pre.preset, {}))  # a preset sets defaults; explicit flags still win
-    a = ap.parse_args()
+    a = ap.parse_args(argv)
+    normalise(a)
+    return a
+
+
+def normalise(a):
     if a.prefill:
         a.segments = ",".join([str(a.prefill)] + ["1"] * 31)
     if a.segments:
         a.batch = sum(int(x) for x in a.segments.split(","))
     return a
+
+
+def cfg_args(name: str, base=None):
+    """An argparse namespace for preset `name` (the other fields from `base` / defaults)."""
+    a = parse([] if base is None else [])
+    for k, v in PRESETS[name].items():
+        setattr(a, k, v)
+    a.preset = name
+    if base is not None:
+        a.dtype, a.pdl = base.dtype, base.pdl
+    return normalise(a)
 
 
 def alg_bytes(rows, nseg, h, r, e=2):
@@ -119,15 +163,32 @@ def workload_name(a):
     return f"{model}-lora h={a.hidden} r={a.rank} {shape} {a.kernel} ({a.dtype})"
 
 
-def bounds_for(a, world=1):
-    """Segment boundaries of the (global) batch: ``world`` copies of the per-GPU batch."""
+def bounds_for(a, copies=1):
+    """Segment boundaries of `copies` concatenated per-GPU batches."""
     if a.segments:
         b = [0]
-        for _ in range(world):
+        for _ in range(copies):
             for x in a.segments.split(","):
                 b.append(b[-1] + int(x))
         return b
-    return segments(a.popularity, a.batch * world)
+    return segments(a.popularity, a.batch * copies)
+
+
+def global_bounds(a, world):
+    """Weak scaling: the global batch is `batch` rows per GPU; strong: `batch` rows in all."""
+    return bounds_for(a, world if a.scaling == "weak" else 1)
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "allowed_cpus": len(os.sched_getaffinity(0)), "cpu_model": model}
 
 
 # ----------------------------------------------------------------------------------
@@ -181,7 +242,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------
-# CPU baselines
+# CPU baselines (the reference's own SGMV; oracle/ is reached only from these legs)
 # ----------------------------------------------------------------------------------
 def _cpu_problem(a, seed=5):
     from oracle.oracle import Oracle
@@ -205,37 +266,79 @@ def cpu_impl():
     return Oracle(), "port"
 
 
-def cpu_baseline(a, budget_s=10.0):
-    """Reference SGMV (fp64, 1 thread, as shipped) on a bounded sample of the workload."""
-    impl, kind = cpu_impl()
-    x, A, B, bounds = _cpu_problem(a)
-    impl.lora_addon(x, bounds, A, B)  # warm
+def _time_cpu(impl, kind, prob, op, budget_s):
+    """Seconds per call of `op` on problem `prob`.  The reference build times a Batch built
+    once (bench_sgmv.cpp:37-47); the port (oracle/ restatement, no Batch type) times its
+    array entry point."""
+    x, A, B, bounds = prob
+    if kind == "reference":
+        return impl.bench_batch(x, bounds, A, B, op, budget_s=budget_s)
+    fn = {"lora_addon": lambda: impl.lora_addon(x, bounds, A, B),
+          "sgmv_shrink": lambda: impl.sgmv_shrink(x, bounds, A),
+          "sgmv_expand": lambda: impl.sgmv_expand(v, bounds, B)}[op]
+    v = impl.sgmv_shrink(x, bounds, A) if op == "sgmv_expand" else None
     n, t0 = 0, time.perf_counter()
     while True:
-        impl.lora_addon(x, bounds, A, B)
+        fn()
         n += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or n >= 2000:
-            break
-    return {"value": el / n * 1e6, "unit": "us/layer", "cores": 1, "kind": kind,
-            "sample": f"{n} x lora_addon(batch={a.batch}, {a.popularity}, h={a.hidden}, r={a.rank}) fp64 "
-                      f"on dequantised {a.dtype} inputs, {el:.1f} s, 1 thread ({'oracle/_ref' if kind == 'reference' else 'oracle port'})"}
+        if el >= budget_s:
+            return el / n, n
+
+
+def cpu_baseline(a, budget_s=6.0):
+    """Reference SGMV (fp64, as shipped) on a Batch built once, one thread pinned to one core
+    (taskset -c <core>), lora_addon plus the shrink / expand split."""
+    impl, kind = cpu_impl()
+    prob = _cpu_problem(a)
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        _time_cpu(impl, kind, prob, "lora_addon", 0.2)  # warm
+        t_add, n_add = _time_cpu(impl, kind, prob, "lora_addon", budget_s)
+        t_sh, n_sh = _time_cpu(impl, kind, prob, "sgmv_shrink", budget_s / 2)
+        t_ex, n_ex = _time_cpu(impl, kind, prob, "sgmv_expand", budget_s / 2)
+    finally:
+        os.sched_setaffinity(0, old)
+    return {"value": t_add * 1e6, "unit": "us/layer", "cores": 1, "kind": kind,
+            "shrink_us": t_sh * 1e6, "expand_us": t_ex * 1e6, "pinned_core": core, **host_info(),
+            "sample": f"{n_add} x lora_addon(batch={a.batch}, {a.popularity}, h={a.hidden}, r={a.rank}) fp64 on "
+                      f"dequantised {a.dtype} inputs, Batch built once (bench_sgmv.cpp:37-47), "
+                      f"{t_add * n_add:.1f} s, 1 thread pinned to core {core} "
+                      f"({'oracle/_ref' if kind == 'reference' else 'oracle port'}); "
+                      f"split: {n_sh} x sgmv_shrink, {n_ex} x sgmv_expand"}
 
 
 def run_reference_arm(a):
+    """The reference's lora_addon on every host core at once (one prebuilt Batch and one
+    pinned thread per core); a step is one call per thread."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     impl, kind = cpu_impl()
-    threads = os.cpu_count() or 1
+    cores = sorted(os.sched_getaffinity(0))
+    threads = len(cores)
     problems = [_cpu_problem(a, seed=5 + t) for t in range(threads)]
+    start, done = threading.Barrier(threads + 1), threading.Barrier(threads + 1)
+    stop = [False]
+
+    def worker(t):
+        os.sched_setaffinity(0, {cores[t]})  # this thread only
+        while True:
+            start.wait()
+            if stop[0]:
+                return
+            _time_cpu(impl, kind, problems[t], "lora_addon", 0.0)  # exactly one call
+            done.wait()
+
+    ths = [threading.Thread(target=worker, args=(t,), daemon=True) for t in range(threads)]
+    for t in ths:
+        t.start()
 
     def one_step():
-        ths = [threading.Thread(target=impl.lora_addon, args=(p[0], p[3], p[1], p[2])) for p in problems]
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
+        start.wait()
+        done.wait()
 
     for _ in range(a.warmup):
         one_step()
@@ -243,37 +346,288 @@ def run_reference_arm(a):
     for _ in range(a.steps):
         one_step()
     el = time.perf_counter() - t0
+    stop[0] = True
+    start.wait()
     sites = a.steps * threads
     us = el / sites * 1e6
-    line = {"metric": "SGMV us/layer (LoRA shrink+expand per projection site)", "value": us, "unit": "us/layer",
+    line = {"metric": METRIC, "value": us, "unit": "us/layer",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
+            "higher_is_better": False, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_name(a), "hidden": a.hidden, "rank": a.rank, "batch": a.batch,
-                       "popularity": a.popularity, "step": f"{threads} concurrent lora_addon calls (one per host thread)"},
-            "cpu_baseline": {"value": us, "unit": "us/layer", "cores": threads, "kind": kind,
-                             "sample": f"{sites} lora_addon calls over {threads} threads, {el:.1f} s"},
+                       "popularity": a.popularity,
+                       "step": f"{threads} concurrent lora_addon calls (one prebuilt Batch and one pinned thread "
+                               f"per host core)"},
+            "cpu_baseline": {"value": us, "unit": "us/layer", "cores": threads, "kind": kind, **host_info(),
+                             "sample": f"{sites} lora_addon calls over {threads} pinned threads, {el:.1f} s "
+                                       f"(aggregate: wall time / calls)"},
             "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------------
-# GPU arm
+# GPU workloads
 # ----------------------------------------------------------------------------------
+class Workload:
+    """One config's device state: adapter pool (one layer per projection site), x / y per
+    site, the segment plan, and the launch of site s."""
+
+    def __init__(self, lsg, torch, a, bounds, dtype, seed=1000, slot_seed=7, sites=None):
+        self.lsg, self.torch, self.a = lsg, torch, a
+        h, r = a.hidden, a.rank
+        self.sites = sites or a.sites
+        self.bounds = [int(v) for v in bounds]
+        self.rows = self.bounds[-1]
+        self.nseg = len(self.bounds) - 1
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        self.nslots = max(a.slots, self.nseg, 1)
+        self.pool = lsg.AdapterPool(self.nslots, self.sites, h, h, r, dtype)
+        self.pool.a.uniform_(-1, 1, generator=gen)
+        self.pool.b.uniform_(-1, 1, generator=gen)
+        self.xs = torch.empty(self.sites, max(self.rows, 1), h, dtype=dtype, device="cuda").uniform_(
+            -1, 1, generator=gen)
+        self.ys = torch.zeros(self.sites, max(self.rows, 1), h, dtype=dtype, device="cuda")
+        self.seg_starts = torch.tensor(self.bounds, dtype=torch.int32, device="cuda")
+        # the batch's adapters are distinct slots spread over the pool
+        slots = torch.randperm(self.nslots, generator=torch.Generator().manual_seed(slot_seed))[:self.nseg]
+        self.slots = slots.to(torch.int32)
+        self.seg_slot = self.slots.cuda()
+        self.row_slot = torch.repeat_interleave(self.slots, torch.tensor(np.diff(self.bounds), dtype=torch.int64)).to(
+            torch.int32).cuda()
+        # The serving engine knows its step's segment lengths: a decode-only step (no segment
+        # of >= 128 rows) skips the tensor-core pass -- a per-call option (lsg_call_opts).
+        self.tc_min_rows = self.rows + 1 if max(np.diff(self.bounds), default=0) < 128 else None
+        self.bytes = alg_bytes(self.rows, self.nseg, h, r)
+
+    def launch(self, s, ys=None, xs=None):
+        ys = self.ys if ys is None else ys
+        xs = self.xs if xs is None else xs
+        if self.rows == 0:
+            return
+        if self.a.kernel == "bgmv":
+            self.lsg.bgmv(ys[s], xs[s], self.pool, self.row_slot, s)
+        else:
+            self.lsg.sgmv(ys[s], xs[s], self.pool, self.seg_starts, self.seg_slot, s, tc_min_rows=self.tc_min_rows)
+
+    def step(self, ys=None, xs=None):
+        for s in range(self.sites):
+            self.launch(s, ys, xs)
+
+    def info(self):
+        return self.lsg.query_launch(self.pool, self.nseg, max(self.rows, 1),
+                                     self.lsg.KERNEL_BGMV if self.a.kernel == "bgmv" else self.lsg.KERNEL_FUSED)
+
+    def free(self):
+        del self.pool, self.xs, self.ys
+
+
+def graph_of(torch, fn, stream):
+    with torch.cuda.stream(stream):
+        fn()  # eager warm-up (sets function attributes before capture)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
+
+
+def device_time_ms(torch, dist, world, stream, fn, k):
+    """k calls of fn on `stream`, bracketed by barrier + synchronize, CUDA events on the
+    launching stream; max over ranks."""
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(k):
+            fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    return ms
+
+
+def measure_graph(torch, stream, wl, replays=10, warm=3):
+    """us per launch of wl's step graph (single GPU, CUDA events on the replay stream)."""
+    g = graph_of(torch, wl.step, stream)
+    with torch.cuda.stream(stream):
+        for _ in range(warm):
+            g.replay()
+    ms = device_time_ms(torch, None, 1, stream, g.replay, replays)
+    del g
+    return ms * 1e3 / (replays * wl.sites)
+
+
+def peak_gbs():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+        if p:
+            return p, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def config_line(name, a, wl, us, peak):
+    gbs = wl.bytes / (us * 1e-6) / 1e9
+    return {"config": name, "workload": workload_name(a), "rows": wl.rows, "segments": wl.nseg,
+            "us_per_launch": us, "alg_bytes": wl.bytes, "gbs": gbs, "frac": gbs / peak, "launch": wl.info()}
+
+
+def run_configs(lsg, torch, a, dtype, stream, peak):
+    out = []
+    for name in EXTRA_CONFIGS:
+        c = cfg_args(name, a)
+        wl = Workload(lsg, torch, c, bounds_for(c), dtype)
+        out.append(config_line(name, c, wl, measure_graph(torch, stream, wl), peak))
+        wl.free()
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_sweep(lsg, torch, a, dtype, stream, peak):
+    """Batch x popularity at the configured shape (the metric's 'vs batch across' part)."""
+    out = []
+    for pop in ("distinct", "uniform", "skewed", "identical"):
+        for batch in (1, 2, 4, 8, 16, 32, 64):
+            c = parse([])
+            c.hidden, c.rank, c.dtype, c.pdl = a.hidden, a.rank, a.dtype, a.pdl
+            c.popularity, c.batch = pop, batch
+            wl = Workload(lsg, torch, c, segments(pop, batch), dtype)
+            line = config_line(f"{pop}-{batch}", c, wl, measure_graph(torch, stream, wl), peak)
+            out.append({k: line[k] for k in ("config", "rows", "segments", "us_per_launch", "gbs", "frac")})
+            wl.free()
+        torch.cuda.empty_cache()
+    return out
+
+
+# ---- DRAM traffic of this build: one ncu pass over a probe run ------------------------
+PROBE_CONFIGS = ["c2"] + EXTRA_CONFIGS
+PROBE_CALLS = 3
+
+
+def traffic_probe(lsg, torch, a, dtype):
+    """Run under ncu: for each probe config, a marker kernel (torch's spin_kernel), then
+    PROBE_CALLS calls on different layers; a final marker closes the last group.  Only
+    our kernels and the markers are profiled (ncu replays each one with cold caches)."""
+    for name in PROBE_CONFIGS:
+        c = cfg_args(name, a)
+        c.sites = PROBE_CALLS
+        wl = Workload(lsg, torch, c, bounds_for(c), dtype, sites=PROBE_CALLS)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(1000)
+        wl.step()
+        torch.cuda.synchronize()
+        wl.free()
+    torch.cuda._sleep(1000)
+    torch.cuda.synchronize()
+
+
+def measure_traffic(a, timeout_s=300):
+    """DRAM bytes per launch of this build for every probe config (ncu counters; the probe's
+    timings are never used).  Returns {config: {...}} or {"error": ...}."""
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    log = os.path.join(ROOT, "gpurun_out", f"traffic_{os.getpid()}.csv")
+    os.makedirs(os.path.dirname(log), exist_ok=True)
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--csv", "--page", "raw",
+           "-k", "regex:sgmv|spin_kernel|dense_lora|tc_", "--log-file", log,
+           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--dtype", a.dtype]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except subprocess.TimeoutExpired:
+        return {"error": f"ncu pass timed out after {timeout_s} s"}
+    if r.returncode != 0 or not os.path.exists(log):
+        return {"error": f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-300:]}"}
+    rows = [row for row in csv.reader(io.StringIO(open(log).read())) if row]
+    hdr_i = next((i for i, row in enumerate(rows) if "Kernel Name" in row), None)
+    if hdr_i is None:
+        return {"error": "ncu csv without a header"}
+    hdr = rows[hdr_i]
+    kn, rd, wr = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    units = rows[hdr_i + 1] if hdr_i + 1 < len(rows) else []
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def val(row, i):
+        return float(row[i].replace(",", "")) * scale.get(units[i] if i < len(units) else "byte", 1)
+
+    groups, cur = [], None
+    for row in rows[hdr_i + 2:]:
+        if len(row) <= max(kn, rd, wr):
+            continue
+        if "spin_kernel" in row[kn]:
+            if cur is not None:
+                groups.append(cur)
+            cur = []
+        elif cur is not None:
+            cur.append((row[kn].split("(")[0].split("<")[0].strip(), val(row, rd), val(row, wr)))
+    out = {}
+    for name, kernels in zip(PROBE_CONFIGS, groups):
+        per_call = sum(k[1] + k[2] for k in kernels) / PROBE_CALLS
+        by_kernel = {}
+        for kname, b_r, b_w in kernels:
+            by_kernel.setdefault(kname, [0.0, 0])
+            by_kernel[kname][0] += b_r + b_w
+            by_kernel[kname][1] += 1
+        dominant = max(by_kernel.items(), key=lambda kv: kv[1][0]) if by_kernel else ("", [0.0, 1])
+        out[name] = {"dram_bytes_per_call": per_call, "kernels_per_call": len(kernels) / PROBE_CALLS,
+                     "dominant_kernel": dominant[0],
+                     "dominant_bytes_per_launch": dominant[1][0] / max(1, dominant[1][1])}
+    try:
+        os.remove(log)
+    except OSError:
+        pass
+    return out
+
+
+def library_hash():
+    p = os.path.join(ROOT, "paper_2310_18547_b200", "lib", "libsgmv_b200.so")
+    try:
+        return hashlib.sha256(open(p, "rb").read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference_arm(a)
         return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (rendezvous on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
     import torch
     import torch.distributed as dist
 
     import paper_2310_18547_b200 as lsg
 
+    dtype = torch.float16 if a.dtype == "fp16" else torch.bfloat16
+    if a.traffic_probe:
+        lsg.set_option(lsg.LSG_OPT_PDL, 0)
+        traffic_probe(lsg, torch, a, dtype)
+        return
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     # One process per GPU.  LSG_BENCH_BACKEND=gloo (test only) lets the N>1 code path
     # run with several ranks sharing one GPU; the product path is NCCL.
     dev = local % max(1, torch.cuda.device_count())
@@ -284,7 +638,6 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
-    dtype = torch.float16 if a.dtype == "fp16" else torch.bfloat16
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, a.cluster)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, a.tile_rows)
@@ -292,60 +645,24 @@ def main():
     lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, int(a.tc_split))
     lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, int(a.no_row_mode))
-    h, r, batch, sites = a.hidden, a.rank, a.batch, a.sites
-    # Request-partitioned weak scaling: the global batch is `batch` rows per GPU; the
-    # partitioner (lsg_partition_segments) hands every rank whole segments (or row
-    # ranges of dominant ones) and each rank runs its share on its own replica of
-    # the adapter pool -- no collective on the data path.
+    h, r, sites = a.hidden, a.rank, a.sites
+    # Request partitioning: the partitioner (lsg_partition_segments) hands every rank whole
+    # segments (or row ranges of dominant ones) and each rank runs its share on its own
+    # replica of the adapter pool -- no collective on the data path.
     from paper_2310_18547_b200.partition import rank_batches
-    gbounds = bounds_for(a, world)
+    gbounds = global_bounds(a, world)
     mine = rank_batches(np.array(gbounds, dtype=np.int32), h, h, r, world)[rank]
-    bounds = [int(v) for v in mine.seg_starts]
-    batch = mine.num_rows
-    nseg = len(bounds) - 1
-    # The serving engine knows its step's segment lengths: a decode-only step (no segment
-    # of >= 128 rows) skips the tensor-core pass (LSG_OPT_TC_MIN_ROWS, include/lsg_sgmv.h).
-    if max(np.diff(bounds), default=0) < 128:
-        lsg.set_option(lsg._lib.LSG_OPT_TC_MIN_ROWS, batch + 1)
-    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    nslots = max(a.slots, nseg)
-    pool = lsg.AdapterPool(nslots, sites, h, h, r, dtype)
-    pool.a.uniform_(-1, 1, generator=gen)
-    pool.b.uniform_(-1, 1, generator=gen)
-    xs = torch.empty(sites, batch, h, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen)
-    ys = torch.zeros(sites, batch, h, dtype=dtype, device="cuda")
-    seg_starts = torch.tensor(bounds, dtype=torch.int32, device="cuda")
-    # the batch's adapters are distinct slots spread over the pool
-    slots = torch.randperm(nslots, generator=torch.Generator().manual_seed(7 + rank))[:nseg].to(torch.int32)
-    seg_slot = slots.cuda()
-    row_slot = torch.repeat_interleave(slots, torch.tensor(np.diff(bounds))).to(torch.int32).cuda()
-    bytes_per_launch = alg_bytes(batch, nseg, h, r)
-    info = lsg.query_launch(pool, nseg, batch, lsg.KERNEL_BGMV if a.kernel == "bgmv" else lsg.KERNEL_FUSED)
-
-    def launch(s):
-        if a.kernel == "bgmv":
-            lsg.bgmv(ys[s], xs[s], pool, row_slot, s)
-        else:
-            lsg.sgmv(ys[s], xs[s], pool, seg_starts, seg_slot, s)
-
-    def step():
-        for s in range(sites):
-            launch(s)
-
+    wl = Workload(lsg, torch, a, [int(v) for v in mine.seg_starts], dtype, seed=1000 + rank, slot_seed=7 + rank)
+    info = wl.info()
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
     if a.profile:
         with torch.cuda.stream(stream):
             for _ in range(max(1, a.warmup)):
-                step()
+                wl.step()
         torch.cuda.synchronize()
         return
-    with torch.cuda.stream(stream):
-        step()  # eager warm-up (sets function attributes before capture)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        step()
+    graph = graph_of(torch, wl.step, stream)
     if a.profile_graph:
         with torch.cuda.stream(stream):
             graph.replay()
@@ -354,109 +671,82 @@ def main():
             torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         return
-    for _ in range(max(3, a.warmup)):
-        graph.replay()
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, a.warmup)):
+            graph.replay()
     torch.cuda.synchronize()
 
-    def timed(fn, k):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            for _ in range(k):
-                fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
-        return ms
-
+    # ---- the timed region: K step-graph replays, max over ranks ----------------------------
     with ClockSampler(dev) as clk:
-        ms = timed(graph.replay, a.steps)
+        ms = device_time_ms(torch, dist, world, stream, graph.replay, a.steps)
     ms_step = ms / a.steps
-    us_site = ms_step * 1e3 / sites  # per-rank device time per launch
-    value = ms * 1e3 / (a.steps * sites * world)  # whole job: max-over-ranks time / all sites
+    us_launch = ms_step * 1e3 / sites  # max-over-ranks device time per launch (per site)
+    # whole job: weak = time per 64-row site-equivalent (all ranks' rows), strong = per site
+    value = us_launch / world if a.scaling == "weak" else us_launch
+    peak, peak_src = peak_gbs()
+    bytes_per_launch = wl.bytes  # this rank's launch (rank 0 reports)
+    achieved = bytes_per_launch / (us_launch * 1e-6) / 1e9
+    extra = {"us_per_launch_max_rank": us_launch}
 
-    extra = {}
-    # isolated single-launch latency (no PDL overlap), L2 flushed between launches
-    lsg.set_option(lsg.LSG_OPT_PDL, 0)
-    flush = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2; hides launch latency
-    lat = []
-    for i in range(20):
-        with torch.cuda.stream(stream):
-            flush.zero_()  # same stream: evicts L2 and covers the host launch latency
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            launch(i)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        lat.append(e0.elapsed_time(e1) * 1e3)
-    extra["isolated_launch_us_median"] = statistics.median(lat)
-    graph_nopdl = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph_nopdl, stream=stream):
-        step()
-    graph_nopdl.replay()
-    ms_nopdl = timed(graph_nopdl.replay, max(3, a.steps // 2)) / max(3, a.steps // 2)
-    extra["us_per_launch_no_pdl"] = ms_nopdl * 1e3 / sites
-    lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
-    del flush
-    # Grouped launches (lsg_sgmv_multi): per layer q/k/v in one launch, o, gate/up in
-    # one launch, down -- 4 launches for the 7 sites, same bytes and results.
-    if a.kernel == "sgmv" and sites % SITES_PER_LAYER == 0:
-        groups = []
-        for l in range(sites // SITES_PER_LAYER):
-            b0 = l * SITES_PER_LAYER
-            groups += [[b0, b0 + 1, b0 + 2], [b0 + 3], [b0 + 4, b0 + 5], [b0 + 6]]
+    single = world == 1 and not a.no_extras
+    if single:
+        # isolated single-launch latency (no PDL overlap), L2 flushed between launches
+        flush = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2
+        lat = []
+        for i in range(20):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # same stream: evicts L2 and covers the host launch latency
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                wl.launch(i)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            lat.append(e0.elapsed_time(e1) * 1e3)
+        extra["isolated_launch_us_median"] = statistics.median(lat)
+        del flush
+        lsg.set_option(lsg.LSG_OPT_PDL, 0)
+        g_nopdl = graph_of(torch, wl.step, stream)
+        kn = max(3, a.steps // 2)
+        extra["us_per_launch_no_pdl"] = device_time_ms(torch, dist, 1, stream, g_nopdl.replay, kn) * 1e3 / (kn * sites)
+        lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
+        del g_nopdl
+        # Grouped launches (lsg_sgmv_multi): per layer q/k/v in one launch, o, gate/up in
+        # one launch, down -- 4 launches for the 7 sites, same bytes and results.
+        if a.kernel == "sgmv" and sites % SITES_PER_LAYER == 0:
+            groups = []
+            for l in range(sites // SITES_PER_LAYER):
+                b0 = l * SITES_PER_LAYER
+                groups += [[b0, b0 + 1, b0 + 2], [b0 + 3], [b0 + 4, b0 + 5], [b0 + 6]]
+            views = {s_: wl.pool.layer_view(s_) for g in groups if len(g) > 1 for s_ in g}  # before capture
 
-        views = {s_: pool.layer_view(s_) for g in groups if len(g) > 1 for s_ in g}  # before capture
+            def step_grouped():
+                for g in groups:
+                    if len(g) == 1:
+                        wl.launch(g[0])
+                    else:  # the sites' weights are layers g[i] of the one bench pool (same slots)
+                        lsg.sgmv_multi([wl.ys[s_] for s_ in g], [wl.xs[s_] for s_ in g], [views[s_] for s_ in g],
+                                       wl.seg_starts, wl.seg_slot, 0, tc_min_rows=wl.tc_min_rows)
 
-        def step_grouped():
-            for g in groups:
-                if len(g) == 1:
-                    launch(g[0])
-                else:  # the sites' weights are layers g[i] of the one bench pool (same slots)
-                    lsg.sgmv_multi([ys[s_] for s_ in g], [xs[s_] for s_ in g],
-                                   [views[s_] for s_ in g], seg_starts, seg_slot, 0)
-
-        with torch.cuda.stream(stream):
-            step_grouped()
-        torch.cuda.synchronize()
-        graph_g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph_g, stream=stream):
-            step_grouped()
-        with torch.cuda.stream(stream):
-            graph_g.replay()
-        kg = max(3, a.steps // 2)
-        extra["grouped_us_per_site"] = timed(graph_g.replay, kg) * 1e3 / (kg * sites * world)  # as `value`
-        extra["grouped_launches_per_layer"] = 4
-
+            g_grp = graph_of(torch, step_grouped, stream)
+            with torch.cuda.stream(stream):
+                g_grp.replay()
+            kg = max(3, a.steps // 2)
+            extra["grouped_us_per_site"] = device_time_ms(torch, dist, 1, stream, g_grp.replay, kg) * 1e3 / (kg * sites)
+            extra["grouped_launches_per_layer"] = 4
+            del g_grp
 
     # e2e through the public API: every step copies that step's activations in from
     # pinned host memory (one H2D of all sites' x) and its outputs back (one D2H of
     # all sites' y).  Steps are pipelined over two device buffer sets and three
     # streams (H2D / compute / D2H), the way a serving loop overlaps PCIe with the
-    # kernels; timed with CUDA events from the first H2D to the last D2H.
+    # kernels; timed with CUDA events from the first H2D to the last D2H, max over ranks.
     e2e = None
     if not a.no_e2e:
-        hx = torch.empty(sites, batch, h, dtype=dtype, pin_memory=True)
-        hx.copy_(xs.cpu())
-        hy = torch.empty(sites, batch, h, dtype=dtype, pin_memory=True)
-        bufs = [(xs, ys), (torch.empty_like(xs), torch.zeros_like(ys))]
-        graphs = [graph]
-        xs1, ys1 = bufs[1]
-        g1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g1, stream=stream):
-            for s_ in range(sites):
-                if a.kernel == "bgmv":
-                    lsg.bgmv(ys1[s_], xs1[s_], pool, row_slot, s_)
-                else:
-                    lsg.sgmv(ys1[s_], xs1[s_], pool, seg_starts, seg_slot, s_)
-        graphs.append(g1)
+        hx = torch.empty_like(wl.xs, device="cpu").pin_memory()
+        hx.copy_(wl.xs.cpu())
+        hy = torch.empty_like(wl.ys, device="cpu").pin_memory()
+        bufs = [(wl.xs, wl.ys), (torch.empty_like(wl.xs), torch.zeros_like(wl.ys))]
+        graphs = [graph, graph_of(torch, lambda: wl.step(bufs[1][1], bufs[1][0]), stream)]
         h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -498,54 +788,59 @@ def main():
             t = torch.tensor([ms_e2e], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = t.item()
-        e2e = {"value": ms_e2e * 1e3 / (ke * sites * world), "unit": "us/layer",
+        us_e2e = ms_e2e * 1e3 / (ke * sites)
+        e2e = {"value": us_e2e / world if a.scaling == "weak" else us_e2e, "unit": "us/layer",
                "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
                "d2h_bytes_per_step": int(hy.numel() * hy.element_size()),
                "how": "per step: one pinned H2D of all x, the step graph, one D2H of all y; "
                       "pipelined over 2 buffer sets (PCIe-bound)"}
-        del bufs, xs1, ys1
-
-    if a.sweep and rank == 0:
-        sweep(a, lsg, torch, dtype, stream)
+        del bufs, graphs, hx, hy
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs")
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md 6.65 TB/s)"
-    peak = peak or 6650.0
-    achieved = bytes_per_launch / (us_site * 1e-6) / 1e9
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        key = f"h{h}_r{r}_b{batch}_{a.popularity}_{a.dtype}"
-        traffic = prof.get(key)
-    except Exception:
-        pass
+    del graph
+    wl.free()
+    torch.cuda.empty_cache()
+    if single:
+        extra["configs"] = run_configs(lsg, torch, a, dtype, stream, peak)
+        extra["sweep"] = run_sweep(lsg, torch, a, dtype, stream, peak)
+    traffic, traffic_src = None, None
+    if single and not a.no_traffic:
+        t = measure_traffic(a)
+        extra["traffic_pass"] = {"library_sha16": library_hash(), **({"error": t["error"]} if "error" in t else {})}
+        if "error" not in t:
+            head = t.get("c2")
+            if head and a.preset in ("", "c2") and a.kernel == "sgmv" and not a.segments:
+                traffic = head["dominant_bytes_per_launch"]
+                traffic_src = f"ncu dram__bytes_read.sum + dram__bytes_write.sum of {head['dominant_kernel']}, " \
+                              f"mean of {PROBE_CALLS} cold launches, this build"
+            for c in extra.get("configs", []):
+                if c["config"] in t:
+                    c["traffic"] = t[c["config"]]["dram_bytes_per_call"]
+                    c["traffic_dominant_kernel"] = t[c["config"]]["dominant_kernel"]
+
     line = {
-        "metric": "SGMV us/layer (LoRA shrink+expand per projection site)",
+        "metric": METRIC,
         "value": value, "unit": "us/layer", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_step, "higher_is_better": False, "scaling": a.scaling, "vs_baseline": None,
         "dtype": a.dtype + " (fp32 accumulate)", "data": "synthetic (U[-1,1) adapters/activations, random init)",
         "config": {"workload": workload_name(a), "model": "Llama-2-7B LoRA sites (h x h)", "hidden": h, "rank": r,
-                   "batch_per_gpu": a.batch, "global_batch": a.batch * world, "segments": nseg,
-                   "global_segments": len(gbounds) - 1, "rank0_rows": batch,
-                   "popularity": a.popularity, "step": f"{sites} fused SGMV launches (7 sites x 32 layers), CUDA graph",
-                   "parallelism": f"request-partitioned x{world} (no collective)",
-                   "kernel": a.kernel, "pool_slots": nslots, "preset": a.preset or None,
+                   "batch_per_gpu": wl.rows, "global_batch": len(gbounds) and gbounds[-1],
+                   "segments": wl.nseg, "global_segments": len(gbounds) - 1, "rank0_rows": wl.rows,
+                   "popularity": a.popularity,
+                   "step": f"{sites} fused SGMV launches (7 sites x 32 layers), CUDA graph",
+                   "parallelism": f"request-partitioned x{world} (no collective), {a.scaling} scaling",
+                   "kernel": a.kernel, "pool_slots": wl.nslots, "preset": a.preset or None,
                    "l2": "inputs larger than L2: weights rotate over a "
-                         f"{pool.a.numel() * 2 * 2 / 2**30:.2f} GiB pool, x/y over {2 * xs.numel() * 2 / 2**20:.0f} MiB per step",
+                         f"{wl.nslots * sites * 2 * h * r * 2 / 2**30:.2f} GiB pool, x/y over "
+                         f"{2 * sites * max(wl.rows, 1) * h * 2 / 2**20:.0f} MiB per step",
                    "pdl": bool(a.pdl), "launch": info},
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_launch": bytes_per_launch, "flop_per_launch": alg_flop(batch, h, r)},
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                     "alg_bytes_per_launch": bytes_per_launch, "flop_per_launch": alg_flop(wl.rows, h, r)},
         "gpu_launches": a.steps * sites,
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -556,46 +851,6 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def sweep(a, lsg, torch, dtype, stream):
-    """Batch x popularity sweep at the configured shape (reported on stderr)."""
-    h, r = a.hidden, a.rank
-    for pop in ("distinct", "uniform", "skewed", "identical"):
-        for batch in (1, 2, 4, 8, 16, 32, 64):
-            bounds = segments(pop, batch)
-            nseg = len(bounds) - 1
-            L = 224
-            pool = lsg.AdapterPool(nseg, L, h, h, r, dtype)
-            pool.a.uniform_(-1, 1)
-            pool.b.uniform_(-1, 1)
-            xs = torch.empty(L, batch, h, dtype=dtype, device="cuda").uniform_(-1, 1)
-            ys = torch.zeros(L, batch, h, dtype=dtype, device="cuda")
-            ss = torch.tensor(bounds, dtype=torch.int32, device="cuda")
-            sl = torch.arange(nseg, dtype=torch.int32, device="cuda")
-            with torch.cuda.stream(stream):
-                for s in range(L):
-                    lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for s in range(L):
-                    lsg.sgmv(ys[s], xs[s], pool, ss, sl, s)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):  # replay on the stream the events are recorded on
-                for _ in range(3):
-                    g.replay()
-                e0.record(stream)
-                for _ in range(10):
-                    g.replay()
-                e1.record(stream)
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / (10 * L)
-            b = alg_bytes(batch, nseg, h, r)
-            sys.stderr.write(json.dumps({"sweep": True, "popularity": pop, "batch": batch, "segments": nseg,
-                                         "us_per_launch": us, "alg_bytes": b, "gbs": b / us / 1e3,
-                                         "launch": lsg.query_launch(pool, nseg, batch)}) + "\n")
-            del pool, xs, ys
 
 
 if __name__ == "__main__":

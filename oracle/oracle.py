@@ -36,10 +36,11 @@ _sz = C.c_size_t
 
 
 def build(ref: bool = True) -> None:
-    """Compile liboracle.so (and _ref/libref.so when /root/reference exists)."""
+    """Compile liboracle.so (and, when /root/reference exists, _ref/libref.so and the
+    reference's acceptance gate linked against the B200 drop-in, _ref/acceptance_b200)."""
     targets = ["all"]
     if ref and os.path.isdir("/root/reference/proj"):
-        targets.append("ref")
+        targets += ["ref", "integration"]
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
@@ -327,6 +328,31 @@ class Reference(_Lib):
         L.ref_roofline_csv.argtypes = [C.c_int, C.c_char_p, _sz]
         L.ref_roofline_csv.restype = _sz
         L.ref_plan_batch.argtypes = [_sz, _ip, _u8p, _i32p, C.POINTER(i64), _ip, P, _sp, _ip, P]
+        L.ref_batch_new.argtypes = [_dp, _sz, _sp, _sz, _dp, _dp, _sz, _sz]
+        L.ref_batch_new.restype = C.c_void_p
+        L.ref_batch_free.argtypes = [C.c_void_p]
+        L.ref_batch_bench.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int)]
+        L.ref_batch_bench.restype = C.c_double
+
+    def bench_batch(self, x, bounds, A, B, op="lora_addon", budget_s=1.0, max_iters=100000):
+        """Seconds per call of one reference operator on a Batch built ONCE outside the
+        timed loop (benchmarks/bench_sgmv.cpp:37-47).  op: lora_addon | sgmv_shrink |
+        sgmv_expand.  Returns (seconds_per_call, calls)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        bounds = np.ascontiguousarray(bounds, dtype=np.uint64)
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        b = self.lib.ref_batch_new(x, x.shape[1], bounds, len(bounds) - 1, A.reshape(-1), B.reshape(-1),
+                                   B.shape[1], B.shape[2])
+        if not b:
+            raise ValueError(self.last_error())
+        try:
+            n = C.c_int()
+            t = self.lib.ref_batch_bench(b, {"lora_addon": 0, "sgmv_shrink": 1, "sgmv_expand": 2}[op],
+                                         budget_s, max_iters, C.byref(n))
+        finally:
+            self.lib.ref_batch_free(b)
+        return t, n.value
 
     def last_error(self) -> str:
         return self.lib.ref_last_error().decode()

@@ -9,6 +9,7 @@
 //   * generate the golden fixtures in tests/golden/ (make_golden.py),
 //   * pin the C restatement in oracle/sgmv_oracle.c live (tests/test_oracle.py),
 //   * serve as bench.py's CPU baseline ("kind": "reference").
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -136,6 +137,41 @@ int ref_lora_loop_oracle(const double* x, size_t h_in, const size_t* bounds, siz
 int ref_gather_bmm_oracle(const double* x, size_t h_in, const size_t* bounds, size_t nseg,
                           const double* A, const double* B, size_t rank, size_t h_out, double* y) {
   return guarded([&] { from_matrix(gather_bmm_oracle(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)), y); });
+}
+
+// ---- prebuilt Batch timing (benchmarks/bench_sgmv.cpp:37-47 pattern) ----------
+// The reference's microbenchmark builds the Batch ONCE (make_batch, :20-35) and
+// times only lora_addon(batch) in the loop.  These entry points do the same:
+// ref_batch_new marshals the arrays into a Batch (outside any timing),
+// ref_batch_bench repeats one operator on it and returns seconds per call,
+// timed with steady_clock around the loop only (the result Matrix each call
+// returns is constructed inside the operator, as in the reference benchmark).
+void* ref_batch_new(const double* x, size_t h_in, const size_t* bounds, size_t nseg, const double* A,
+                    const double* B, size_t rank, size_t h_out) {
+  Batch* out = nullptr;
+  const int st = guarded([&] { out = new Batch(make_batch(x, h_in, bounds, nseg, A, B, rank, h_out)); });
+  return st == 0 ? out : nullptr;
+}
+void ref_batch_free(void* b) { delete static_cast<Batch*>(b); }
+
+// op: 0 lora_addon (shrink + expand), 1 sgmv_shrink, 2 sgmv_expand (on v = shrink(batch),
+// computed once beforehand).  Runs until budget_s has elapsed or max_iters calls.
+double ref_batch_bench(void* bp, int op, double budget_s, int max_iters, int* iters_out) {
+  const Batch& b = *static_cast<const Batch*>(bp);
+  static volatile double sink = 0.0;
+  Matrix v;
+  if (op == 2) v = sgmv_shrink(b);
+  int n = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  double el = 0.0;
+  do {
+    Matrix r = op == 0 ? lora_addon(b) : op == 1 ? sgmv_shrink(b) : sgmv_expand(v, b.segments, b.models);
+    if (!r.data().empty()) sink = sink + r.data()[0];
+    ++n;
+    el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  } while (el < budget_s && n < max_iters);
+  if (iters_out) *iters_out = n;
+  return el / n;
 }
 
 // ---- verify_sgmv (experiments.cpp:35-102) ------------------------------------

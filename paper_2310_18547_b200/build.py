@@ -1,9 +1,12 @@
 """In-tree build of the native libraries (no pip install, no JIT cache).
 
-  paper_2310_18547_b200/lib/libsgmv_b200.so     CUDA kernels + the C-ABI (include/lsg_sgmv.h)
-  paper_2310_18547_b200/lib/liblorasim_b200.so  C++ drop-in for lorasim::sgmv_* (host/), linked
-                                                against libsgmv_b200.so
-  paper_2310_18547_b200/lib/lorasim_b200        CLI (verify-sgmv, roofline)
+  paper_2310_18547_b200/lib/libsgmv_b200.so          CUDA kernels + the C-ABI (include/lsg_sgmv.h)
+  paper_2310_18547_b200/lib/liblorasim_sgmv_b200.so  C++ drop-in replacing exactly the reference's
+                                                     core/src/sgmv.cpp (lorasim::sgmv_* & co.),
+                                                     linked against libsgmv_b200.so
+  paper_2310_18547_b200/lib/liblorasim_b200.so       this repo's restatement of the rest of the
+                                                     SGMV tooling (workload, cost model, verify)
+  paper_2310_18547_b200/lib/lorasim_b200             CLI (verify-sgmv, roofline)
 
 Everything is compiled for sm_100a only: -gencode arch=compute_100a,code=sm_100a.
 Targets are rebuilt only when a source is newer than the output.
@@ -32,6 +35,8 @@ CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", f"-I{INCLUDE}",
              f"-I{os.path.join(HOST, 'include')}", f"-I{CUDA}/include"]
 
 SGMV_SO = os.path.join(LIB, "libsgmv_b200.so")
+DROPIN_SO = os.path.join(LIB, "liblorasim_sgmv_b200.so")
+DROPIN_SRCS = ("matrix.cpp", "sgmv_cuda.cpp")
 HOST_SO = os.path.join(LIB, "liblorasim_b200.so")
 CLI_BIN = os.path.join(LIB, "lorasim_b200")
 
@@ -71,15 +76,25 @@ def build(verbose: bool = False) -> None:
         _run([NVCC] + ARCH + ["-shared", "-o", SGMV_SO] + objs, verbose)
 
     host_hdrs = glob.glob(os.path.join(HOST, "include", "lorasim", "*.hpp")) + glob.glob(os.path.join(INCLUDE, "*.h"))
-    host_srcs = sorted(glob.glob(os.path.join(HOST, "src", "*.cpp")))
-    if host_srcs and _newer(HOST_SO, host_srcs + host_hdrs + [SGMV_SO]):
-        _run(["g++"] + CXX_FLAGS + ["-shared", "-o", HOST_SO] + host_srcs +
+    # The drop-in: exactly the symbols the reference's core/src/sgmv.cpp defines
+    # (matmul, max_abs_diff, Segments / LoraModel / Batch, the four operators and the two
+    # oracles), so a reference build that drops sgmv.cpp links it without duplicates.
+    dropin_srcs = [os.path.join(HOST, "src", f) for f in DROPIN_SRCS]
+    if _newer(DROPIN_SO, dropin_srcs + host_hdrs + [SGMV_SO]):
+        _run(["g++"] + CXX_FLAGS + ["-shared", "-o", DROPIN_SO] + dropin_srcs +
              [f"-L{LIB}", "-lsgmv_b200", f"-L{CUDA}/lib64", "-lcudart_static", "-lcublas", "-ldl", "-lrt", "-lpthread",
               "-Wl,-rpath,$ORIGIN", f"-Wl,-rpath,{CUDA}/lib64"], verbose)
+    # This repo's own restatement of the rest of the SGMV tooling (workload RNG, cost
+    # formulas, verify_sgmv / roofline_sweep) for the CLI and the C++ tests.
+    host_srcs = sorted(p for p in glob.glob(os.path.join(HOST, "src", "*.cpp")) if os.path.basename(p) not in DROPIN_SRCS)
+    if host_srcs and _newer(HOST_SO, host_srcs + host_hdrs + [DROPIN_SO]):
+        _run(["g++"] + CXX_FLAGS + ["-shared", "-o", HOST_SO] + host_srcs +
+             [f"-L{LIB}", "-llorasim_sgmv_b200", "-Wl,-rpath,$ORIGIN"], verbose)
     cli_src = os.path.join(HOST, "tools", "lorasim_b200_cli.cpp")
-    if os.path.exists(cli_src) and _newer(CLI_BIN, [cli_src, HOST_SO] + host_hdrs):
-        _run(["g++"] + CXX_FLAGS + ["-o", CLI_BIN, cli_src, f"-L{LIB}", "-llorasim_b200", "-lsgmv_b200",
-              f"-L{CUDA}/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread", "-Wl,-rpath,$ORIGIN", f"-Wl,-rpath,{CUDA}/lib64"], verbose)
+    if os.path.exists(cli_src) and _newer(CLI_BIN, [cli_src, HOST_SO, DROPIN_SO] + host_hdrs):
+        _run(["g++"] + CXX_FLAGS + ["-o", CLI_BIN, cli_src, f"-L{LIB}", "-llorasim_b200", "-llorasim_sgmv_b200",
+              "-lsgmv_b200", f"-L{CUDA}/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread", "-Wl,-rpath,$ORIGIN",
+              f"-Wl,-rpath,{CUDA}/lib64"], verbose)
 
 
 if __name__ == "__main__":

@@ -399,8 +399,12 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   // Multi-row tiles carry MT rows of compute per CTA: clusters above MT measured slower
   // (rank 64, c3: MT = 8 C = 16 27.3 us vs C = 8 16.0 us; MT = 4 C = 8 23.4 us vs C = 4 14.8 us).
   const int c_cap = pl.mt > 1 ? pl.mt : kMaxCluster;
-  for (int cand = 1; cand <= c_cap; ++cand) {
-    if (span % cand != 0 && cand != c_cap) continue;
+  // Launches with a shrink reduce over DSMEM with st.async, which needs a real
+  // cluster (compute-sanitizer memcheck: "Cluster needs to have at least 2 blocks"):
+  // at least 2 CTAs (a CTA without chunks only receives).  Expand-only launches: 1.
+  const int c_min = pl.mode == kExpand ? 1 : 2;
+  for (int cand = c_min; cand <= c_cap; ++cand) {
+    if (span % cand != 0 && cand != c_cap && cand != c_min) continue;
     if (smem_for(cand) > kSmemBudget) continue;
     if (c_small == 0) c_small = cand;
     const int64_t limit = (pl.tile_scan || cand <= 4) ? 256 : 148;
@@ -413,7 +417,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     if ((span % cand == 0 || cand == kMaxCluster) && smem_for(cand) <= kSmemBudget) c = cand;
   if (c == 0) c = kMaxCluster;
   const int forced = cur().force_cluster;
-  if (forced >= 1 && forced <= kMaxCluster && smem_for(forced) <= kSmemBudget) c = forced;
+  if (forced >= 1 && forced <= kMaxCluster && smem_for(std::max(forced, c_min)) <= kSmemBudget)
+    c = std::max(forced, c_min);
   pl.red_all = red_all_for(c);
   pl.alias_ab = alias_for(c);
   pl.cluster = c;

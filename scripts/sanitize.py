@@ -148,8 +148,26 @@ def generic_cases():
     check("generic odd shape", y, ref)
 
 
+def one_cases():
+    """python scripts/sanitize.py one <rank> <pop> <batch> <cluster> <tile_rows> <row_mode> <pdl>"""
+    r, pop, batch, c, mt, row, pdl = (int(v) for v in sys.argv[2:9])
+    bounds, _, _ = segments_for(pop, batch, 3)
+    pool, x, ss, sl, ref = problem(512, 256, r, bounds, 4)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
+    lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, mt)
+    lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, 1 - row)
+    lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+    y = torch.zeros(batch, 256, dtype=torch.float16, device=dev)
+    lsg.sgmv(y, x, pool, ss, sl, 0)
+    print("launch", lsg.query_launch(pool, len(bounds) - 1, batch))
+    check(f"one r{r} pop{pop} b{batch} c{c} mt{mt} row{row} pdl{pdl}", y, ref)
+
+
 def main():
     torch.cuda.set_device(0)
+    if sys.argv[1:2] == ["one"]:
+        one_cases()
+        sys.exit(1 if failures else 0)
     which = sys.argv[1:] or ["fused", "grouped", "tc", "dense", "builder", "generic"]
     for w in which:
         globals()[f"{w}_cases"]()

@@ -145,7 +145,23 @@ def main():
         p["plan"] = ref.plan_segments(p["lora"], p["done"], p["prompt"])
     with open(os.path.join(HERE, "plan_batch.json"), "w") as f:
         json.dump(plans, f, indent=0)
+    # --- the symbols core/src/sgmv.cpp defines (what the drop-in must replace, exactly) ---
+    with open(os.path.join(HERE, "sgmv_cpp_symbols.txt"), "w") as f:
+        f.write("\n".join(reference_sgmv_symbols()) + "\n")
     print("golden fixtures written to", HERE)
+
+
+def reference_sgmv_symbols():
+    """Demangled text symbols of the reference's core/src/sgmv.cpp, compiled here."""
+    import subprocess
+    import tempfile
+    ref = "/root/reference/proj"
+    with tempfile.TemporaryDirectory() as d:
+        obj = os.path.join(d, "sgmv.o")
+        subprocess.run(["g++", "-std=c++20", "-O2", "-c", f"-I{ref}/core/include", f"{ref}/core/src/sgmv.cpp",
+                        "-o", obj], check=True)
+        out = subprocess.run(["nm", "--defined-only", "-C", obj], capture_output=True, text=True, check=True).stdout
+    return sorted({line.split(" T ", 1)[1] for line in out.splitlines() if " T " in line})
 
 
 if __name__ == "__main__":

@@ -98,3 +98,17 @@ def test_launch_planning_is_host_only():
     t2 = _table(h_in=136)
     assert L.lsg_query_launch(C.byref(t2), 4, 4, _lib.KERNEL_FUSED, C.byref(info)) == 0
     assert info.path == 1  # h_in not a multiple of 128 -> generic kernel
+
+
+def test_dropin_library_defines_exactly_the_reference_sgmv_cpp_symbols():
+    """liblorasim_sgmv_b200.so replaces core/src/sgmv.cpp one for one: its lorasim:: text
+    symbols (outside this repo's lorasim::b200 extras) are exactly the ones sgmv.cpp defines
+    (tests/golden/sgmv_cpp_symbols.txt, from the reference compiled by make_golden.py), so a
+    reference build that drops sgmv.cpp links it with no duplicate and no missing symbol."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_2310_18547_b200", "lib", "liblorasim_sgmv_b200.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", "-C", so], capture_output=True, text=True, check=True).stdout
+    ours = sorted({ln.split(" T ", 1)[1] for ln in out.splitlines()
+                   if " T " in ln and "lorasim::" in ln and "lorasim::b200::" not in ln})
+    golden = [ln for ln in open(os.path.join(ROOT, "tests", "golden", "sgmv_cpp_symbols.txt")).read().splitlines() if ln]
+    assert ours == golden

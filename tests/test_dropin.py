@@ -18,12 +18,12 @@ CLI = os.path.join(LIB, "lorasim_b200")
 
 
 def _build():
-    deps = [SRC, os.path.join(LIB, "liblorasim_b200.so"), os.path.join(ORACLE, "liboracle.so")]
+    deps = [SRC, os.path.join(LIB, "liblorasim_b200.so"), os.path.join(LIB, "liblorasim_sgmv_b200.so"), os.path.join(ORACLE, "liboracle.so")]
     if os.path.exists(BIN) and all(os.path.getmtime(BIN) >= os.path.getmtime(d) for d in deps if os.path.exists(d)):
         return
     subprocess.run(["g++", "-std=c++20", "-O2", "-o", BIN, SRC,
                     f"-I{ROOT}/paper_2310_18547_b200/host/include", f"-I{ROOT}/include", f"-I{ORACLE}",
-                    "-I/usr/local/cuda/include", f"-L{LIB}", "-llorasim_b200", f"-L{ORACLE}", "-loracle",
+                    "-I/usr/local/cuda/include", f"-L{LIB}", "-llorasim_b200", "-llorasim_sgmv_b200", f"-L{ORACLE}", "-loracle",
                     f"-Wl,-rpath,{LIB}", f"-Wl,-rpath,{ORACLE}"], check=True)
 
 
@@ -61,3 +61,22 @@ def test_cli_verify_sgmv_contract_on_gpu():
     r = subprocess.run([CLI, "verify-sgmv", "--trials", "4", "--inject-fault"], capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 1, r.stdout + r.stderr
+
+
+ACCEPTANCE = os.path.join(ORACLE, "_ref", "acceptance_b200")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_with_b200_dropin():
+    """The reference's own release gate (proj/tests/acceptance/acceptance_main.cpp, compiled
+    unmodified with the reference's other core TUs by integration/CMakeLists.txt -- core/src/
+    sgmv.cpp removed, liblorasim_sgmv_b200.so linked instead) on the GPU: criteria 1-3 (the SGMV
+    path: verify_sgmv(1000, 42) three-way equivalence < 1e-10 in < 60 s, the intensity algebra,
+    the formula anchors) must PASS; the simulator criteria 4-8 run on the same binary too."""
+    assert os.path.exists(ACCEPTANCE), "oracle/_ref/acceptance_b200 missing: build() with /root/reference present"
+    r = subprocess.run([ACCEPTANCE, os.path.join(ORACLE, "_ref")], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    lines = r.stdout.splitlines()
+    for i in (1, 2, 3):
+        assert any(ln.startswith(f"PASS  {i}.") for ln in lines), r.stdout + r.stderr
+    assert r.returncode == 0 and "all 8 criteria passed" in r.stdout, r.stdout + r.stderr
