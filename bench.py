@@ -506,6 +506,89 @@ def run_sweep(lsg, torch, a, dtype, stream, peak):
     return out
 
 
+# ---- a real decode step: backbone projections + the LoRA adds -------------------------
+LLAMA7B_SITES = [("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
+                 ("gate", 4096, 11008), ("up", 4096, 11008), ("down", 11008, 4096)]
+
+
+def run_decode_step(lsg, torch, a, dtype, stream, layers=LAYERS, batch=64, rank=16, replays=10):
+    """One Llama-2-7B decode step at batch 64, Distinct adapters, on the real projection shapes
+    (q/k/v/o 4096->4096, gate/up 4096->11008, down 11008->4096): per site the backbone GEMM
+    y = x . W (cuBLAS through torch.matmul) then the LoRA add y += x . A . B (lsg_sgmv, PDL on).
+    Three CUDA graphs of the whole step -- backbone only, backbone + one LoRA launch per site,
+    backbone + grouped LoRA launches (q/k/v and gate/up each one lsg_sgmv_multi) -- give the
+    in-model LoRA overhead per site (the paper's +2 ms/token on A100)."""
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    bounds = segments("distinct", batch)
+    nseg = len(bounds) - 1
+    ss = torch.tensor(bounds, dtype=torch.int32, device="cuda")
+    sl = torch.arange(nseg, dtype=torch.int32, device="cuda")
+    pools, Ws, xs, ys = {}, [], [], []
+    for name, hi, ho in LLAMA7B_SITES:
+        pool = lsg.AdapterPool(nseg, layers, hi, ho, rank, dtype)
+        pool.a.uniform_(-0.05, 0.05, generator=gen)
+        pool.b.uniform_(-0.05, 0.05, generator=gen)
+        pools[name] = pool
+    views = {}
+    for layer in range(layers):
+        for name, hi, ho in LLAMA7B_SITES:
+            Ws.append(torch.empty(hi, ho, dtype=dtype, device="cuda").uniform_(-0.02, 0.02, generator=gen))
+            xs.append(torch.empty(batch, hi, dtype=dtype, device="cuda").uniform_(-1, 1, generator=gen))
+            ys.append(torch.empty(batch, ho, dtype=dtype, device="cuda"))
+            views[(layer, name)] = pools[name].layer_view(layer)
+    nsites = layers * len(LLAMA7B_SITES)
+    no_tc = batch + 1  # decode-only step: no tensor-core pass
+
+    def backbone(i):
+        torch.matmul(xs[i], Ws[i], out=ys[i])
+
+    def step_base():
+        for i in range(nsites):
+            backbone(i)
+
+    def step_lora():
+        for i in range(nsites):
+            layer, name = i // len(LLAMA7B_SITES), LLAMA7B_SITES[i % len(LLAMA7B_SITES)][0]
+            backbone(i)
+            lsg.sgmv(ys[i], xs[i], pools[name], ss, sl, layer, tc_min_rows=no_tc)
+
+    def step_grouped():
+        for layer in range(layers):
+            b0 = layer * len(LLAMA7B_SITES)
+            for i in range(b0, b0 + 7):
+                backbone(i)
+            for grp in ((0, 1, 2), (3,), (4, 5), (6,)):
+                idx = [b0 + g for g in grp]
+                if len(idx) == 1:
+                    name = LLAMA7B_SITES[grp[0]][0]
+                    lsg.sgmv(ys[idx[0]], xs[idx[0]], pools[name], ss, sl, layer, tc_min_rows=no_tc)
+                else:
+                    lsg.sgmv_multi([ys[i] for i in idx], [xs[i] for i in idx],
+                                   [views[(layer, LLAMA7B_SITES[g][0])] for g in grp], ss, sl, 0, tc_min_rows=no_tc)
+
+    out = {}
+    for key, fn in (("backbone_only", step_base), ("backbone_lora", step_lora), ("backbone_lora_grouped", step_grouped)):
+        g = graph_of(torch, fn, stream)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g.replay()
+        out[key + "_ms"] = device_time_ms(torch, None, 1, stream, g.replay, replays) / replays
+        del g
+    # shrink + expand algorithmic bytes per site (cost_model.cpp:13-19 for both halves, e = 2)
+    lora_bytes = sum((batch * (hi + 2 * rank + ho) + nseg * rank * (hi + ho)) * 2 for _, hi, ho in LLAMA7B_SITES) * layers
+    out.update({
+        "model": "Llama-2-7B, 32 layers, batch 64 decode, Distinct adapters, rank 16",
+        "lora_overhead_us_per_site": (out["backbone_lora_ms"] - out["backbone_only_ms"]) * 1e3 / nsites,
+        "lora_overhead_us_per_site_grouped": (out["backbone_lora_grouped_ms"] - out["backbone_only_ms"]) * 1e3 / nsites,
+        "lora_overhead_frac": out["backbone_lora_ms"] / out["backbone_only_ms"] - 1.0,
+        "lora_alg_bytes_per_step": lora_bytes,
+        "backbone_weight_bytes_per_step": sum(hi * ho * 2 for _, hi, ho in LLAMA7B_SITES) * layers,
+    })
+    del pools, Ws, xs, ys, views
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---- DRAM traffic of this build: one ncu pass over a probe run ------------------------
 PROBE_CONFIGS = ["c2"] + EXTRA_CONFIGS
 PROBE_CALLS = 3
@@ -806,6 +889,7 @@ def main():
     if single:
         extra["configs"] = run_configs(lsg, torch, a, dtype, stream, peak)
         extra["sweep"] = run_sweep(lsg, torch, a, dtype, stream, peak)
+        extra["decode_step"] = run_decode_step(lsg, torch, a, dtype, stream)
     traffic, traffic_src = None, None
     if single and not a.no_traffic:
         t = measure_traffic(a)

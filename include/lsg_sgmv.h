@@ -16,6 +16,8 @@
  *   lsg_build_segments <- lorasim::plan_batch grouping             core/src/simulator.cpp:267-309,
  *                         and the per-row gather loop              sgmv.cpp:195-203
  *   lsg_partition_segments <- Scheduler::place (request -> GPU)    core/src/scheduler.cpp:12-29
+ *   lsg_tp_sgmv / _nccl <- (no reference counterpart: TP is out of the reference's scope,
+ *                         SPEC.md:15) the 70B TP expand with its output all-gather
  *
  * Mapping from the reference's value types:
  *   Segments::boundaries() (sgmv.hpp:28, size_t)  -> seg_starts[n+1] int32, device memory
@@ -155,6 +157,41 @@ int lsg_sgmv_multi_ex(const lsg_sgmv_site* sites, int32_t num_sites, const int32
                       const int32_t* seg_slot, int32_t num_segments, int32_t total_rows, int32_t layer,
                       const lsg_call_opts* opts, lsg_stream_t stream);
 
+/* Tensor-parallel LoRA site (BASELINE configs[4], Llama-2-70B): y [s_n, h] is replicated on
+ * the `size` ranks of a TP group, A is replicated and B column-sharded (this rank's shard:
+ * columns [rank * h_out, (rank + 1) * h_out) of the full B, shard->h_out = h / size).
+ *
+ * lsg_tp_sgmv: the all-gather fused into the expand epilogue -- the kernel computes this
+ * rank's columns and stores every output vector straight into EVERY rank's y (peer memory
+ * over NVLink / NVSwitch: y_peer[d] are device pointers valid in this process, from CUDA
+ * IPC or peer access), then one tiny kernel raises this rank's flag at every rank
+ * (st.release.sys) and waits for every rank's flag here.  On stream completion every
+ * rank's y holds the full result.  flag_peer[d]: rank d's flag array of `size` u32
+ * (device, zero-initialised once); `epoch` must increase by one per call (never 0).
+ * Decode batches only (one-row tiles, no segment of >= 128 rows).
+ *
+ * lsg_tp_sgmv_nccl: the baseline -- this rank's columns in place, then ncclAllGather over
+ * `nccl_comm` (an ncclComm_t; libnccl.so.2 resolved at run time) through a workspace of
+ * lsg_tp_nccl_workspace_size() bytes, and the other ranks' columns copied into y.
+ *
+ * Each output element is computed by exactly one rank with the unsharded arithmetic, so
+ * every rank's y equals the single-GPU result bitwise.  The reference has no TP
+ * (SPEC.md:15); its closest analogue is request placement, scheduler.cpp:12-29. */
+typedef struct lsg_tp_group {
+  int32_t rank;
+  int32_t size;                 /* 1..8 */
+  void* const* y_peer;          /* host array [size] of device pointers: rank d's y base */
+  uint32_t* const* flag_peer;   /* host array [size] of device pointers: rank d's flags [size] */
+} lsg_tp_group;
+int lsg_tp_sgmv(const lsg_tp_group* group, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* shard,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                int32_t layer, uint32_t epoch, lsg_stream_t stream);
+size_t lsg_tp_nccl_workspace_size(int32_t total_rows, int32_t h_out_shard, int32_t tp_size);
+int lsg_tp_sgmv_nccl(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* shard,
+                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                     int32_t layer, int32_t tp_rank, int32_t tp_size, void* nccl_comm /* ncclComm_t */,
+                     void* workspace, size_t workspace_bytes, lsg_stream_t stream);
+
 /* Dense projection with the LoRA add in the GEMM epilogue (decode shapes):
  *   y[s_n, h_out] = x[s_n, h_in] . W[h_in, h_out] + x . A_slot(s) . B_slot(s)   (overwrite)
  * <- lorasim::dense_projection(const Batch&, const Matrix& w), sgmv.cpp:143-155.
@@ -255,12 +292,14 @@ typedef enum {
   LSG_OPT_NO_ROW_MODE = 7,     /* 1: one-row tiles use the segment-major decode (row split / tile scan)
                                   instead of one cluster per row with a segment search */
   LSG_OPT_NO_MULTIROW_TILES = 8, /* 1: rank 64 keeps one-row tiles even when rows share adapters */
-  LSG_OPT_TC_MIN_ROWS = 9       /* 0 (default 128): segments with at least this many rows take the
+  LSG_OPT_TC_MIN_ROWS = 9,      /* 0 (default 128): segments with at least this many rows take the
                                    tensor-core path.  A call with >= this many rows launches the
                                    tensor-core kernel even when no segment turns out that long (the
                                    host does not read segment lengths), which costs ~1 us per launch
                                    at 128-256 decode rows: an engine that knows a step has no prefill
                                    segment sets it above the batch size for that step. */
+  LSG_OPT_TC_LEGACY = 10        /* 1: rank-16 long segments on the first-generation fused tensor-core kernel
+                                   instead of the streamed one (A/B measurements) */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

@@ -16,7 +16,7 @@ LSG_OK, LSG_EINVAL, LSG_EUNSUPPORTED, LSG_ECUDA, LSG_ENODEVICE = 0, -1, -2, -3, 
 LSG_F16, LSG_BF16 = 0, 1
 (LSG_OPT_PDL, LSG_OPT_FORCE_CLUSTER, LSG_OPT_FORCE_GENERIC, LSG_OPT_FORCE_TILE_ROWS, LSG_OPT_NO_L2_STAGING,
  LSG_OPT_NO_TENSOR_CORES, LSG_OPT_TC_SPLIT, LSG_OPT_NO_ROW_MODE, LSG_OPT_NO_MULTIROW_TILES,
- LSG_OPT_TC_MIN_ROWS) = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9
+ LSG_OPT_TC_MIN_ROWS, LSG_OPT_TC_LEGACY) = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 KERNEL_FUSED, KERNEL_SHRINK, KERNEL_EXPAND, KERNEL_BGMV = 0, 1, 2, 3
 
 # Every symbol include/lsg_sgmv.h declares (checked by tests/test_abi.py).
@@ -26,6 +26,7 @@ EXPORTED = (
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
     "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments", "lsg_sgmv_multi",
     "lsg_dense_lora", "lsg_dense_lora_workspace_size", "lsg_sgmv_ex", "lsg_sgmv_multi_ex",
+    "lsg_tp_sgmv", "lsg_tp_sgmv_nccl", "lsg_tp_nccl_workspace_size",
 )
 
 
@@ -61,6 +62,13 @@ class CallOpts(C.Structure):
     """Mirror of ``lsg_call_opts`` (-1 = process default)."""
 
     _fields_ = [("pdl", C.c_int32), ("tc_min_rows", C.c_int32), ("no_tensor_cores", C.c_int32)]
+
+
+class TpGroup(C.Structure):
+    """Mirror of ``lsg_tp_group``."""
+
+    _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("y_peer", C.POINTER(C.c_void_p)),
+                ("flag_peer", C.POINTER(C.c_void_p))]
 
 
 class Piece(C.Structure):
@@ -115,6 +123,10 @@ def lib() -> C.CDLL:
         L.lsg_last_error.restype = C.c_char_p
         L.lsg_version.restype = C.c_int
         L.lsg_set_trace.argtypes = [vp, i32]
+        L.lsg_tp_sgmv.argtypes = [C.POINTER(TpGroup), i64, vp, i64, tp, vp, vp, i32, i32, i32, C.c_uint32, vp]
+        L.lsg_tp_nccl_workspace_size.argtypes = [i32, i32, i32]
+        L.lsg_tp_nccl_workspace_size.restype = C.c_size_t
+        L.lsg_tp_sgmv_nccl.argtypes = [vp, i64, vp, i64, tp, vp, vp, i32, i32, i32, i32, i32, vp, vp, C.c_size_t, vp]
         L.lsg_partition_segments.argtypes = [C.POINTER(i32), C.POINTER(i32), i32, i32, i32, i32, i32, i32, i32,
                                              C.POINTER(Piece), C.POINTER(i32)]
         _lib = L

@@ -115,3 +115,64 @@ int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st) {
 }
 
 }  // namespace lsg
+
+#include "sgmv_tc2.cuh"
+
+namespace lsg {
+
+// Streamed tensor-core kernel: a persistent grid of at most the co-resident clusters
+// (cudaOccupancyMaxActiveClusters, cached per device / cluster size / smem); clusters
+// loop over the long-segment tiles.
+template <typename T, int R>
+static int launch_tc_stream_inst(const Tc2Params& p, int C, uint32_t smem, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_stream_kernel<T, R>;
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc stream smem)");
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc stream cluster)");
+    mark_configured(configured);
+  }
+  static std::atomic<int> cached[64][2];  // [device][C == 16] -> co-resident clusters (0: not queried)
+  const int dev = current_device() & 63, ci = C == 16 ? 1 : 0;
+  int maxc = cached[dev][ci].load();
+  if (maxc == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(C), 1024, 1);
+    cfg.blockDim = dim3(kT2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = static_cast<unsigned>(C);
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(kern), &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 148 / C;
+    }
+    maxc = n;
+    cached[dev][ci].store(n);
+  }
+  const int clusters = std::max(1, std::min(tiles, maxc));
+  const dim3 grid(static_cast<unsigned>(C), static_cast<unsigned>(clusters), 1);
+  const cudaError_t e = launch_ex(kern, grid, dim3(kT2Threads), static_cast<int>(smem), C, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_stream_kernel launch");
+}
+
+int launch_tc_stream(int dtype, int rank, const Tc2Params& p, int C, uint32_t smem, int tiles, cudaStream_t st) {
+#define LSG_TC2_R(T)                                                                       \
+  switch (rank) {                                                                          \
+    case 16: return launch_tc_stream_inst<T, 16>(p, C, smem, tiles, st);                   \
+    case 32: return launch_tc_stream_inst<T, 32>(p, C, smem, tiles, st);                   \
+    default: return fail(LSG_EUNSUPPORTED, "streamed tensor-core kernel: rank not in {16,32}"); \
+  }
+  if (dtype == LSG_F16) LSG_TC2_R(__half)
+  LSG_TC2_R(__nv_bfloat16)
+#undef LSG_TC2_R
+}
+
+}  // namespace lsg

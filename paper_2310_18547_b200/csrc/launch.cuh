@@ -33,6 +33,7 @@ struct Plan {
   int tile_scan = 0;
   int row_mode = 0;  // one cluster per row, segment found by search (one-row tiles, no long-segment skip)
   int multi = 0;     // grouped launch over several sites (row mode, fused)
+  int tp = 0;        // tensor-parallel launch: row mode, output stored into every rank's y
 };
 
 // Function attributes (max dynamic smem, non-portable clusters) are per device:
@@ -67,6 +68,8 @@ int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int t
 int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st);
 struct TcFusedParams;
 int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st);
+struct Tc2Params;
+int launch_tc_stream(int dtype, int rank, const Tc2Params& p, int C, uint32_t smem, int tiles, cudaStream_t st);
 struct DenseLoraParams;
 int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st);
 
@@ -144,10 +147,15 @@ int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
       if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemRowMulti>(p, pl, st);
       return fail(LSG_EINVAL, "lsg: grouped launches are fused-only");
     }
+    if (pl.tp) {
+      if constexpr (MODE == kFused) return launch_fast_inst<T, R, 1, MODE, kItemRowTp>(p, pl, st);
+      return fail(LSG_EINVAL, "lsg: tensor-parallel launches are fused-only");
+    }
     if (pl.row_mode) return launch_fast_inst<T, R, 1, MODE, kItemRow>(p, pl, st);
     return pl.tile_scan ? launch_fast_inst<T, R, 1, MODE, kItemTileScan>(p, pl, st)
                         : launch_fast_inst<T, R, 1, MODE, kItemRowSplit>(p, pl, st);
   }
+  if (pl.multi || pl.tp) return fail(LSG_EINVAL, "lsg: grouped / tensor-parallel launches need one-row tiles");
   if (pl.mt == 4) {  // rank-64 fused launches with shared adapters (tile scan)
     if constexpr (R == 64 && MODE == kFused) return launch_fast_inst<T, R, 4, MODE, kItemTileScan>(p, pl, st);
     return fail(LSG_EINVAL, "lsg: 4-row tiles are rank-64 fused only");

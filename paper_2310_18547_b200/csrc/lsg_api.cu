@@ -18,10 +18,13 @@
 
 #include <mutex>
 
+#include <dlfcn.h>
+
 #include "../../include/lsg_sgmv.h"
 #include "launch.cuh"
 #include "segment_builder.cuh"
 #include "sgmv_tc.cuh"
+#include "sgmv_tc2.cuh"
 
 namespace lsg {
 
@@ -35,6 +38,28 @@ int fail(int status, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string(what) + ": " + cudaGetErrorString(e);
   return LSG_ECUDA;
+}
+
+// Tensor-parallel completion flags: raise this rank's flag at every rank (release,
+// system scope: the SGMV kernel's peer stores before it in stream order are visible
+// first), then wait until every rank's flag at this rank carries the epoch.
+struct TpFlagParams {
+  uint32_t* peer_flag[8];
+  uint32_t* my_flag;
+  int32_t rank, size;
+  uint32_t epoch;
+};
+__global__ void tp_flags_kernel(const __grid_constant__ TpFlagParams p) {
+  const int d = threadIdx.x;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (d < p.size)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flag[d] + p.rank), "r"(p.epoch) : "memory");
+  if (d < p.size) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.my_flag + d) : "memory");
+    } while (static_cast<int32_t>(v - p.epoch) < 0);
+  }
 }
 
 namespace {
@@ -57,16 +82,17 @@ std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
 std::atomic<int> g_opt_no_rank64_tiles{0};
 std::atomic<int> g_opt_tc_min_rows{0};  // rows from which a segment takes the tensor-core path (0 = default)
+std::atomic<int> g_opt_tc_legacy{0};    // 1: rank-16 long segments on the first-generation fused kernel
 
 struct Opts {
   int pdl, force_cluster, force_generic, force_tile_rows, no_alias, no_tile_scan, no_tc, tc_split, no_row_mode,
-      no_rank64_tiles, tc_min_rows;
+      no_rank64_tiles, tc_min_rows, tc_legacy;
 };
 
 Opts snapshot(const lsg_call_opts* c) {
   Opts o{g_opt_pdl.load(),     g_opt_force_cluster.load(), g_opt_force_generic.load(), g_opt_force_tile_rows.load(),
          g_opt_no_alias.load(), g_opt_no_tile_scan.load(), g_opt_no_tc.load(),        g_opt_tc_split.load(),
-         g_opt_no_row_mode.load(), g_opt_no_rank64_tiles.load(), g_opt_tc_min_rows.load()};
+         g_opt_no_row_mode.load(), g_opt_no_rank64_tiles.load(), g_opt_tc_min_rows.load(), g_opt_tc_legacy.load()};
   if (c != nullptr) {
     if (c->pdl >= 0) o.pdl = c->pdl ? 1 : 0;
     if (c->tc_min_rows >= 0) o.tc_min_rows = c->tc_min_rows;
@@ -138,8 +164,10 @@ int tc_min_rows() {
   return x > 0 ? x : kTcMinRows;
 }
 
+bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
-  if (tc_fused_c(t, nullptr) > 0 && !cur().tc_split) return 0;  // the fused kernel keeps v on chip
+  // the fused kernels keep v on chip
+  if (!cur().tc_split && (tc2_choose(t, nullptr) || tc_fused_c(t, nullptr) > 0)) return 0;
   return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
@@ -190,9 +218,41 @@ struct LongPlan {
   TcShrinkParams sp;
   TcExpandParams ep;
   TcFusedParams fp;
+  Tc2Params tp;
   int nq = 0, tiles = 0;
-  int fused_c = 0;  // > 0: one fused tensor-core launch with clusters of fused_c CTAs
+  int fused_c = 0;   // > 0: one first-generation fused tensor-core launch, clusters of fused_c CTAs
+  int stream_c = 0;  // > 0: one streamed tensor-core launch (sgmv_tc2.cuh), clusters of stream_c CTAs
+  uint32_t stream_smem = 0;
 };
+
+// Streamed tensor-core kernel plan (ranks 16 / 32): the smallest cluster C in {8, 16}
+// whose per-CTA share (its K boxes, at most two 256-column expand chunks) fits shared
+// memory with a ring of >= 4 boxes when the ring also stages y chunk 1.  Depends on
+// the shape only (the canonical K split of these rows).
+struct Tc2Choice {
+  int C = 0, kbs = 0, chs = 0, stages = 0;
+  uint32_t smem = 0;
+};
+bool tc2_choose(const lsg_weight_table* t, Tc2Choice* out) {
+  if ((t->rank != 16 && t->rank != 32) || t->h_in % kTcKB != 0 || t->h_out % kTcNT != 0 ||
+      t->a_layer_stride % 8 != 0 || t->b_layer_stride % 8 != 0)
+    return false;
+  const int nkb = t->h_in / kTcKB, nch = t->h_out / kTcNT;
+  for (int C : {8, 16}) {
+    if (nkb < C) continue;
+    const int kbs = (nkb + C - 1) / C, chs = (nch + C - 1) / C;
+    if (chs > 2) continue;
+    const int smin = chs == 2 ? 4 : 1;
+    for (int stages = std::max(smin, std::min(kbs, kT2MaxStages)); stages >= smin; --stages) {
+      const Tc2Layout L = tc2_layout(t->rank, kbs, chs, stages);
+      if (L.total <= static_cast<uint32_t>(kSmemBudget)) {
+        if (out) *out = Tc2Choice{C, kbs, chs, stages, L.total};
+        return true;
+      }
+    }
+  }
+  return false;
+}
 
 // Cluster size of the fused tensor-core kernel for this shape (0: not applicable).
 // Rank 16 only; every CTA expands at most two 256-column chunks.
@@ -218,6 +278,38 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   const int nq = tc_nq(tbl);
   if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
+  Tc2Choice ch;
+  if (!cur().tc_split && !(cur().tc_legacy && tbl->rank == 16) && tc2_choose(tbl, &ch)) {
+    Tc2Params& tp = lp.tp;
+    tp = Tc2Params{};
+    if (!encode_rows_map(&tp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx) ||
+        !encode_rows_map(&tp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
+      return false;
+    lp.stream_c = ch.C;
+    lp.stream_smem = ch.smem;
+    lp.tiles = tc_tile_bound(s_n, n_seg);
+    tp.y = y;
+    tp.ldy = ldy;
+    tp.a_ptr = tbl->a_ptr;
+    tp.b_ptr = tbl->b_ptr;
+    tp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+    tp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+    tp.seg_starts = seg_starts;
+    tp.seg_slot = seg_slot;
+    tp.n_seg = n_seg;
+    tp.s_n = s_n;
+    tp.num_slots = tbl->num_slots;
+    tp.h_in = tbl->h_in;
+    tp.h_out = tbl->h_out;
+    tp.kbs_max = ch.kbs;
+    tp.chs_max = ch.chs;
+    tp.stages = ch.stages;
+    tp.min_rows = tc_min_rows();
+    tp.tiles = lp.tiles;
+    tp.trace = g_trace;
+    tp.trace_ctas = g_trace_ctas;
+    return true;
+  }
   int compact = 0;
   const int fc = cur().tc_split ? 0 : tc_fused_c(tbl, &compact);
   if (fc > 0) {
@@ -291,23 +383,21 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
 }
 
 int launch_long_segments(const LongPlan& lp, int dtype, int rank, cudaStream_t cs) {
+  if (lp.stream_c > 0) return launch_tc_stream(dtype, rank, lp.tp, lp.stream_c, lp.stream_smem, lp.tiles, cs);
   if (lp.fused_c > 0) return launch_tc_fused(dtype, lp.fp, lp.fused_c, lp.tiles, cs);
   const int st = launch_tc_shrink(dtype, rank, lp.sp, lp.nq, lp.tiles, cs);
   if (st != LSG_OK) return st;
   return launch_tc_expand(dtype, rank, lp.ep, lp.tiles, cs);
 }
 
-int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
 enum Kernel { kKFused = 0, kKShrink = 1, kKExpand = 2, kKBgmv = 3 };
 
+
+// Destinations of a tensor-parallel launch: every rank's y, at this rank's columns.
+struct TpDest {
+  int n;
+  void* y[kMaxSites];
+};
 
 int validate_table(const lsg_weight_table* t) {
   if (t == nullptr) return fail(LSG_EINVAL, "lsg: weight table is NULL");
@@ -433,7 +523,7 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
         const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
         const int32_t* row_slot, int32_t n_seg, int32_t s_n, int32_t layer, lsg_stream_t stream,
         void* ws = nullptr, size_t ws_bytes = 0, bool library_ws = false, const lsg_sgmv_site* sites = nullptr,
-        int n_sites = 0) {
+        int n_sites = 0, const TpDest* tp = nullptr) {
   int st = validate_table(tbl);
   if (st != LSG_OK) return st;
   if (s_n < 0) return fail(LSG_EINVAL, "lsg: total_rows must be >= 0");
@@ -512,6 +602,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
     pl.multi = 1;
     pl.clusters = n_sites * s_n;
   }
+  if (tp != nullptr) {  // tensor-parallel expand: the grouped item mode's store into every rank's y
+    if (!pl.row_mode || pl.mt != 1 || skip_long || kernel != kKFused)
+      return fail(LSG_EUNSUPPORTED, "lsg_tp_sgmv: decode batches only (one-row tiles, no long segments)");
+    pl.tp = 1;
+  }
   // Launches with one work item per cluster put the item count in gridDim.y (max
   // 65535): above that, clusters loop over tiles (tile-scan decode) instead.
   if (!pl.tile_scan && !pl.multi && kernel != kKBgmv && pl.clusters > kMaxGridY) {
@@ -560,6 +655,10 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   for (int i = 0; i < p.n_sites; ++i)
     p.sites[i] = SiteParams{sites[i].y, sites[i].x, sites[i].tbl->a_ptr, sites[i].tbl->b_ptr, sites[i].ldx,
                             sites[i].ldy};
+  if (tp != nullptr) {
+    p.n_sites = tp->n;
+    for (int i = 0; i < tp->n; ++i) p.sites[i] = SiteParams{tp->y[i], x, tbl->a_ptr, tbl->b_ptr, ldx, ldy};
+  }
 #ifdef LSG_INSTRUMENT
   // experiment switches (instrumented builds only; production kernels compile them out)
   static const int exp_flags = [] {
@@ -675,6 +774,97 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
   return lsg_sgmv_multi_ex(sites, num_sites, seg_starts, seg_slot, num_segments, total_rows, layer, nullptr, stream);
 }
 
+int lsg_tp_sgmv(const lsg_tp_group* g, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* shard,
+                const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                int32_t layer, uint32_t epoch, lsg_stream_t stream) {
+  lsg_call_opts o{-1, -1, 1};  // decode batches: long segments would need the tensor-core kernels
+  CallScope scope(&o);
+  if (g == nullptr || g->size < 1 || g->size > kMaxSites || g->rank < 0 || g->rank >= g->size ||
+      g->y_peer == nullptr || g->flag_peer == nullptr)
+    return fail(LSG_EINVAL, "lsg_tp_sgmv: bad group (size 1..8, rank < size, peer arrays)");
+  int st = validate_table(shard);
+  if (st != LSG_OK) return st;
+  if (epoch == 0) return fail(LSG_EINVAL, "lsg_tp_sgmv: epoch must be non-zero (flags start at 0)");
+  TpDest d{};
+  d.n = g->size;
+  const int64_t c0 = static_cast<int64_t>(g->rank) * shard->h_out;  // this rank's columns
+  for (int r = 0; r < g->size; ++r) {
+    if (g->y_peer[r] == nullptr || g->flag_peer[r] == nullptr) return fail(LSG_EINVAL, "lsg_tp_sgmv: NULL peer buffer");
+    d.y[r] = static_cast<char*>(g->y_peer[r]) + c0 * 2;
+  }
+  if (ldy < static_cast<int64_t>(g->size) * shard->h_out)
+    return fail(LSG_EINVAL, "lsg_tp_sgmv: ldy < size * h_out (y rows hold every rank's columns)");
+  st = run(kKFused, d.y[g->rank], ldy, x, ldx, nullptr, nullptr, shard, seg_starts, seg_slot, nullptr, num_segments,
+           total_rows, layer, stream, nullptr, 0, false, nullptr, 0, &d);
+  if (st != LSG_OK) return st;
+  // every rank's stores are complete (stream order) -> raise my flag at every rank, then
+  // wait for every rank's flag at mine (epoch-stamped, no reset needed between steps)
+  TpFlagParams f{};
+  f.rank = g->rank;
+  f.size = g->size;
+  f.epoch = epoch;
+  f.my_flag = g->flag_peer[g->rank];
+  for (int r = 0; r < g->size; ++r) f.peer_flag[r] = g->flag_peer[r];
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  tp_flags_kernel<<<1, 32, 0, cs>>>(f);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "tp_flags_kernel launch");
+}
+
+size_t lsg_tp_nccl_workspace_size(int32_t total_rows, int32_t h_out_shard, int32_t tp_size) {
+  if (total_rows < 0 || h_out_shard < 0 || tp_size < 1) return 0;
+  return static_cast<size_t>(tp_size + 1) * total_rows * h_out_shard * 2;
+}
+
+int lsg_tp_sgmv_nccl(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* shard,
+                     const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
+                     int32_t layer, int32_t tp_rank, int32_t tp_size, void* nccl_comm, void* workspace,
+                     size_t workspace_bytes, lsg_stream_t stream) {
+  CallScope scope(nullptr);
+  int st = validate_table(shard);
+  if (st != LSG_OK) return st;
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size || nccl_comm == nullptr || y == nullptr)
+    return fail(LSG_EINVAL, "lsg_tp_sgmv_nccl: bad rank / size / communicator");
+  const int64_t w = shard->h_out;
+  if (ldy < tp_size * w) return fail(LSG_EINVAL, "lsg_tp_sgmv_nccl: ldy < size * h_out");
+  if (total_rows < 0) return fail(LSG_EINVAL, "lsg_tp_sgmv_nccl: total_rows < 0");
+  if (total_rows == 0) return LSG_OK;
+  if (workspace == nullptr || workspace_bytes < lsg_tp_nccl_workspace_size(total_rows, static_cast<int32_t>(w), tp_size))
+    return fail(LSG_EINVAL, "lsg_tp_sgmv_nccl: workspace too small (lsg_tp_nccl_workspace_size)");
+  using AllGatherFn = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+  static AllGatherFn allgather = [] {
+    void* f = dlsym(RTLD_DEFAULT, "ncclAllGather");
+    if (f == nullptr) {
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (h != nullptr) f = dlsym(h, "ncclAllGather");
+    }
+    return reinterpret_cast<AllGatherFn>(f);
+  }();
+  if (allgather == nullptr) return fail(LSG_EUNSUPPORTED, "lsg_tp_sgmv_nccl: libnccl.so.2 not found");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  char* yb = static_cast<char*>(y);
+  const int64_t c0 = tp_rank * w;
+  // 1. this rank's column slice of y += x . A . B_shard (in place, strided)
+  st = run(kKFused, yb + c0 * 2, ldy, x, ldx, nullptr, nullptr, shard, seg_starts, seg_slot, nullptr, num_segments,
+           total_rows, layer, stream);
+  if (st != LSG_OK) return st;
+  // 2. slice -> contiguous send buffer, 3. all-gather, 4. every other rank's slice -> y
+  char* send = static_cast<char*>(workspace);
+  char* recv = send + static_cast<size_t>(total_rows) * w * 2;
+  cudaError_t e = cudaMemcpy2DAsync(send, w * 2, yb + c0 * 2, ldy * 2, w * 2, total_rows, cudaMemcpyDeviceToDevice, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "lsg_tp_sgmv_nccl: stage copy");
+  const int nccl_type = shard->dtype == LSG_F16 ? 6 /* ncclFloat16 */ : 9 /* ncclBfloat16 */;
+  const int nr = allgather(send, recv, static_cast<size_t>(total_rows) * w, nccl_type, nccl_comm, cs);
+  if (nr != 0) return fail(LSG_ECUDA, "lsg_tp_sgmv_nccl: ncclAllGather failed (" + std::to_string(nr) + ")");
+  for (int r = 0; r < tp_size; ++r) {
+    if (r == tp_rank) continue;
+    e = cudaMemcpy2DAsync(yb + r * w * 2, ldy * 2, recv + static_cast<size_t>(r) * total_rows * w * 2, w * 2, w * 2,
+                          total_rows, cudaMemcpyDeviceToDevice, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "lsg_tp_sgmv_nccl: gather copy");
+  }
+  return LSG_OK;
+}
+
 size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
   CallScope scope(nullptr);
   if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
@@ -786,6 +976,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       if (value < 0) return fail(LSG_EINVAL, "lsg: tensor-core row threshold must be >= 0");
       g_opt_tc_min_rows = value;
       return LSG_OK;
+    case LSG_OPT_TC_LEGACY: g_opt_tc_legacy = value ? 1 : 0; return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -802,6 +993,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_NO_ROW_MODE: return cur().no_row_mode;
     case LSG_OPT_NO_MULTIROW_TILES: return cur().no_rank64_tiles;
     case LSG_OPT_TC_MIN_ROWS: return g_opt_tc_min_rows.load();
+    case LSG_OPT_TC_LEGACY: return g_opt_tc_legacy.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -181,7 +181,11 @@ __device__ __forceinline__ float ordered_sum(const float* v, int stride, int n) 
 
 // How a cluster finds its work item (compile-time, so each instantiation carries
 // only its own decode path -- see the code-size note at LSG_INSTRUMENT).
-enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3, kItemRowMulti = 4 };
+// kItemRowTp: row mode whose expand stores every output vector into each of the
+// n_sites destinations sites[d].y (the TP group's y buffers, peer memory over NVLink)
+// -- the all-gather of the tensor-parallel expand fused into the epilogue.
+enum ItemMode : int { kItemRowSplit = 0, kItemTileScan = 1, kItemBgmv = 2, kItemRow = 3, kItemRowMulti = 4,
+                      kItemRowTp = 5 };
 
 template <typename T, int R, int MT, int MODE, int ITEM>
 __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
   int64_t s_ldx = p.ldx, s_ldy = p.ldy;
   for (int item = blockIdx.y;; item += gridDim.y, wphase ^= 1u) {
     int slot, seg_begin, seg_end, first_tile, tile_step;
-    if constexpr (ITEM == kItemBgmv || ITEM == kItemRow || ITEM == kItemRowMulti) {
+    if constexpr (ITEM == kItemBgmv || ITEM == kItemRow || ITEM == kItemRowMulti || ITEM == kItemRowTp) {
       int row = item;
       if constexpr (ITEM == kItemRowMulti) {  // cluster y = site * s_n + row
         const int g = item / p.s_n;
@@ -774,8 +778,15 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
             Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = acc[j] + yo[j];
-            st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
-                         Cvt<T>::pack8(acc));
+            if constexpr (ITEM == kItemRowTp) {  // every rank's y (own one included)
+              const uint4 out = Cvt<T>::pack8(acc);
+              for (int d = 0; d < p.n_sites; ++d)
+                st_global_v4(static_cast<T*>(p.sites[d].y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
+                             out);
+            } else {
+              st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
+                           Cvt<T>::pack8(acc));
+            }
           }
         }
       }

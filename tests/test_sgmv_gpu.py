@@ -36,7 +36,7 @@ def _reset_options(lsg):
     yield
     for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
                 lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE,
-                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES):
+                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES, lsg._lib.LSG_OPT_TC_LEGACY):
         lsg.set_option(opt, 0)
 
 
@@ -790,3 +790,86 @@ def test_grid_limit_many_rows(lsg):
     ref = np.stack([xs[i] @ pool.a[segs[i], 0].double().cpu().numpy() @ pool.b[segs[i], 0].double().cpu().numpy()
                     for i in range(len(pick))])
     assert row_norm_err(y[torch.tensor(pick, device="cuda")].double().cpu().numpy(), ref) <= tol(torch.float16)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", [(4096, 4096, 16), (4096, 4096, 32), (8192, 8192, 16), (5120, 5120, 16),
+                                   (1024, 1024, 32)])
+def test_streamed_tc_kernel_many_tiles_and_legacy_agree(lsg, dtype, shape):
+    """The streamed tensor-core kernel (sgmv_tc2.cuh) with more tiles than co-resident clusters
+    (persistent tile loop), partial last tiles, a no-adapter long segment and decode rows in
+    between: oracle tolerance, run-to-run bitwise, and within tolerance of the first-generation
+    fused kernel (rank 16) / the two-kernel form."""
+    h_in, h_out, r = shape
+    lens = [300, 1, 129, 7, 1000, 2, 260, 128, 3, 700, 1, 450]
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 811)
+    y0 = oracle().rng(812).fill_pm1(int(bounds[-1]) * h_out).reshape(-1, h_out)
+    slots = list(range(len(lens)))
+    slots[6] = -1  # a long segment without an adapter: rows untouched
+    p = Problem(lsg, x, A, B, bounds, dtype, slots=slots, num_slots=len(lens), y0=y0)
+    got = p.run()
+    ref = p.reference()
+    assert row_norm_err(got.double().cpu().numpy(), ref) <= tol(dtype)
+    assert torch.equal(got[int(bounds[6]):int(bounds[7])], p.y0[int(bounds[6]):int(bounds[7])])
+    assert torch.equal(p.run(), got)
+    other = (lsg._lib.LSG_OPT_TC_LEGACY if r == 16 else lsg._lib.LSG_OPT_TC_SPLIT)
+    lsg.set_option(other, 1)
+    try:
+        alt = p.run()
+    finally:
+        lsg.set_option(other, 0)
+    assert row_norm_err(alt.double().cpu().numpy(), ref) <= tol(dtype)
+    for s, n in enumerate(lens):  # decode rows: the CUDA-core kernel in both runs
+        a, b = int(bounds[s]), int(bounds[s + 1])
+        if n < 128:
+            assert torch.equal(alt[a:b], got[a:b]), s
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tp_p2p_fused_allgather_every_rank_bitwise(lsg, tp):
+    """lsg_tp_sgmv (configs[4], 70B TP): every rank's kernel stores its column slice into EVERY
+    rank's y, then the flag exchange.  The tp ranks are emulated on one GPU, each on its own
+    stream, all in flight together (the flag wait needs every peer): afterwards each rank's y
+    equals the unsharded single-GPU result bit for bit -- over two consecutive steps (epochs)."""
+    from paper_2310_18547_b200 import tp as tpmod
+    h, r = 8192, 16
+    bounds, _, _ = segments_for(DISTINCT, 32, 5)
+    x, A, B = random_problem(h, h, r, bounds, 6)
+    y0 = oracle().rng(7).fill_pm1(32 * h).reshape(32, h)
+    p = Problem(lsg, x, A, B, bounds, torch.float16, y0=y0)
+    base = p.run()
+    base2 = base.clone()
+    lsg.sgmv(base2, p.x, p.pool, p.seg_starts, p.seg_slot, 0)
+    torch.cuda.synchronize()
+    ys = [p.y0.clone() for _ in range(tp)]
+    flags = [torch.zeros(tp, dtype=torch.int32, device="cuda") for _ in range(tp)]
+    shards = [tpmod.tp_pool(p.pool.a, p.pool.b, tp, rk) for rk in range(tp)]
+    groups = [tpmod.TpGroup(rk, [t.data_ptr() for t in ys], [f.data_ptr() for f in flags]) for rk in range(tp)]
+    streams = [torch.cuda.Stream() for _ in range(tp)]
+    for step, expect in ((1, base), (2, base2)):
+        torch.cuda.synchronize()
+        for rk in range(tp):
+            with torch.cuda.stream(streams[rk]):
+                tpmod.tp_sgmv_p2p(groups[rk], ys[rk], p.x, shards[rk], p.seg_starts, p.seg_slot, 0)
+        torch.cuda.synchronize()
+        for rk in range(tp):
+            assert torch.equal(ys[rk], expect), (step, rk)
+            assert flags[rk].tolist() == [step] * tp
+
+
+def test_tp_nccl_allgather_single_rank_comm(lsg):
+    """lsg_tp_sgmv_nccl's plumbing (slice in place, ncclAllGather, copies back) on a one-rank
+    NCCL communicator: bitwise the plain launch."""
+    from paper_2310_18547_b200 import tp as tpmod
+    h, r = 8192, 16
+    bounds, _, _ = segments_for(UNIFORM, 24, 8)
+    x, A, B = random_problem(h, h, r, bounds, 9)
+    y0 = oracle().rng(10).fill_pm1(24 * h).reshape(24, h)
+    p = Problem(lsg, x, A, B, bounds, torch.bfloat16, y0=y0)
+    base = p.run()
+    comm = tpmod.nccl_comm_single()
+    y = p.y0.clone()
+    tpmod.tp_sgmv_nccl(y, p.x, tpmod.tp_pool(p.pool.a, p.pool.b, 1, 0), p.seg_starts, p.seg_slot, 0, 0, 1, comm)
+    torch.cuda.synchronize()
+    assert torch.equal(y, base)
