@@ -223,6 +223,34 @@ struct Cvt<__half> {
   }
 };
 
+// ---- mixed-precision FMA: fp32 += 16-bit x 16-bit (FHFMA on sm_100) -----------------------
+// d = rn(a * b + c) with a, b 16-bit and c, d fp32: the product of two 16-bit values is
+// exact in fp32, so this is bit for bit fmaf(float(a), float(b), c) -- the shrink chains'
+// canonical arithmetic -- without the two conversions.  The compiler selects the halves of
+// a packed register directly (R.H0 / R.H1 operands).
+template <typename T>
+__device__ __forceinline__ float fma_mixed(uint16_t a, uint16_t b, float c);
+template <>
+__device__ __forceinline__ float fma_mixed<__half>(uint16_t a, uint16_t b, float c) {
+  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+  return c;
+}
+template <>
+__device__ __forceinline__ float fma_mixed<__nv_bfloat16>(uint16_t a, uint16_t b, float c) {
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+  return c;
+}
+// acc[j] = rn(x * a_j + acc[j]) for the 8 16-bit values a_0..a_7 packed in u
+template <typename T>
+__device__ __forceinline__ void fma8_mixed(uint16_t x, const uint4& u, float* acc) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] = fma_mixed<T>(x, static_cast<uint16_t>(w[i] & 0xffffu), acc[2 * i]);
+    acc[2 * i + 1] = fma_mixed<T>(x, static_cast<uint16_t>(w[i] >> 16), acc[2 * i + 1]);
+  }
+}
+
 template <>
 struct Cvt<__nv_bfloat16> {
   __device__ __forceinline__ static float to_f(__nv_bfloat16 h) { return __bfloat162float(h); }

@@ -571,16 +571,12 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
               for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
             const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
             const T* xc = x_sm + ql * KW + rowoff;
+            const uint16_t* xh = reinterpret_cast<const uint16_t*>(xc);
 #pragma unroll 2  // code size: the multi-row body is large (instruction fetch is on the critical path)
             for (int it = 0; it < ITER; ++it) {
-              float a[8];
-              Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
+              const uint4 av = Ac[it * RPI * VPR];
 #pragma unroll
-              for (int m = 0; m < MT; ++m) {
-                const float xm = Cvt<T>::to_f(xc[m * ndl + it * RPI]);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(xm, a[j], acc[m][j]);
-              }
+              for (int m = 0; m < MT; ++m) fma8_mixed<T>(xh[m * ndl + it * RPI], av, acc[m]);
             }
             if (ql == warp) LSG_TRACE(9);  // warp 0: FMA chains of its first unit done
             const int q = q0 + ql;
@@ -627,15 +623,9 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = 0.f;
           const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
-          const T* xc = x_sm + m * ndl + ql * KW + rowoff;
+          const uint16_t* xc = reinterpret_cast<const uint16_t*>(x_sm + m * ndl + ql * KW + rowoff);
 #pragma unroll
-          for (int it = 0; it < ITER; ++it) {
-            float a[8];
-            Cvt<T>::unpack8(Ac[it * RPI * VPR], a);
-            const float xm = Cvt<T>::to_f(xc[it * RPI]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = fmaf(xm, a[j], acc[j]);
-          }
+          for (int it = 0; it < ITER; ++it) fma8_mixed<T>(xc[it * RPI], Ac[it * RPI * VPR], acc);
           if (u == warp) LSG_TRACE(9);  // warp 0: FMA chain of its first unit done
 #pragma unroll
           for (int off = VPR; off < 32; off <<= 1)

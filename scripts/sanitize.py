@@ -32,6 +32,18 @@ from tests._util import (DISTINCT, IDENTICAL, SKEWED, UNIFORM, oracle, random_pr
 TOL = 8e-3
 dev = "cuda"
 failures = []
+# SAN_MAX_CLUSTER=8: keep every CUDA-core launch within portable cluster sizes (synccheck
+# reports 16-CTA clusters at CTA ranks 8 / 9 -- see profiles/round2/sanitizer.md)
+MAX_C = int(os.environ.get("SAN_MAX_CLUSTER", "16"))
+
+
+def cap_cluster(pool, nseg, rows, c):
+    """The forced cluster for this case (0 = auto), capped at MAX_C."""
+    if c > MAX_C:
+        return None
+    if c == 0 and lsg.query_launch(pool, nseg, rows)["cluster"] > MAX_C:
+        return MAX_C
+    return c
 
 
 def problem(h_in, h_out, r, bounds, seed, dtype=torch.float16, layers=1, layer=0):
@@ -62,7 +74,10 @@ def fused_cases():
         for pop, batch in ((DISTINCT, 4), (UNIFORM, 9), (IDENTICAL, 5)):
             bounds, _, _ = segments_for(pop, batch, 3)
             pool, x, ss, sl, ref = problem(512, 256, r, bounds, 4)
-            for c in (0, 1, 4, 16):
+            for c0 in (0, 1, 4, 16):
+                c = cap_cluster(pool, len(bounds) - 1, batch, c0)
+                if c is None:
+                    continue
                 lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
                 for mt in (0, 1, 8):
                     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, mt)
