@@ -298,8 +298,9 @@ typedef enum {
                                    host does not read segment lengths), which costs ~1 us per launch
                                    at 128-256 decode rows: an engine that knows a step has no prefill
                                    segment sets it above the batch size for that step. */
-  LSG_OPT_TC_LEGACY = 10        /* 1: rank-16 long segments on the first-generation fused tensor-core kernel
-                                   instead of the streamed one (A/B measurements) */
+  LSG_OPT_TC_LEGACY = 10        /* long-segment kernel generation (A/B measurements): 0 (default) the
+                                   cluster-free partials + expand pair; 1 the first fused cluster kernel
+                                   (rank 16); 2 the streamed cluster kernel (ranks 16 / 32) */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

@@ -176,3 +176,60 @@ int launch_tc_stream(int dtype, int rank, const Tc2Params& p, int C, uint32_t sm
 }
 
 }  // namespace lsg
+
+#include "sgmv_tc3.cuh"
+
+namespace lsg {
+
+template <typename T, int R>
+static int launch_tc3_parts_inst(const Tc3PartParams& p, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_part_kernel<T, R>;
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc3PartLayout<R>::kTotal);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc parts smem)");
+    mark_configured(configured);
+  }
+  const dim3 grid(static_cast<unsigned>(p.kparts), static_cast<unsigned>(tiles), 1);
+  const cudaError_t e =
+      launch_ex(kern, grid, dim3(kT3Threads), static_cast<int>(Tc3PartLayout<R>::kTotal), 0, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_part_kernel launch");
+}
+
+template <typename T, int R>
+static int launch_tc3_expand_inst(const Tc3ExpParams& p, int tiles, cudaStream_t st) {
+  auto kern = sgmv_tc_exp_kernel<T, R>;
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  if (!configured_on_device(configured)) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc3ExpLayout<R>::kTotal);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc expand2 smem)");
+    mark_configured(configured);
+  }
+  const dim3 grid(static_cast<unsigned>(p.h_out / kTcNT), static_cast<unsigned>(tiles), 1);
+  const cudaError_t e =
+      launch_ex(kern, grid, dim3(kT3Threads), static_cast<int>(Tc3ExpLayout<R>::kTotal), 0, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_tc_exp_kernel launch");
+}
+
+#define LSG_TC3_R(FN, T, ...)                                                        \
+  switch (rank) {                                                                    \
+    case 16: return FN<T, 16>(__VA_ARGS__);                                          \
+    case 32: return FN<T, 32>(__VA_ARGS__);                                          \
+    case 64: return FN<T, 64>(__VA_ARGS__);                                          \
+    default: return fail(LSG_EUNSUPPORTED, "tensor-core path: rank not in {16,32,64}"); \
+  }
+
+int launch_tc3_parts(int dtype, int rank, const Tc3PartParams& p, int tiles, cudaStream_t st) {
+  if (dtype == LSG_F16) LSG_TC3_R(launch_tc3_parts_inst, __half, p, tiles, st)
+  LSG_TC3_R(launch_tc3_parts_inst, __nv_bfloat16, p, tiles, st)
+}
+
+int launch_tc3_expand(int dtype, int rank, const Tc3ExpParams& p, int tiles, cudaStream_t st) {
+  if (dtype == LSG_F16) LSG_TC3_R(launch_tc3_expand_inst, __half, p, tiles, st)
+  LSG_TC3_R(launch_tc3_expand_inst, __nv_bfloat16, p, tiles, st)
+}
+#undef LSG_TC3_R
+
+}  // namespace lsg

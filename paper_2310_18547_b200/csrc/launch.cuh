@@ -68,6 +68,10 @@ int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int t
 int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st);
 struct TcFusedParams;
 int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st);
+struct Tc3PartParams;
+struct Tc3ExpParams;
+int launch_tc3_parts(int dtype, int rank, const Tc3PartParams& p, int tiles, cudaStream_t st);
+int launch_tc3_expand(int dtype, int rank, const Tc3ExpParams& p, int tiles, cudaStream_t st);
 struct Tc2Params;
 int launch_tc_stream(int dtype, int rank, const Tc2Params& p, int C, uint32_t smem, int tiles, cudaStream_t st);
 struct DenseLoraParams;
@@ -160,8 +164,10 @@ int dispatch_item(const FastParams& p, const Plan& pl, cudaStream_t st) {
     if constexpr (R == 64 && MODE == kFused) return launch_fast_inst<T, R, 4, MODE, kItemTileScan>(p, pl, st);
     return fail(LSG_EINVAL, "lsg: 4-row tiles are rank-64 fused only");
   }
-  return pl.tile_scan ? launch_fast_inst<T, R, 8, MODE, kItemTileScan>(p, pl, st)
-                      : launch_fast_inst<T, R, 8, MODE, kItemRowSplit>(p, pl, st);
+  // multi-row tiles always run the tile-scan decode: one tile per work item (the fp32 B of
+  // a tile's expand reuses the shared memory of its A, reloaded per item)
+  if (!pl.tile_scan) return fail(LSG_EINVAL, "lsg: multi-row tiles need the tile-scan decode");
+  return launch_fast_inst<T, R, 8, MODE, kItemTileScan>(p, pl, st);
 }
 
 template <typename T, int MODE>

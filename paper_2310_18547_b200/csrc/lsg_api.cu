@@ -25,6 +25,7 @@
 #include "segment_builder.cuh"
 #include "sgmv_tc.cuh"
 #include "sgmv_tc2.cuh"
+#include "sgmv_tc3.cuh"
 
 namespace lsg {
 
@@ -82,7 +83,7 @@ std::atomic<int> g_opt_tc_split{0};
 std::atomic<int> g_opt_no_row_mode{0};
 std::atomic<int> g_opt_no_rank64_tiles{0};
 std::atomic<int> g_opt_tc_min_rows{0};  // rows from which a segment takes the tensor-core path (0 = default)
-std::atomic<int> g_opt_tc_legacy{0};    // 1: rank-16 long segments on the first-generation fused kernel
+std::atomic<int> g_opt_tc_legacy{0};    // long-segment kernel generation (LSG_OPT_TC_LEGACY)
 
 struct Opts {
   int pdl, force_cluster, force_generic, force_tile_rows, no_alias, no_tile_scan, no_tc, tc_split, no_row_mode,
@@ -165,9 +166,20 @@ int tc_min_rows() {
 }
 
 bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
+// Long segments run on the cluster-free partials + expand kernels (sgmv_tc3.cuh) unless an
+// A/B option picks an earlier generation: LSG_OPT_TC_LEGACY 1 = the first fused kernel
+// (rank 16), 2 = the streamed cluster kernel (ranks 16 / 32); LSG_OPT_TC_SPLIT = the
+// first two-kernel form.
+bool tc3_ok(const lsg_weight_table* t) {
+  return !cur().tc_split && cur().tc_legacy == 0 && tc_nq(t) > 0 && t->h_out % kTcNT == 0;
+}
+size_t tc3_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg) {
+  return static_cast<size_t>(tc_tile_bound(s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
+}
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
+  if (tc_nq(t) > 0 && s_n >= tc_min_rows() && tc3_ok(t)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows());
   // the fused kernels keep v on chip
-  if (!cur().tc_split && (tc2_choose(t, nullptr) || tc_fused_c(t, nullptr) > 0)) return 0;
+  if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) || tc_fused_c(t, nullptr) > 0)) return 0;
   return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
@@ -219,6 +231,9 @@ struct LongPlan {
   TcExpandParams ep;
   TcFusedParams fp;
   Tc2Params tp;
+  Tc3PartParams pp;
+  Tc3ExpParams xp;
+  int tc3 = 0;       // 1: the cluster-free partials + expand pair (sgmv_tc3.cuh), the default
   int nq = 0, tiles = 0;
   int fused_c = 0;   // > 0: one first-generation fused tensor-core launch, clusters of fused_c CTAs
   int stream_c = 0;  // > 0: one streamed tensor-core launch (sgmv_tc2.cuh), clusters of stream_c CTAs
@@ -278,8 +293,49 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   const int nq = tc_nq(tbl);
   if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
+  if (tc3_ok(tbl)) {
+    if (ws == nullptr || !aligned16(ws) || ws_bytes < tc3_ws_bytes(tbl, s_n, n_seg)) return false;
+    Tc3PartParams& pp = lp.pp;
+    Tc3ExpParams& xp = lp.xp;
+    pp = Tc3PartParams{};
+    xp = Tc3ExpParams{};
+    if (!encode_rows_map(&pp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx) ||
+        !encode_rows_map(&xp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
+      return false;
+    lp.tc3 = 1;
+    lp.tiles = tc_tile_bound(s_n, n_seg);
+    pp.ws = static_cast<float*>(ws);
+    pp.a_ptr = tbl->a_ptr;
+    pp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+    pp.seg_starts = seg_starts;
+    pp.seg_slot = seg_slot;
+    pp.n_seg = n_seg;
+    pp.s_n = s_n;
+    pp.num_slots = tbl->num_slots;
+    pp.h_in = tbl->h_in;
+    pp.kparts = tc3_kparts(tbl->h_in);
+    pp.min_rows = tc_min_rows();
+    pp.trace = g_trace;
+    pp.trace_ctas = g_trace_ctas;
+    xp.y = y;
+    xp.ldy = ldy;
+    xp.ws = static_cast<const float*>(ws);
+    xp.b_ptr = tbl->b_ptr;
+    xp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+    xp.seg_starts = seg_starts;
+    xp.seg_slot = seg_slot;
+    xp.n_seg = n_seg;
+    xp.s_n = s_n;
+    xp.num_slots = tbl->num_slots;
+    xp.h_out = tbl->h_out;
+    xp.kparts = pp.kparts;
+    xp.min_rows = pp.min_rows;
+    xp.trace = g_trace;
+    xp.trace_ctas = g_trace_ctas;
+    return true;
+  }
   Tc2Choice ch;
-  if (!cur().tc_split && !(cur().tc_legacy && tbl->rank == 16) && tc2_choose(tbl, &ch)) {
+  if (!cur().tc_split && cur().tc_legacy == 2 && tc2_choose(tbl, &ch)) {
     Tc2Params& tp = lp.tp;
     tp = Tc2Params{};
     if (!encode_rows_map(&tp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx) ||
@@ -311,7 +367,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     return true;
   }
   int compact = 0;
-  const int fc = cur().tc_split ? 0 : tc_fused_c(tbl, &compact);
+  const int fc = cur().tc_split || cur().tc_legacy != 1 ? 0 : tc_fused_c(tbl, &compact);
   if (fc > 0) {
     TcFusedParams& fp = lp.fp;
     fp = TcFusedParams{};
@@ -383,6 +439,11 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
 }
 
 int launch_long_segments(const LongPlan& lp, int dtype, int rank, cudaStream_t cs) {
+  if (lp.tc3) {
+    const int st = launch_tc3_parts(dtype, rank, lp.pp, lp.tiles, cs);
+    if (st != LSG_OK) return st;
+    return launch_tc3_expand(dtype, rank, lp.xp, lp.tiles, cs);
+  }
   if (lp.stream_c > 0) return launch_tc_stream(dtype, rank, lp.tp, lp.stream_c, lp.stream_smem, lp.tiles, cs);
   if (lp.fused_c > 0) return launch_tc_fused(dtype, lp.fp, lp.fused_c, lp.tiles, cs);
   const int st = launch_tc_shrink(dtype, rank, lp.sp, lp.nq, lp.tiles, cs);
@@ -434,10 +495,10 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int forced_mt = cur().force_tile_rows;
   if (kernel == kKBgmv)
     pl.mt = 1;
-  else if (forced_mt == 1 || forced_mt == 8)
+  else if (forced_mt == 1 || forced_mt == 8 || (forced_mt == 4 && t->rank == 64 && kernel == kKFused))
     pl.mt = forced_mt;
   else if (t->rank == 64 && s_n > n_seg && !cur().no_rank64_tiles)
-    pl.mt = kernel == kKFused ? 4 : 8;  // rank 64, shared adapters: one weight read per tile (c3: 4 rows, C = 4)
+    pl.mt = 8;  // rank 64, shared adapters: one weight read per 8-row tile (c3)
   else
     pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
   if (kernel == kKBgmv) {
@@ -486,9 +547,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   const int span = std::max(1, pl.mode == kExpand ? ncvt : pl.mode == kShrink ? nq : std::gcd(nq, ncvt));
   const int64_t est_clusters = long_on_tc ? n_seg : pl.clusters;
   int c = 0, c_small = 0;
-  // Multi-row tiles carry MT rows of compute per CTA: clusters above MT measured slower
-  // (rank 64, c3: MT = 8 C = 16 27.3 us vs C = 8 16.0 us; MT = 4 C = 8 23.4 us vs C = 4 14.8 us).
-  const int c_cap = pl.mt > 1 ? pl.mt : kMaxCluster;
+  const int c_cap = kMaxCluster;
   // Launches with a shrink reduce over DSMEM with st.async, which needs a real
   // cluster (compute-sanitizer memcheck: "Cluster needs to have at least 2 blocks"):
   // at least 2 CTAs (a CTA without chunks only receives).  Expand-only launches: 1.
@@ -964,7 +1023,8 @@ int lsg_set_option(int32_t option, int32_t value) {
       return LSG_OK;
     case LSG_OPT_FORCE_GENERIC: g_opt_force_generic = value ? 1 : 0; return LSG_OK;
     case LSG_OPT_FORCE_TILE_ROWS:
-      if (value != 0 && value != 1 && value != 8) return fail(LSG_EINVAL, "lsg: tile rows must be 0, 1 or 8");
+      if (value != 0 && value != 1 && value != 4 && value != 8)
+        return fail(LSG_EINVAL, "lsg: tile rows must be 0, 1, 4 (rank-64 fused) or 8");
       g_opt_force_tile_rows = value;
       return LSG_OK;
     case LSG_OPT_NO_L2_STAGING: g_opt_no_alias = value > 0 ? 1 : value < 0 ? -1 : 0; return LSG_OK;
@@ -976,7 +1036,10 @@ int lsg_set_option(int32_t option, int32_t value) {
       if (value < 0) return fail(LSG_EINVAL, "lsg: tensor-core row threshold must be >= 0");
       g_opt_tc_min_rows = value;
       return LSG_OK;
-    case LSG_OPT_TC_LEGACY: g_opt_tc_legacy = value ? 1 : 0; return LSG_OK;
+    case LSG_OPT_TC_LEGACY:
+      if (value < 0 || value > 2) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0, 1 or 2");
+      g_opt_tc_legacy = value;
+      return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -133,6 +133,8 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
   uint32_t o = 0;
   const bool sh = mode != kExpand, ex = mode != kShrink;
   const uint32_t a_bytes = sh ? nqc_max * KW * R * 2 : 0, b_bytes = ex ? R * ncv_max * 16 : 0;
+  // multi-row tiles convert B to fp32 once for all rows of the tile, over A / x (consumed)
+  const uint32_t bf_bytes = ex && MT > 1 ? R * ncv_max * 32 : 0;
   L.bars = o;
   o += 128;
   L.a = o;
@@ -145,6 +147,7 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
     o = align128(o + a_bytes);
     L.x = o;
     if (sh) o = align128(o + MT * nqc_max * KW * 2);
+    if (o < L.a + bf_bytes) o = align128(L.a + bf_bytes);
     L.b = o;
     o = align128(o + b_bytes);
   }
@@ -153,7 +156,7 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
   L.recv = o;  // chunk partials received from the cluster
   if (sh) o = align128(o + (red_all ? nq * MT * R : nq * slice_floats(MT, R, C)) * 4);
   L.v = o;
-  o = align128(o + MT * R * 4);
+  o = align128(o + MT * (MT > 1 ? R + 4 : R) * 4);  // multi-row tiles: padded rows (bank spread)
   L.total = o;
   return L;
 }
@@ -201,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
   // One-row fused tiles move x / y_old with one bulk copy each (mbarrier-completed)
   // instead of per-thread cp.async + a block barrier.
   constexpr bool kActBulk = MT == 1 && MODE == kFused;
+  constexpr int VP = MT > 1 ? R + 4 : R;  // V_sm row pitch (floats)
 
   extern __shared__ __align__(128) uint8_t smem[];
   // A CTA that leaves without work: with PDL a grid's completion must imply its
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
       }
 
       if constexpr (MODE == kExpand) {
-        for (int i = tid; i < no; i += kThreads) V_sm[i] = p.v_in[static_cast<int64_t>(r0) * R + i];
+        for (int i = tid; i < no; i += kThreads) V_sm[(i / R) * VP + i % R] = p.v_in[static_cast<int64_t>(r0) * R + i];
       } else {
         if constexpr (kActBulk) {
           if (nqc > 0) mbar_wait(&bars[kBarX], phase);
@@ -557,63 +561,9 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
         const uint4* Av = reinterpret_cast<const uint4*>(A_sm);
         // Work unit = (chunk, row): every warp takes units until none are left.  A
         // unit's arithmetic depends only on its chunk and row, never on which warp,
-        // CTA or tile size computes it.
-        if constexpr (MT > 1) {
-          // Multi-row tiles: unit = one chunk for ALL rows of the tile -- each A vector
-          // is read and converted once and feeds MT independent per-row chains (the same
-          // per-lane chain per row as a one-row unit, so results are unchanged).
-          for (int ql = warp; ql < nqc; ql += kWarps) {
-            mbar_wait(&bars[split_owner(ql, nqc, npieces)], wphase);
-            float acc[MT][8];
-#pragma unroll
-            for (int m = 0; m < MT; ++m)
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
-            const uint4* Ac = Av + (ql * KW + rowoff) * VPR + vec;
-            const T* xc = x_sm + ql * KW + rowoff;
-            const uint16_t* xh = reinterpret_cast<const uint16_t*>(xc);
-#pragma unroll 2  // code size: the multi-row body is large (instruction fetch is on the critical path)
-            for (int it = 0; it < ITER; ++it) {
-              const uint4 av = Ac[it * RPI * VPR];
-#pragma unroll
-              for (int m = 0; m < MT; ++m) fma8_mixed<T>(xh[m * ndl + it * RPI], av, acc[m]);
-            }
-            if (ql == warp) LSG_TRACE(9);  // warp 0: FMA chains of its first unit done
-            const int q = q0 + ql;
-            const int g = lane / VPR;
-            // butterflies of all rows level by level (independent shuffle chains interleave)
-#pragma unroll
-            for (int off = VPR; off < 32; off <<= 1)
-#pragma unroll
-              for (int m = 0; m < MT; ++m)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[m][j] += __shfl_xor_sync(0xffffffffu, acc[m][j], off);
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-              if (m >= rows) break;  // warp-uniform
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int o = m * R + vec * 8 + h * 4;
-                if (red_all) {
-                  const uint32_t local = smem_u32(recv + q * MT * R + o), lbar = smem_u32(&bars[kBarRed]);
-                  for (int dst = (g + h) % RPI; dst < C; dst += RPI)
-                    st_async_v4(mapa_u32(recv + q * MT * R + o, static_cast<uint32_t>(dst)), acc[m][h * 4 + 0],
-                                acc[m][h * 4 + 1], acc[m][h * 4 + 2], acc[m][h * 4 + 3],
-                                mapa_u32(&bars[kBarRed], static_cast<uint32_t>(dst)));
-                  (void)local;
-                  (void)lbar;
-                } else if (g == h) {
-                  const int owner = split_owner(o / 4, no / 4, C);
-                  const int jl = o - split_lo(owner, no / 4, C) * 4;
-                  st_async_v4(mapa_u32(recv + q * slice_max + jl, static_cast<uint32_t>(owner)), acc[m][h * 4 + 0],
-                              acc[m][h * 4 + 1], acc[m][h * 4 + 2], acc[m][h * 4 + 3],
-                              mapa_u32(&bars[kBarRed], static_cast<uint32_t>(owner)));
-                }
-              }
-            }
-            if (ql == warp) LSG_TRACE(13);  // warp 0: first unit pushed
-          }
-        } else {
+        // CTA or tile size computes it.  (Multi-row tiles use the same units: with the
+        // mixed-precision FMA a unit costs one shared-memory load of A per 8 FMAs and
+        // no conversions, and a tile's rows * chunks units keep every warp busy.)
         const int nunits = nqc * rows;
         for (int u = warp; u < nunits; u += kWarps) {
           const int ql = MT == 1 ? u : u / rows, m = MT == 1 ? 0 : u - ql * rows;
@@ -662,7 +612,6 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
           }
           if (u == warp) LSG_TRACE(13);  // warp 0: first unit pushed
         }
-        }  // MT == 1
         if (alias_ab) fence_proxy_async_smem();  // A reads done before TMA overwrites them
         __syncthreads();
         if (kEx && alias_ab && warp == b_warp && ncv > 0) {
@@ -696,8 +645,9 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
               float s4[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) s4[e] = ordered_sum(recv + (o - o0) + e, slice_max, p.nq);
+              float* vd = V_sm + (o / R) * VP + o % R;  // 4 outputs of one row
               for (int dst = 0; dst < C; ++dst)
-                st_async_v4(mapa_u32(V_sm + o, static_cast<uint32_t>(dst)), s4[0], s4[1], s4[2], s4[3],
+                st_async_v4(mapa_u32(vd, static_cast<uint32_t>(dst)), s4[0], s4[1], s4[2], s4[3],
                             mapa_u32(&bars[kBarV], static_cast<uint32_t>(dst)));
             }
           }
@@ -715,39 +665,46 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
           mbar_wait(&bars[kBarB], wphase);
           LSG_TRACE(10);
           if constexpr (MT > 1) {
-            // Multi-row tiles: item = (column vector, 4 rows); each B vector is
-            // read and converted once for the 4 rows (same per-element chain over k).
-            constexpr int RG = 4;
-            const int ngr = (rows + RG - 1) / RG;
-            for (int i = tid; i < ngr * ncv; i += kThreads) {
-              const int gr = i / ncv, cv = i - gr * ncv;
-              float acc[RG][8];
+            // Multi-row tiles: B -> fp32 once (over the consumed A / x), then lane = (row m,
+            // column vector): the MT lanes of a vector read the same B values (broadcast) and
+            // each runs its row's chain over k -- the same per-element chain as one-row tiles.
+            float* Bf = reinterpret_cast<float*>(smem + L.a);
+            for (int i = tid; i < R * ncv; i += kThreads) {
+              float b[8];
+              Cvt<T>::unpack8(B_sm[i], b);
+              reinterpret_cast<float4*>(Bf)[2 * i] = make_float4(b[0], b[1], b[2], b[3]);
+              reinterpret_cast<float4*>(Bf)[2 * i + 1] = make_float4(b[4], b[5], b[6], b[7]);
+            }
+            __syncthreads();
+            constexpr int CPW = 32 / MT;  // column vectors per warp pass
+            const int m = lane % MT, cvl = lane / MT;
+            for (int cvb = warp * CPW; cvb < ncv; cvb += kWarps * CPW) {
+              const int cv = cvb + cvl;
+              if (cv < ncv && m < rows) {
+                float acc[8];
 #pragma unroll
-              for (int r = 0; r < RG; ++r)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
-#pragma unroll 4
-              for (int k = 0; k < R; ++k) {
-                float b[8];
-                Cvt<T>::unpack8(B_sm[k * ncv + cv], b);
-#pragma unroll
-                for (int r = 0; r < RG; ++r) {
-                  const float vk = V_sm[(gr * RG + r) * R + k];
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) acc[r][j] = fmaf(vk, b[j], acc[r][j]);
+                for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+                const float* vr = V_sm + m * VP;
+                const float4* bc = reinterpret_cast<const float4*>(Bf) + 2 * cv;
+#pragma unroll 8
+                for (int k = 0; k < R; ++k) {
+                  const float4 b0 = bc[2 * k * ncv], b1 = bc[2 * k * ncv + 1];
+                  const float vk = vr[k];
+                  acc[0] = fmaf(vk, b0.x, acc[0]);
+                  acc[1] = fmaf(vk, b0.y, acc[1]);
+                  acc[2] = fmaf(vk, b0.z, acc[2]);
+                  acc[3] = fmaf(vk, b0.w, acc[3]);
+                  acc[4] = fmaf(vk, b1.x, acc[4]);
+                  acc[5] = fmaf(vk, b1.y, acc[5]);
+                  acc[6] = fmaf(vk, b1.z, acc[6]);
+                  acc[7] = fmaf(vk, b1.w, acc[7]);
                 }
-              }
+                float yo[8];
+                Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
 #pragma unroll
-              for (int r = 0; r < RG; ++r) {
-                const int m = gr * RG + r;
-                if (m < rows) {
-                  float yo[8];
-                  Cvt<T>::unpack8(y_sm[m * ncv + cv], yo);
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) acc[r][j] = acc[r][j] + yo[j];
-                  st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
-                               Cvt<T>::pack8(acc[r]));
-                }
+                for (int j = 0; j < 8; ++j) acc[j] = acc[j] + yo[j];
+                st_global_v4(static_cast<T*>(s_y) + static_cast<int64_t>(r0 + m) * s_ldy + (cv0 + cv) * 8,
+                             Cvt<T>::pack8(acc));
               }
             }
           } else

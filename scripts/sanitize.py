@@ -118,16 +118,18 @@ def grouped_cases():
 
 
 def tc_cases():
-    for r, split in ((16, 0), (16, 1), (32, 0)):
+    for r, split, gen in ((16, 0, 0), (32, 0, 0), (64, 0, 0), (16, 1, 0), (16, 0, 1), (16, 0, 2), (32, 0, 2)):
         lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, split)
+        lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, gen)
         bounds = np.array([0, 130, 133, 134], dtype=np.uint64)
         pool, x, ss, sl, ref = problem(1024, 1024, r, bounds, 20 + r)
         for pdl in (0, 1):
             lsg.set_option(lsg.LSG_OPT_PDL, pdl)
             y = torch.zeros(134, 1024, dtype=torch.float16, device=dev)
             lsg.sgmv(y, x, pool, ss, sl, 0)
-            check(f"tensor-core r{r} split{split} pdl{pdl}", y, ref)
+            check(f"tensor-core r{r} split{split} gen{gen} pdl{pdl}", y, ref)
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, 0)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 0)
     lsg.set_option(lsg.LSG_OPT_PDL, 0)
 
 

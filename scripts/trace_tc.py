@@ -30,8 +30,11 @@ def main():
     ap.add_argument("--sites", type=int, default=16)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--split", type=int, default=0, help="1: two-kernel path (LSG_OPT_TC_SPLIT)")
+    ap.add_argument("--gen", type=int, default=0, help="LSG_OPT_TC_LEGACY: 0 cluster-free pair, 1 fused, 2 streamed")
     a = ap.parse_args()
     lsg.set_option(_lib.LSG_OPT_TC_SPLIT, a.split)
+    lsg.set_option(_lib.LSG_OPT_TC_LEGACY, a.gen)
+    two = a.split or a.gen == 0
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lens = [int(v) for v in a.segments.split(",")]
     bounds = [0]
@@ -70,7 +73,7 @@ def main():
     allt = buf.view(2 * ctas, 16).cpu().double()
     t0 = None
     groups = ((("shrink", SHRINK, allt[ctas:ctas + ctas // 2]), ("expand", EXPAND, allt[ctas + ctas // 2:]))
-              if a.split else (("fused", FUSED, allt[ctas:ctas + ctas // 2]),))
+              if two else (("fused", FUSED, allt[ctas:ctas + ctas // 2]),))
     for name, phases, part in groups:
         tv = part[part[:, len(phases) - 1] != 0]
         if not tv.numel():

@@ -794,12 +794,12 @@ def test_grid_limit_many_rows(lsg):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("shape", [(4096, 4096, 16), (4096, 4096, 32), (8192, 8192, 16), (5120, 5120, 16),
-                                   (1024, 1024, 32)])
-def test_streamed_tc_kernel_many_tiles_and_legacy_agree(lsg, dtype, shape):
-    """The streamed tensor-core kernel (sgmv_tc2.cuh) with more tiles than co-resident clusters
-    (persistent tile loop), partial last tiles, a no-adapter long segment and decode rows in
-    between: oracle tolerance, run-to-run bitwise, and within tolerance of the first-generation
-    fused kernel (rank 16) / the two-kernel form."""
+                                   (1024, 1024, 32), (4096, 4096, 64)])
+def test_tc_generations_many_tiles_agree(lsg, dtype, shape):
+    """Many long segments (more tiles than co-resident CTAs / clusters), partial last tiles, a
+    no-adapter long segment and decode rows in between, on the default cluster-free kernels
+    (sgmv_tc3.cuh): oracle tolerance, run-to-run bitwise, and within tolerance of every earlier
+    tensor-core generation (streamed cluster kernel, first fused kernel, two-kernel form)."""
     h_in, h_out, r = shape
     lens = [300, 1, 129, 7, 1000, 2, 260, 128, 3, 700, 1, 450]
     bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
@@ -813,17 +813,20 @@ def test_streamed_tc_kernel_many_tiles_and_legacy_agree(lsg, dtype, shape):
     assert row_norm_err(got.double().cpu().numpy(), ref) <= tol(dtype)
     assert torch.equal(got[int(bounds[6]):int(bounds[7])], p.y0[int(bounds[6]):int(bounds[7])])
     assert torch.equal(p.run(), got)
-    other = (lsg._lib.LSG_OPT_TC_LEGACY if r == 16 else lsg._lib.LSG_OPT_TC_SPLIT)
-    lsg.set_option(other, 1)
-    try:
-        alt = p.run()
-    finally:
-        lsg.set_option(other, 0)
-    assert row_norm_err(alt.double().cpu().numpy(), ref) <= tol(dtype)
-    for s, n in enumerate(lens):  # decode rows: the CUDA-core kernel in both runs
-        a, b = int(bounds[s]), int(bounds[s + 1])
-        if n < 128:
-            assert torch.equal(alt[a:b], got[a:b]), s
+    alts = [(lsg._lib.LSG_OPT_TC_SPLIT, 1), (lsg._lib.LSG_OPT_TC_LEGACY, 2)]
+    if r == 16:
+        alts.append((lsg._lib.LSG_OPT_TC_LEGACY, 1))
+    for opt, val in alts:  # every earlier tensor-core generation agrees within tolerance
+        lsg.set_option(opt, val)
+        try:
+            alt = p.run()
+        finally:
+            lsg.set_option(opt, 0)
+        assert row_norm_err(alt.double().cpu().numpy(), ref) <= tol(dtype), (opt, val)
+        for s, n in enumerate(lens):  # decode rows: the CUDA-core kernel in both runs
+            a, b = int(bounds[s]), int(bounds[s + 1])
+            if n < 128:
+                assert torch.equal(alt[a:b], got[a:b]), (opt, val, s)
 
 
 @pytest.mark.parametrize("tp", [2, 4, 8])
