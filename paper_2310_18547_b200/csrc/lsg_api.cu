@@ -531,7 +531,8 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
   };
   auto alias_for = [&](int c) {
     const int o = cur().no_alias;  // 1: never, -1: always (single-tile launches), 0: when co-residency needs it
-    if (pl.mode != kFused || !single_tile || o > 0) return 0;
+    // (multi-row tiles never alias: their expand widens B to fp32 over A / x, sgmv_kernels.cuh)
+    if (pl.mode != kFused || !single_tile || o > 0 || pl.mt > 1) return 0;
     return o < 0 || smem_alias(c, 0) > kCoresidentSmem ? 1 : 0;
   };
   auto smem_for = [&](int c) { return smem_alias(c, alias_for(c)); };

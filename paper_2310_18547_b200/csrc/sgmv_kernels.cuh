@@ -138,7 +138,7 @@ __host__ __device__ inline SmemLayout make_layout(int mode, int R, int MT, int C
   L.bars = o;
   o += 128;
   L.a = o;
-  if (alias_ab) {  // B is loaded over A once the shrink has consumed it
+  if (alias_ab && MT == 1) {  // B is loaded over A once the shrink has consumed it
     L.b = o;
     o = align128(o + (a_bytes > b_bytes ? a_bytes : b_bytes));
     L.x = o;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
   // path is not even emitted into those instantiations)
   // (multi-row tiles always use the owner-sliced two-round reduction: compile-time too)
   constexpr int red_all = MODE == kFused && MT == 1 ? 1 : 0;
-  const int alias_ab = MODE == kFused ? p.alias_ab : 0;
+  const int alias_ab = MODE == kFused && MT == 1 ? p.alias_ab : 0;  // multi-row tiles never alias
   const SmemLayout L = make_layout(MODE, R, MT, C, p.nq, p.nqc_max, p.ncv_max, red_all, alias_ab);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   T* A_sm = reinterpret_cast<T*>(smem + L.a);
