@@ -93,6 +93,10 @@ def parse(argv=None):
     ap.add_argument("--no-tc", action="store_true", help="long segments stay on the CUDA-core kernel")
     ap.add_argument("--tc-split", action="store_true", help="two-kernel tensor-core path for rank-16 long segments")
     ap.add_argument("--no-row-mode", action="store_true", help="segment-major decode for one-row tiles")
+    ap.add_argument("--tc-gen", type=int, default=0, help="LSG_OPT_TC_LEGACY (long-segment kernel generation)")
+    ap.add_argument("--mma-min-rows", type=int, default=0, help="LSG_OPT_MMA_MIN_ROWS (0 = auto)")
+    ap.add_argument("--tc-min-rows", type=int, default=0,
+                    help="per-call tensor-core row threshold (0 = from the step's own segment plan)")
     ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
                     help="sgmv: segmented launch; bgmv: per-row adapter slots (decode BGMV)")
     ap.add_argument("--slots", type=int, default=0, help="adapter-pool slots (0 = one per segment)")
@@ -397,6 +401,8 @@ class Workload:
         # The serving engine knows its step's segment lengths: a decode-only step (no segment
         # of >= 128 rows) skips the tensor-core pass -- a per-call option (lsg_call_opts).
         self.tc_min_rows = self.rows + 1 if max(np.diff(self.bounds), default=0) < 128 else None
+        if a.tc_min_rows > 0:
+            self.tc_min_rows = a.tc_min_rows
         self.bytes = alg_bytes(self.rows, self.nseg, h, r)
 
     def launch(self, s, ys=None, xs=None):
@@ -727,6 +733,8 @@ def main():
     lsg.set_option(lsg.LSG_OPT_NO_L2_STAGING, 1 if a.no_l2_staging else -1 if a.l2_staging else 0)
     lsg.set_option(lsg.LSG_OPT_NO_TENSOR_CORES, int(a.no_tc))
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, int(a.tc_split))
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, a.tc_gen)
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, a.mma_min_rows)
     lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, int(a.no_row_mode))
     h, r, sites = a.hidden, a.rank, a.sites
     # Request partitioning: the partitioner (lsg_partition_segments) hands every rank whole

@@ -126,7 +126,8 @@ int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weig
 typedef struct lsg_call_opts {
   int32_t pdl;             /* programmatic dependent launch: 0 off, 1 on */
   int32_t tc_min_rows;     /* rows from which a segment takes the tensor-core path (0 = 128) */
-  int32_t no_tensor_cores; /* 1: long segments stay on the CUDA-core kernel */
+  int32_t no_tensor_cores; /* 1: every segment stays on the CUDA-core kernel */
+  int32_t mma_min_rows;    /* LSG_OPT_MMA_MIN_ROWS for this call (0 = auto) */
 } lsg_call_opts;
 
 /* lsg_sgmv with per-call options and an optional caller workspace (NULL: the
@@ -298,9 +299,14 @@ typedef enum {
                                    host does not read segment lengths), which costs ~1 us per launch
                                    at 128-256 decode rows: an engine that knows a step has no prefill
                                    segment sets it above the batch size for that step. */
-  LSG_OPT_TC_LEGACY = 10        /* long-segment kernel generation (A/B measurements): 0 (default) the
+  LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation (A/B measurements): 0 (default) the
                                    cluster-free partials + expand pair; 1 the first fused cluster kernel
-                                   (rank 16); 2 the streamed cluster kernel (ranks 16 / 32) */
+                                   (rank 16); 2 the streamed cluster kernel (ranks 16 / 32); 3 the
+                                   segment-tile MMA pair (16-row tiles, mma.sync) */
+  LSG_OPT_MMA_MIN_ROWS = 11     /* segments with at least this many rows (and below the long-segment
+                                   threshold) take the segment-tile MMA pair; 0 (default) = auto: rank 64
+                                   calls whose rows share adapters (total_rows > num_segments) send every
+                                   segment to it, other ranks keep the CUDA-core kernel */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

@@ -68,6 +68,8 @@ int launch_tc_shrink(int dtype, int rank, const TcShrinkParams& p, int nq, int t
 int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cudaStream_t st);
 struct TcFusedParams;
 int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st);
+struct MmaParams;
+int launch_mma_pair(int dtype, int rank, const MmaParams& p, int tiles, cudaStream_t st);
 struct Tc3PartParams;
 struct Tc3ExpParams;
 int launch_tc3_parts(int dtype, int rank, const Tc3PartParams& p, int tiles, cudaStream_t st);

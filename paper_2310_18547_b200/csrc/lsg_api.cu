@@ -26,6 +26,7 @@
 #include "sgmv_tc.cuh"
 #include "sgmv_tc2.cuh"
 #include "sgmv_tc3.cuh"
+#include "sgmv_mma.cuh"
 
 namespace lsg {
 
@@ -84,20 +85,23 @@ std::atomic<int> g_opt_no_row_mode{0};
 std::atomic<int> g_opt_no_rank64_tiles{0};
 std::atomic<int> g_opt_tc_min_rows{0};  // rows from which a segment takes the tensor-core path (0 = default)
 std::atomic<int> g_opt_tc_legacy{0};    // long-segment kernel generation (LSG_OPT_TC_LEGACY)
+std::atomic<int> g_opt_mma_min_rows{0};  // rows from which a segment takes the segment-tile MMA pair (0 = auto)
 
 struct Opts {
   int pdl, force_cluster, force_generic, force_tile_rows, no_alias, no_tile_scan, no_tc, tc_split, no_row_mode,
-      no_rank64_tiles, tc_min_rows, tc_legacy;
+      no_rank64_tiles, tc_min_rows, tc_legacy, mma_min_rows;
 };
 
 Opts snapshot(const lsg_call_opts* c) {
   Opts o{g_opt_pdl.load(),     g_opt_force_cluster.load(), g_opt_force_generic.load(), g_opt_force_tile_rows.load(),
          g_opt_no_alias.load(), g_opt_no_tile_scan.load(), g_opt_no_tc.load(),        g_opt_tc_split.load(),
-         g_opt_no_row_mode.load(), g_opt_no_rank64_tiles.load(), g_opt_tc_min_rows.load(), g_opt_tc_legacy.load()};
+         g_opt_no_row_mode.load(), g_opt_no_rank64_tiles.load(), g_opt_tc_min_rows.load(), g_opt_tc_legacy.load(),
+         g_opt_mma_min_rows.load()};
   if (c != nullptr) {
     if (c->pdl >= 0) o.pdl = c->pdl ? 1 : 0;
     if (c->tc_min_rows >= 0) o.tc_min_rows = c->tc_min_rows;
     if (c->no_tensor_cores >= 0) o.no_tc = c->no_tensor_cores ? 1 : 0;
+    if (c->mma_min_rows >= 0) o.mma_min_rows = c->mma_min_rows;
   }
   return o;
 }
@@ -181,6 +185,108 @@ size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
   // the fused kernels keep v on chip
   if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) || tc_fused_c(t, nullptr) > 0)) return 0;
   return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
+}
+
+// ---- segment-tile MMA pair (K7, sgmv_mma.cuh) ---------------------------------------
+// Rows [lo, hi) of a fused call take the MMA pair.  Default (LSG_OPT_MMA_MIN_ROWS = 0):
+// rank 64 with rows sharing adapters (total_rows > num_segments, so some segment has >= 2
+// rows) sends EVERY segment to it (lo = 1: no CUDA-core launch at all -- the weights of each
+// segment are spread over ~one CTA per SM whatever its length); otherwise off.  With
+// LSG_OPT_TC_LEGACY = 3 the pair also takes the long segments (instead of sgmv_tc3.cuh).
+constexpr int kRowsInf = 0x7fffffff;
+bool mma_shape_ok(const lsg_weight_table* t) {
+  return (t->rank == 16 || t->rank == 32 || t->rank == 64) && t->h_in % kMmaKC == 0 && t->h_out % kMmaKC == 0 &&
+         t->a_layer_stride % 8 == 0 && t->b_layer_stride % 8 == 0;
+}
+struct RowRanges {
+  int mma_lo = 0, mma_hi = 0;  // [mma_lo, mma_hi): MMA pair (mma_lo == 0: none)
+  int tc_lo = 0;               // [tc_lo, inf): long-segment tensor-core kernels (0: none)
+};
+RowRanges row_ranges(const lsg_weight_table* t, int n_seg, int s_n) {
+  RowRanges rr;
+  if (cur().no_tc) return rr;
+  const bool tc = tc_nq(t) > 0 && s_n >= tc_min_rows();
+  const bool gen3 = cur().tc_legacy == 3 && mma_shape_ok(t);
+  if (tc && !gen3) rr.tc_lo = tc_min_rows();
+  int lo = cur().mma_min_rows;
+  if (lo <= 0) lo = (t->rank == 64 && s_n > n_seg) ? 1 : 0;
+  if (!mma_shape_ok(t)) lo = 0;
+  if (gen3 && tc) lo = lo > 0 ? std::min(lo, tc_min_rows()) : tc_min_rows();
+  const int hi = rr.tc_lo > 0 ? rr.tc_lo : kRowsInf;
+  if (lo > 0 && lo < hi && s_n >= lo) {
+    rr.mma_lo = lo;
+    rr.mma_hi = hi;
+  }
+  return rr;
+}
+// 16-row tiles of the segments with len >= lo: sum ceil(len/16) <= s_n/16 + #segments
+int mma_tile_bound(int s_n, int n_seg, int lo) {
+  return std::max(1, s_n / kMmaM + std::min(n_seg, s_n / std::max(lo, 1)));
+}
+// K / column splits: about one CTA per SM for each of the two kernels (the tile bound
+// overestimates the real tiles), the largest divisor of the 64-column stage count that
+// keeps tiles x split <= 160.
+int mma_split(int nstages, int tiles) {
+  int best = 1;
+  for (int d = 1; d <= nstages; ++d)
+    if (nstages % d == 0 && static_cast<int64_t>(tiles) * d <= 160) best = d;
+  return best;
+}
+// workspace bound: tiles * kparts <= max(160, tiles)
+size_t mma_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg, int lo) {
+  const int tiles = mma_tile_bound(s_n, n_seg, lo);
+  return static_cast<size_t>(std::max(160, tiles)) * kMmaM * t->rank * sizeof(float);
+}
+constexpr uint32_t kMmaSmemTarget = 100 * 1024;  // two CTAs per SM
+int mma_stages(uint32_t fixed, uint32_t stage, int nst) {
+  const int fit = static_cast<int>((kMmaSmemTarget - fixed) / stage);
+  return std::max(1, std::min({nst, kMmaMaxStages, fit}));
+}
+bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_t ldy, const void* x, int64_t ldx,
+                 const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg, int s_n,
+                 int layer, void* ws, size_t ws_bytes) {
+  if (rr.mma_lo == 0) return false;
+  if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0) return false;
+  tiles = mma_tile_bound(s_n, n_seg, rr.mma_lo);
+  if (tiles > kMaxGridY) return false;
+  if (ws == nullptr || !aligned16(ws) || ws_bytes < mma_ws_bytes(tbl, s_n, n_seg, rr.mma_lo)) return false;
+  const int R = tbl->rank;
+  mp = MmaParams{};
+  mp.y = y;
+  mp.x = x;
+  mp.ldx = ldx;
+  mp.ldy = ldy;
+  mp.a_ptr = tbl->a_ptr;
+  mp.b_ptr = tbl->b_ptr;
+  mp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+  mp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+  mp.seg_starts = seg_starts;
+  mp.seg_slot = seg_slot;
+  mp.ws = static_cast<float*>(ws);
+  mp.n_seg = n_seg;
+  mp.s_n = s_n;
+  mp.num_slots = tbl->num_slots;
+  mp.h_in = tbl->h_in;
+  mp.h_out = tbl->h_out;
+  mp.kparts = mma_split(tbl->h_in / kMmaKC, tiles);
+  mp.ncol = mma_split(tbl->h_out / kMmaKC, tiles);
+  mp.stages_p = mma_stages(mma_part_smem(R, 0), mma_part_stage_bytes(R), tbl->h_in / mp.kparts / kMmaKC);
+  mp.stages_e = mma_stages(mma_exp_smem(R, 0), mma_exp_stage_bytes(R), tbl->h_out / mp.ncol / kMmaKC);
+  mp.min_rows = rr.mma_lo;
+  mp.max_rows = rr.mma_hi;
+  mp.trace = g_trace;
+  mp.trace_ctas = g_trace_ctas;
+  return true;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+// Workspace a fused call of total_rows rows may need, over every segment count: the MMA
+// partials (worst case: rows sharing adapters, one segment per row) + the K5 v.
+size_t call_ws_bound(const lsg_weight_table* t, int s_n) {
+  const RowRanges rr = row_ranges(t, std::max(0, s_n - 1), s_n);
+  size_t b = rr.mma_lo > 0 ? align256(mma_ws_bytes(t, s_n, s_n, rr.mma_lo)) : 0;
+  if (tc_nq(t) > 0 && s_n >= tc_min_rows()) b += tc_workspace_bytes(t, s_n);
+  return b;
 }
 
 // Library-owned workspace of lsg_sgmv(), one per device (a process may drive
@@ -483,7 +589,10 @@ bool fast_shape_ok(const lsg_weight_table* t) {
 }
 
 // Choose tile rows, row splits and the split-K cluster size for a launch.
-Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast, bool long_on_tc = false) {
+// long_on_tc: the launch's long / shared segments go to tensor-core kernels; short_rows > 0:
+// the segments left to this kernel are shorter than short_rows rows.
+Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool fast, bool long_on_tc = false,
+               int short_rows = 0) {
   Plan pl;
   pl.mode = kernel == kKShrink ? kShrink : kernel == kKExpand ? kExpand : kFused;
   if (!fast || cur().force_generic) {
@@ -497,7 +606,7 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     pl.mt = 1;
   else if (forced_mt == 1 || forced_mt == 8 || (forced_mt == 4 && t->rank == 64 && kernel == kKFused))
     pl.mt = forced_mt;
-  else if (t->rank == 64 && s_n > n_seg && !cur().no_rank64_tiles)
+  else if (t->rank == 64 && s_n > n_seg && !cur().no_rank64_tiles && !(short_rows > 0 && short_rows <= 8))
     pl.mt = 8;  // rank 64, shared adapters: one weight read per 8-row tile (c3)
   else
     pl.mt = 1;  // one row per cluster: the shortest critical path per launch (profiles/README.md)
@@ -636,17 +745,45 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   // stream their weights there (measured neutral on c4, 24.0 us either way).  The
   // tensor-core shrink triggers its dependents only after its own PDL wait, so the
   // expand may stage y_old before waiting for v.
+  // Rows of segments in [mma_lo, mma_hi) go to the segment-tile MMA pair (K7), rows of
+  // segments >= tc_lo to the long-segment tensor-core kernels (K5); the CUDA-core kernel
+  // then skips every segment of >= skip_long rows -- or is not launched at all when the
+  // tensor-core kernels cover every segment.  Workspace: [MMA partials | K5 v].
   int skip_long = 0;
+  bool cuda_core = true;
   LongPlan lp;
-  if (kernel == kKFused && !cur().no_tc && s_n >= tc_min_rows() && tc_nq(tbl) > 0) {
-    if (library_ws) {
-      ws_bytes = tc_workspace_bytes(tbl, s_n);
-      ws = library_workspace(ws_bytes, cs);
+  MmaParams mp{};
+  int mma_tiles = 0;
+  bool use_tc = false, use_mma = false;
+  if (kernel == kKFused) {
+    RowRanges rr = row_ranges(tbl, n_seg, s_n);
+    if (rr.mma_lo > 0 || rr.tc_lo > 0) {
+      const size_t mma_b = rr.mma_lo > 0 ? align256(mma_ws_bytes(tbl, s_n, n_seg, rr.mma_lo)) : 0;
+      if (library_ws) {
+        ws_bytes = mma_b + (rr.tc_lo > 0 ? tc_workspace_bytes(tbl, s_n) : 0);
+        ws = ws_bytes > 0 ? library_workspace(ws_bytes, cs) : nullptr;
+        if (ws == nullptr) ws_bytes = 0;
+      }
+      if (rr.tc_lo > 0) {
+        void* tws = ws != nullptr && ws_bytes >= mma_b ? static_cast<char*>(ws) + mma_b : nullptr;
+        use_tc = prepare_long_segments(lp, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, tws,
+                                       tws != nullptr ? ws_bytes - mma_b : 0);
+        if (!use_tc) {
+          if (rr.mma_lo > 0) rr.mma_hi = kRowsInf;  // the MMA pair takes the long segments too
+          rr.tc_lo = 0;
+        }
+      }
+      use_mma = prepare_mma(mp, mma_tiles, rr, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, ws,
+                            ws_bytes);
+      if (use_mma) {
+        skip_long = rr.mma_lo;
+        cuda_core = !(rr.mma_lo == 1 && rr.mma_hi == kRowsInf);
+      } else if (use_tc) {
+        skip_long = rr.tc_lo;
+      }
     }
-    if (prepare_long_segments(lp, y, ldy, x, ldx, tbl, seg_starts, seg_slot, n_seg, s_n, layer, ws, ws_bytes))
-      skip_long = tc_min_rows();
   }
-  Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true) : pl0;
+  Plan pl = skip_long ? make_plan(tbl, kernel, n_seg, s_n, fast, true, skip_long) : pl0;
   // One-row tiles without a long-segment split: one cluster per row, exact grid.
   if (pl.mt == 1 && kernel != kKBgmv && !skip_long && !cur().no_row_mode && s_n <= kMaxGridY) {
     pl.row_mode = 1;
@@ -727,10 +864,15 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   }();
   p.exp_flags = exp_flags;
 #endif
-  if (skip_long) {
+  if (use_mma) {
+    st = launch_mma_pair(tbl->dtype, tbl->rank, mp, mma_tiles, cs);
+    if (st != LSG_OK) return st;
+  }
+  if (use_tc) {
     st = launch_long_segments(lp, tbl->dtype, tbl->rank, cs);
     if (st != LSG_OK) return st;
   }
+  if (!cuda_core) return LSG_OK;
   switch (pl.mode) {
     case kFused: st = launch_fast_fused(tbl->dtype, tbl->rank, p, pl, cs); break;
     case kShrink: st = launch_fast_shrink(tbl->dtype, tbl->rank, p, pl, cs); break;
@@ -766,7 +908,7 @@ int lsg_sgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
 size_t lsg_sgmv_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
   CallScope scope(nullptr);
   if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
-  return tc_workspace_bytes(tbl, total_rows);
+  return call_ws_bound(tbl, total_rows);
 }
 
 int lsg_sgmv_ws(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* tbl,
@@ -837,7 +979,7 @@ int lsg_sgmv_multi(const lsg_sgmv_site* sites, int32_t num_sites, const int32_t*
 int lsg_tp_sgmv(const lsg_tp_group* g, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_table* shard,
                 const int32_t* seg_starts, const int32_t* seg_slot, int32_t num_segments, int32_t total_rows,
                 int32_t layer, uint32_t epoch, lsg_stream_t stream) {
-  lsg_call_opts o{-1, -1, 1};  // decode batches: long segments would need the tensor-core kernels
+  lsg_call_opts o{-1, -1, 1, -1};  // decode batches: long segments would need the tensor-core kernels
   CallScope scope(&o);
   if (g == nullptr || g->size < 1 || g->size > kMaxSites || g->rank < 0 || g->rank >= g->size ||
       g->y_peer == nullptr || g->flag_peer == nullptr)
@@ -1038,8 +1180,12 @@ int lsg_set_option(int32_t option, int32_t value) {
       g_opt_tc_min_rows = value;
       return LSG_OK;
     case LSG_OPT_TC_LEGACY:
-      if (value < 0 || value > 2) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0, 1 or 2");
+      if (value < 0 || value > 3) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0 .. 3");
       g_opt_tc_legacy = value;
+      return LSG_OK;
+    case LSG_OPT_MMA_MIN_ROWS:
+      if (value < 0) return fail(LSG_EINVAL, "lsg: MMA row threshold must be >= 0");
+      g_opt_mma_min_rows = value;
       return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
@@ -1058,6 +1204,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_NO_MULTIROW_TILES: return cur().no_rank64_tiles;
     case LSG_OPT_TC_MIN_ROWS: return g_opt_tc_min_rows.load();
     case LSG_OPT_TC_LEGACY: return g_opt_tc_legacy.load();
+    case LSG_OPT_MMA_MIN_ROWS: return g_opt_mma_min_rows.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -1,0 +1,455 @@
+// sgmv_mma.cuh -- K7: segment-tile tensor-core pair for segments whose rows share one
+// adapter (ranks 16 / 32 / 64): shared-adapter decode batches (Uniform / Skewed /
+// Identical, BASELINE configs[2]) and prefill segments (configs[3]).
+//
+// A tile is up to 16 rows of one segment -- exactly one m16 block of the warp-level
+// tensor-core MMA (mma.sync m16n8k16, fp32 accumulate).  Two launches, chained with
+// programmatic dependent launch:
+//
+//   partials  grid (kparts, tile bound), 128 threads.  CTA (ks, t) computes the partial
+//             P_ks[16][R] = x[tile rows, K slice ks] . A[K slice ks, :] over its K slice of
+//             KS = h_in / kparts columns, in stages of 64 columns (x 16 x 64 and A 64 x R,
+//             both cp.async'd into XOR-swizzled shared memory so ldmatrix is conflict-free;
+//             the A stages of the whole ring are requested BEFORE the PDL wait).  Warp w
+//             takes k16-step w of every stage; the four warp accumulators are summed in warp
+//             order and P_ks goes to the workspace [tile][ks][16][R] fp32 (L2-resident).
+//   expand    grid (ncol, tile bound), 128 threads.  CTA (j, t) stages its B column slice
+//             (R x NC) and y_old (16 x NC) before its PDL wait -- the partials kernel
+//             triggers its dependents only after its own wait, so every kernel before it has
+//             completed and y_old is final -- then sums the tile's partials in ks order
+//             (v, fp32), splits v into 16-bit hi + lo (hi = rn(v), lo = rn(v - hi)) and
+//             runs D = hi.B + lo.B on the tensor cores (the lo term keeps v's fp32
+//             precision), adds y_old in fp32 and rounds once.  Stores are 16-byte vectors of
+//             the tile's valid rows only.
+//
+// Why this shape: a shared-adapter segment is weight-bound (h=5120 r=64: 1.25 MiB of A+B
+// per segment against 8 rows x 20 KiB of activations), so the weights of one tile are
+// spread over kparts x ncol CTAs (about one per SM) instead of one cluster; long prefill
+// segments are activation-bound and get one CTA per 16-row tile with the whole K (or N)
+// range streamed through a ring.  The same two kernels cover both with different splits
+// (lsg_api.cu: mma_plan).
+//
+// Canonical arithmetic for these rows (deterministic; depends only on the shape, never on
+// the batch composition or the launch): v = sum over parts ks ascending of
+// (sum over warps w ascending of the MMA chain of k16-steps w, w+4, ... of part ks);
+// y = rn(fp32(hi.B + lo.B) + y_old).  Within tolerance of the CUDA-core rows, not bitwise.
+#pragma once
+
+#include "sgmv_device.cuh"
+#include "sgmv_tc.cuh"  // LSG_TC_TRACE
+
+namespace lsg {
+
+constexpr int kMmaM = 16;         // rows per tile (one m16 block)
+constexpr int kMmaThreads = 128;  // 4 warps
+constexpr int kMmaKC = 64;        // columns per pipeline stage (4 k16-steps: one per warp)
+
+struct MmaParams {
+  void* y;
+  const void* x;
+  int64_t ldx;
+  int64_t ldy;
+  const void* const* a_ptr;
+  const void* const* b_ptr;
+  int64_t a_off;  // layer * a_layer_stride
+  int64_t b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  float* ws;  // [tile bound][kparts][16][R] fp32 partials
+  int32_t n_seg, s_n, num_slots, h_in, h_out;
+  int32_t kparts;    // K slices (gridDim.x of the partials kernel)
+  int32_t ncol;      // column slices (gridDim.x of the expand kernel)
+  int32_t stages_p;  // ring depth of the partials kernel
+  int32_t stages_e;  // ring depth of the expand kernel
+  int32_t min_rows;  // segments with min_rows <= len < max_rows take this path
+  int32_t max_rows;
+  unsigned long long* trace;  // phase stamps (instrumented builds only, LSG_TC_TRACE layout)
+  int32_t trace_ctas;
+};
+
+// ---- warp-level MMA primitives ----------------------------------------------------------
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+template <typename T>
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1);
+template <>
+__device__ __forceinline__ void mma16816<__half>(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <>
+__device__ __forceinline__ void mma16816<__nv_bfloat16>(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// rn(d0 + y[0]), rn(d1 + y[1]) for the two 16-bit values packed in y (fp32 add, one rounding)
+template <typename T>
+__device__ __forceinline__ uint32_t add2_round(uint32_t y, float d0, float d1);
+template <>
+__device__ __forceinline__ uint32_t add2_round<__half>(uint32_t y, float d0, float d1) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&y));
+  const __half2 r = __floats2half2_rn(d0 + f.x, d1 + f.y);
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+template <>
+__device__ __forceinline__ uint32_t add2_round<__nv_bfloat16>(uint32_t y, float d0, float d1) {
+  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&y));
+  const __nv_bfloat162 r = __floats2bfloat162_rn(d0 + f.x, d1 + f.y);
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+
+// 16-byte cp.async that zero-fills instead of reading when !valid (rows past a tile's end)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+// arrive on `bar` once all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Swizzle of a row of CPR 16-byte chunks (CPR = 2, 4, 8): chunk c of row k lives at chunk
+// c ^ mma_swz<CPR>(k).  Any 8 consecutive rows (aligned) then hit 8 distinct 16-byte bank
+// groups for a fixed logical chunk -- ldmatrix (plain or .trans) is conflict-free.
+template <int CPR>
+__device__ __forceinline__ int mma_swz(int k) {
+  static_assert(CPR == 2 || CPR == 4 || CPR == 8, "chunks per row");
+  return (k >> (CPR == 8 ? 0 : CPR == 4 ? 1 : 2)) & (CPR - 1);
+}
+
+// Tile t -> (segment, tile within it) over the segments with min_rows <= len < max_rows,
+// 16-row tiles: warp prefix sums over 32 segments per step (all lanes of one warp).
+__device__ __forceinline__ void mma_tile_of(const int32_t* seg_starts, int n_seg, int t, int lane, int min_rows,
+                                            int max_rows, int& seg, int& tin) {
+  int base = 0;
+  seg = -1;
+  tin = 0;
+  for (int c0 = 0; c0 < n_seg && seg < 0; c0 += 32) {
+    const int sg = c0 + lane;
+    int nt = 0;
+    if (sg < n_seg) {
+      const int len = seg_starts[sg + 1] - seg_starts[sg];
+      nt = (len >= min_rows && len < max_rows) ? (len + kMmaM - 1) / kMmaM : 0;
+    }
+    int incl = nt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, nt > 0 && t < base + incl);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      seg = c0 + l;
+      tin = t - (base + __shfl_sync(0xffffffffu, incl - nt, l));
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ---- shared-memory plans (host and device) -----------------------------------------------
+__host__ __device__ constexpr uint32_t mma_part_stage_bytes(int R) { return kMmaM * kMmaKC * 2 + kMmaKC * R * 2; }
+__host__ __device__ constexpr uint32_t mma_exp_stage_bytes(int R) { return R * kMmaKC * 2 + kMmaM * kMmaKC * 2; }
+// partials: [ring stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, barriers
+__host__ __device__ constexpr uint32_t mma_part_smem(int R, int stages) {
+  return stages * mma_part_stage_bytes(R) + 4 * kMmaM * R * 4 + 2 * 8 * 32 + 128;
+}
+// expand: [ring stages][B 128R B | y 2 KB], v hi / lo (16 x R 16-bit each), barriers
+__host__ __device__ constexpr uint32_t mma_exp_smem(int R, int stages) {
+  return stages * mma_exp_stage_bytes(R) + 2 * kMmaM * R * 2 + 2 * 8 * 32 + 128;
+}
+constexpr int kMmaMaxStages = 32;
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid_constant__ MmaParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
+  constexpr int CPR = R / 8;                     // 16-byte chunks per A row
+  constexpr uint32_t kXB = kMmaM * kMmaKC * 2;   // x stage bytes
+  constexpr uint32_t kSB = mma_part_stage_bytes(R);
+  constexpr int NT = R / 8;                      // n8 tiles of the accumulator
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int S = p.stages_p;
+  float* red = reinterpret_cast<float*>(smem + S * kSB);                     // [4][16][R]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kSB + 4 * kMmaM * R * 4);  // [S] stage landed
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ks = static_cast<int>(blockIdx.x);
+  const int KS = p.h_in / p.kparts, nst = KS / kMmaKC;
+  LSG_TC_TRACE(0, 0);
+
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    mma_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, p.min_rows, p.max_rows, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], kMmaThreads);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
+  // CTAs without work leave at once; the first row of the grid still waits for the preceding
+  // grid (and triggers) so this grid's completion implies the predecessor's.
+  if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {
+    if (blockIdx.y == 0) {
+      pdl_wait();
+      pdl_launch_dependents();
+    }
+    return;
+  }
+  const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
+  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
+  const int k0 = ks * KS;
+  const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(k0) * R;
+  const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx + k0;
+
+  auto load_a = [&](int s) {  // stage s of A: 64 rows x R, swizzled
+    uint8_t* dst = smem + (s % S) * kSB + kXB;
+    const T* src = A + static_cast<int64_t>(s) * kMmaKC * R;
+    for (int i = tid; i < kMmaKC * CPR; i += kMmaThreads) {
+      const int k = i / CPR, c = i - k * CPR;
+      cp_async16(dst + k * (R * 2) + ((c ^ mma_swz<CPR>(k)) << 4), src + static_cast<int64_t>(i) * 8);
+    }
+  };
+  auto load_x = [&](int s) {  // stage s of x: 16 rows x 64 columns, swizzled, zero rows past the tile
+    uint8_t* dst = smem + (s % S) * kSB;
+    const int m = tid >> 3, c = tid & 7;  // 128 threads = 16 rows x 8 chunks
+    cp_async16_zfill(dst + m * 128 + ((c ^ (m & 7)) << 4), X + static_cast<int64_t>(m < rows ? m : 0) * p.ldx +
+                                                                 s * kMmaKC + c * 8,
+                     m < rows);
+  };
+  // weights first (before the PDL wait): the whole ring of A stages
+  const int pre = min(S, nst);
+  for (int s = 0; s < pre; ++s) load_a(s);
+  LSG_TC_TRACE(0, 1);
+  pdl_wait();  // x may come from the preceding kernel
+  LSG_TC_TRACE(0, 2);
+  // Dependents (the expand) start now: every kernel before this one has completed, so the
+  // expand may stage y_old before its own wait (it waits only for these partials).
+  pdl_launch_dependents();
+  for (int s = 0; s < pre; ++s) {
+    load_x(s);
+    cp_async_arrive(&full[s]);
+  }
+
+  float acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  // lane's ldmatrix row / chunk within a 16 x 16 block
+  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = lane >> 4;
+  for (int s = 0; s < nst; ++s) {
+    const int b = s % S;
+    mbar_wait(&full[b], (s / S) & 1);
+    if (s == 0) LSG_TC_TRACE(0, 3);
+    const uint32_t xs = smem_u32(smem + b * kSB), as = xs + kXB;
+    uint32_t a[4];
+    {  // x rows 0..15, k16-step `warp` of this stage: chunks 2w, 2w+1
+      const int c = 2 * warp + lc;
+      ldsm_x4(xs + lr * 128 + ((c ^ (lr & 7)) << 4), a[0], a[1], a[2], a[3]);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; j += 2) {  // A rows 16w..16w+15, n8 tiles j, j+1
+      const int k = 16 * warp + lr, c = j + lc;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(as + k * (R * 2) + ((c ^ mma_swz<CPR>(k)) << 4), b0, b1, b2, b3);
+      mma16816<T>(acc[j], a, b0, b1);
+      mma16816<T>(acc[j + 1], a, b2, b3);
+    }
+    __syncthreads();  // every warp is done with buffer b
+    if (s + S < nst) {
+      load_a(s + S);
+      load_x(s + S);
+      cp_async_arrive(&full[b]);
+    }
+  }
+  // ---- sum the four warp accumulators in warp order, write the partial ------------------
+  LSG_TC_TRACE(0, 4);
+  {
+    const int g = lane >> 2, t = lane & 3;
+    float* rw = red + warp * kMmaM * R;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      *reinterpret_cast<float2*>(rw + g * R + j * 8 + 2 * t) = make_float2(acc[j][0], acc[j][1]);
+      *reinterpret_cast<float2*>(rw + (g + 8) * R + j * 8 + 2 * t) = make_float2(acc[j][2], acc[j][3]);
+    }
+  }
+  __syncthreads();
+  float* dst = p.ws + (static_cast<int64_t>(blockIdx.y) * p.kparts + ks) * kMmaM * R;
+  for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
+    float4 s4 = *reinterpret_cast<const float4*>(red + i);
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      const float4 o = *reinterpret_cast<const float4*>(red + w * kMmaM * R + i);
+      s4.x += o.x, s4.y += o.y, s4.z += o.z, s4.w += o.w;
+    }
+    *reinterpret_cast<float4*>(dst + i) = s4;
+  }
+  LSG_TC_TRACE(0, 5);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_constant__ MmaParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
+  constexpr int CPR = R / 8;
+  constexpr uint32_t kBB = R * kMmaKC * 2;  // B stage bytes (R rows x 64 columns)
+  constexpr uint32_t kSB = mma_exp_stage_bytes(R);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int S = p.stages_e;
+  uint8_t* vhi = smem + S * kSB;
+  uint8_t* vlo = vhi + kMmaM * R * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(vlo + kMmaM * R * 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NC = p.h_out / p.ncol, nst = NC / kMmaKC;
+  const int n0 = static_cast<int>(blockIdx.x) * NC;
+  LSG_TC_TRACE(1, 0);
+
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    mma_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, p.min_rows, p.max_rows, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], kMmaThreads);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
+  if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {
+    if (blockIdx.y == 0) {
+      pdl_wait();
+      pdl_launch_dependents();
+    }
+    return;
+  }
+  const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
+  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
+  const T* Bg = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
+  T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy + n0;
+
+  auto load_b = [&](int s) {  // stage s of B: R rows x 64 columns, swizzled
+    uint8_t* dst = smem + (s % S) * kSB;
+    for (int i = tid; i < R * 8; i += kMmaThreads) {
+      const int k = i >> 3, c = i & 7;
+      cp_async16(dst + k * 128 + ((c ^ (k & 7)) << 4), Bg + static_cast<int64_t>(k) * p.h_out + s * kMmaKC + c * 8);
+    }
+  };
+  auto load_y = [&](int s) {  // stage s of y_old: 16 rows x 64 columns, swizzled
+    uint8_t* dst = smem + (s % S) * kSB + kBB;
+    const int m = tid >> 3, c = tid & 7;
+    cp_async16_zfill(dst + m * 128 + ((c ^ (m & 7)) << 4),
+                     Yg + static_cast<int64_t>(m < rows ? m : 0) * p.ldy + s * kMmaKC + c * 8, m < rows);
+  };
+  // B and y_old of the whole ring before the PDL wait (y_old is final: see the header)
+  const int pre = min(S, nst);
+  for (int s = 0; s < pre; ++s) {
+    load_b(s);
+    load_y(s);
+    cp_async_arrive(&full[s]);
+  }
+  LSG_TC_TRACE(1, 1);
+  pdl_wait();  // the partials
+  pdl_launch_dependents();
+  LSG_TC_TRACE(1, 2);
+  {  // v = sum of the partials in ks order -> 16-bit hi + lo, swizzled rows of R values
+    const float* src = p.ws + static_cast<int64_t>(blockIdx.y) * p.kparts * kMmaM * R;
+    for (int i = tid * 8; i < kMmaM * R; i += kMmaThreads * 8) {
+      float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int q = 0; q < p.kparts; ++q) {
+        const float4 u = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i);
+        const float4 w = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i + 4);
+        f[0] += u.x, f[1] += u.y, f[2] += u.z, f[3] += u.w, f[4] += w.x, f[5] += w.y, f[6] += w.z, f[7] += w.w;
+      }
+      float hf[8], lo[8];
+      const uint4 hi = Cvt<T>::pack8(f);
+      Cvt<T>::unpack8(hi, hf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) lo[e] = f[e] - hf[e];
+      const int m = i / R, c = (i - m * R) >> 3;
+      const uint32_t off = m * (R * 2) + ((c ^ mma_swz<CPR>(m)) << 4);
+      *reinterpret_cast<uint4*>(vhi + off) = hi;
+      *reinterpret_cast<uint4*>(vlo + off) = Cvt<T>::pack8(lo);
+    }
+  }
+  __syncthreads();
+  LSG_TC_TRACE(1, 3);
+  // A fragments of v (hi and lo) for every k16-step: R/16 steps
+  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = lane >> 4;
+  uint32_t ah[R / 16][4], al[R / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < R / 16; ++kk) {
+    const int c = 2 * kk + lc;
+    const uint32_t off = lr * (R * 2) + ((c ^ mma_swz<CPR>(lr)) << 4);
+    ldsm_x4(smem_u32(vhi + off), ah[kk][0], ah[kk][1], ah[kk][2], ah[kk][3]);
+    ldsm_x4(smem_u32(vlo + off), al[kk][0], al[kk][1], al[kk][2], al[kk][3]);
+  }
+  const int g = lane >> 2, t = lane & 3;
+  for (int s = 0; s < nst; ++s) {
+    const int b = s % S;
+    mbar_wait(&full[b], (s / S) & 1);
+    uint8_t* bs = smem + b * kSB;
+    uint8_t* ys = bs + kBB;
+    // warp w: columns 16w .. 16w+15 of the stage (n8 tiles 2w, 2w+1)
+    float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < R / 16; ++kk) {
+      const int k = 16 * kk + lr, c = 2 * warp + lc;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(smem_u32(bs + k * 128 + ((c ^ (k & 7)) << 4)), b0, b1, b2, b3);
+      mma16816<T>(d[0], ah[kk], b0, b1);
+      mma16816<T>(d[1], ah[kk], b2, b3);
+      mma16816<T>(d[0], al[kk], b0, b1);
+      mma16816<T>(d[1], al[kk], b2, b3);
+    }
+    // epilogue in place: y = rn(D + y_old), rows g and g + 8, columns 2t, 2t+1 of chunk 2w + j
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = 2 * warp + j;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = g + 8 * h;
+        uint32_t* q = reinterpret_cast<uint32_t*>(ys + m * 128 + ((c ^ (m & 7)) << 4) + 4 * t);
+        *q = add2_round<T>(*q, d[j][2 * h], d[j][2 * h + 1]);
+      }
+    }
+    __syncthreads();  // the stage's y tile is complete
+    {  // 16-byte stores of the valid rows: thread = (row, chunk)
+      const int m = tid >> 3, c = tid & 7;
+      if (m < rows)
+        st_global_v4(Yg + static_cast<int64_t>(m) * p.ldy + s * kMmaKC + c * 8,
+                     *reinterpret_cast<const uint4*>(ys + m * 128 + ((c ^ (m & 7)) << 4)));
+    }
+    __syncthreads();  // buffer b is free
+    if (s == 0) LSG_TC_TRACE(1, 4);
+    if (s + S < nst) {
+      load_b(s + S);
+      load_y(s + S);
+      cp_async_arrive(&full[b]);
+    }
+  }
+  LSG_TC_TRACE(1, 5);
+}
+
+}  // namespace lsg

@@ -100,19 +100,21 @@ def _rows_check(x: torch.Tensor | None, y: torch.Tensor | None, pool: AdapterPoo
 
 
 def call_opts(pdl: bool | None = None, tc_min_rows: int | None = None,
-              no_tensor_cores: bool | None = None) -> "_lib.CallOpts":
+              no_tensor_cores: bool | None = None, mma_min_rows: int | None = None) -> "_lib.CallOpts":
     """Per-call options (``lsg_call_opts``); ``None`` keeps the process default."""
     return _lib.CallOpts(-1 if pdl is None else int(bool(pdl)), -1 if tc_min_rows is None else int(tc_min_rows),
-                         -1 if no_tensor_cores is None else int(bool(no_tensor_cores)))
+                         -1 if no_tensor_cores is None else int(bool(no_tensor_cores)),
+                         -1 if mma_min_rows is None else int(mma_min_rows))
 
 
 def sgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.Tensor,
          seg_slot: torch.Tensor, layer: int, num_segments: int | None = None, *, pdl: bool | None = None,
-         tc_min_rows: int | None = None, no_tensor_cores: bool | None = None) -> torch.Tensor:
+         tc_min_rows: int | None = None, no_tensor_cores: bool | None = None,
+         mma_min_rows: int | None = None) -> torch.Tensor:
     """y += x . A_slot . B_slot per segment (fused shrink+expand, one launch).
 
-    ``pdl`` / ``tc_min_rows`` / ``no_tensor_cores`` override the process defaults
-    (``set_option``) for this call only (``lsg_sgmv_ex``)."""
+    ``pdl`` / ``tc_min_rows`` / ``no_tensor_cores`` / ``mma_min_rows`` override the process
+    defaults (``set_option``) for this call only (``lsg_sgmv_ex``)."""
     _rows_check(x, y, pool)
     _check_i32(seg_starts, "seg_starts")
     _check_i32(seg_slot, "seg_slot")
@@ -121,7 +123,7 @@ def sgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, seg_starts: torch.
     # it comes from torch's caching allocator (stream-ordered, graph-capture safe).
     wsb = sgmv_workspace_size(pool, x.shape[0])
     ws = torch.empty(wsb, dtype=torch.uint8, device=x.device) if wsb else None
-    opts = call_opts(pdl, tc_min_rows, no_tensor_cores)
+    opts = call_opts(pdl, tc_min_rows, no_tensor_cores, mma_min_rows)
     _lib.call("lsg_sgmv_ex", _ptr(y), y.stride(0), _ptr(x), x.stride(0), C.byref(pool.table), _ptr(seg_starts),
               _ptr(seg_slot), n, x.shape[0], layer, _ptr(ws) if ws is not None else None, wsb, C.byref(opts),
               _stream())

@@ -141,16 +141,23 @@ def nccl_library() -> C.CDLL:
     raise RuntimeError("libnccl.so.2 not found")
 
 
+class _NcclUniqueId(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]  # ncclUniqueId (nccl.h): passed BY VALUE to ncclCommInitRank
+
+
 def nccl_comm_single() -> int:
     """A one-rank ncclComm_t (tests of the NCCL plumbing on one GPU)."""
     L = nccl_library()
-    uid = (C.c_char * 128)()
-    if L.ncclGetUniqueId(uid) != 0:
+    uid = _NcclUniqueId()
+    L.ncclGetUniqueId.argtypes = [C.POINTER(_NcclUniqueId)]
+    if L.ncclGetUniqueId(C.byref(uid)) != 0:
         raise RuntimeError("ncclGetUniqueId failed")
     comm = C.c_void_p()
-    L.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_char * 128, C.c_int]
-    if L.ncclCommInitRank(C.byref(comm), 1, uid, 0) != 0:
-        raise RuntimeError("ncclCommInitRank failed")
+    L.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, _NcclUniqueId, C.c_int]
+    rc = L.ncclCommInitRank(C.byref(comm), 1, uid, 0)
+    if rc != 0:
+        L.ncclGetErrorString.restype = C.c_char_p
+        raise RuntimeError(f"ncclCommInitRank failed ({rc}: {L.ncclGetErrorString(rc).decode()})")
     return comm.value
 
 

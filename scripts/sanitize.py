@@ -10,6 +10,7 @@ the sanitizer but computes garbage still fails.  Families covered:
   sgmv_fast_kernel   fused / shrink / expand x item modes (row, row-split, tile-scan,
                      BGMV, grouped row) x tile rows 1 / 4 / 8, clusters 1..16, PDL on/off
   sgmv_tc_*          fused tensor-core kernel (rank 16), two-kernel form (rank 32 / split)
+  sgmv_mma_*         segment-tile MMA pair (ranks 16 / 32 / 64, short and long segments)
   dense_lora         tcgen05 GEMM with the LoRA epilogue
   build_segments     K6 builder, permute_rows gather / scatter
   sgmv_generic       odd shapes
@@ -98,7 +99,10 @@ def fused_cases():
                 lsg.set_option(opt, 0)
             rs = torch.repeat_interleave(sl, torch.tensor(np.diff(bounds.astype(np.int64)), device=dev)).to(torch.int32)
             y = torch.zeros(batch, 256, dtype=torch.float16, device=dev)
+            if lsg.query_launch(pool, len(bounds) - 1, batch, lsg.KERNEL_BGMV)["cluster"] > MAX_C:
+                lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, MAX_C)
             lsg.bgmv(y, x, pool, rs, 0)
+            lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, 0)
             check(f"bgmv r{r} pop{pop}", y, ref)
     # rank 64 with shared adapters: the automatic 4-row tiles (c3's plan)
     bounds, _, _ = segments_for(SKEWED, 24, 5)
@@ -131,6 +135,22 @@ def tc_cases():
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, 0)
     lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 0)
     lsg.set_option(lsg.LSG_OPT_PDL, 0)
+
+
+def mma_cases():
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, 1)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 3)
+    for r in (16, 32, 64):
+        for lens in ((3, 3, 3), (130, 3, 1), (1, 17, 40)):
+            bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+            pool, x, ss, sl, ref = problem(512, 256, r, bounds, 50 + r)
+            for pdl in (0, 1):
+                lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+                y = torch.zeros(int(bounds[-1]), 256, dtype=torch.float16, device=dev)
+                lsg.sgmv(y, x, pool, ss, sl, 0)
+                check(f"mma pair r{r} lens{lens} pdl{pdl}", y, ref)
+    for opt in (lsg._lib.LSG_OPT_MMA_MIN_ROWS, lsg._lib.LSG_OPT_TC_LEGACY, lsg.LSG_OPT_PDL):
+        lsg.set_option(opt, 0)
 
 
 def dense_cases():
@@ -185,7 +205,7 @@ def main():
     if sys.argv[1:2] == ["one"]:
         one_cases()
         sys.exit(1 if failures else 0)
-    which = sys.argv[1:] or ["fused", "grouped", "tc", "dense", "builder", "generic"]
+    which = sys.argv[1:] or ["fused", "grouped", "tc", "mma", "dense", "builder", "generic"]
     for w in which:
         globals()[f"{w}_cases"]()
     print(f"sanitize cases done: {len(failures)} numerical failures", flush=True)

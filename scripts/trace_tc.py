@@ -18,6 +18,8 @@ SHRINK = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "partials_in",
 EXPAND = ["entry", "weights_staged", "pdl_wait_done", "y_landed", "d2_ready", "end"]
 
 
+MMA_P = ["entry", "a_issued", "pdl_wait_done", "stage0_landed", "mma_done", "end"]
+MMA_E = ["entry", "b_y_issued", "pdl_wait_done", "v_ready", "stage0_stored", "end"]
 FUSED = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "v_ready", "chunk0_ready", "chunk1_ready",
          "end"]
 
@@ -30,11 +32,15 @@ def main():
     ap.add_argument("--sites", type=int, default=16)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--split", type=int, default=0, help="1: two-kernel path (LSG_OPT_TC_SPLIT)")
-    ap.add_argument("--gen", type=int, default=0, help="LSG_OPT_TC_LEGACY: 0 cluster-free pair, 1 fused, 2 streamed")
+    ap.add_argument("--gen", type=int, default=0,
+                    help="LSG_OPT_TC_LEGACY: 0 cluster-free pair, 1 fused, 2 streamed, 3 segment-tile MMA pair")
+    ap.add_argument("--mma-min-rows", type=int, default=0, help="LSG_OPT_MMA_MIN_ROWS")
     a = ap.parse_args()
     lsg.set_option(_lib.LSG_OPT_TC_SPLIT, a.split)
     lsg.set_option(_lib.LSG_OPT_TC_LEGACY, a.gen)
-    two = a.split or a.gen == 0
+    lsg.set_option(_lib.LSG_OPT_MMA_MIN_ROWS, a.mma_min_rows)
+    mma = a.gen == 3 or a.mma_min_rows > 0 or a.rank == 64
+    two = a.split or a.gen in (0, 3) or mma
     lsg.set_option(lsg.LSG_OPT_PDL, a.pdl)
     lens = [int(v) for v in a.segments.split(",")]
     bounds = [0]
@@ -72,7 +78,8 @@ def main():
     torch.cuda.synchronize()
     allt = buf.view(2 * ctas, 16).cpu().double()
     t0 = None
-    groups = ((("shrink", SHRINK, allt[ctas:ctas + ctas // 2]), ("expand", EXPAND, allt[ctas + ctas // 2:]))
+    names = (MMA_P, MMA_E) if mma else (SHRINK, EXPAND)
+    groups = ((("shrink", names[0], allt[ctas:ctas + ctas // 2]), ("expand", names[1], allt[ctas + ctas // 2:]))
               if two else (("fused", FUSED, allt[ctas:ctas + ctas // 2]),))
     for name, phases, part in groups:
         tv = part[part[:, len(phases) - 1] != 0]

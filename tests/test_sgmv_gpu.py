@@ -36,7 +36,7 @@ def _reset_options(lsg):
     yield
     for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
                 lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE,
-                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES, lsg._lib.LSG_OPT_TC_LEGACY):
+                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES, lsg._lib.LSG_OPT_TC_LEGACY, lsg._lib.LSG_OPT_MMA_MIN_ROWS):
         lsg.set_option(opt, 0)
 
 
@@ -519,13 +519,20 @@ def test_grouped_sites_fall_back_with_long_segments(lsg):
         assert row_norm_err(ys[i].double().cpu().numpy(), probs[i].reference()) <= tol(torch.bfloat16)
 
 
+NO_MMA = 1 << 30  # LSG_OPT_MMA_MIN_ROWS value that keeps every segment off the MMA pair
+
+
 @pytest.mark.parametrize("h", [4096, 8192])
 def test_rank64_multirow_tiles_large_hidden(lsg, h):
-    """Multi-row rank-64 tiles at h = 8192 need a cluster above the tile-row cap to fit
-    shared memory: still correct and bitwise the one-row result."""
+    """Rank 64 with shared adapters: the default MMA pair, and (MMA pair off) the CUDA-core
+    multi-row tiles, which at h = 8192 need a cluster above the tile-row cap to fit shared
+    memory -- both correct, the CUDA-core tiles bitwise the one-row result."""
     bounds, _, _ = segments_for(UNIFORM, 32, 93)
     x, A, B = random_problem(h, h, 64, bounds, 94)
     p = Problem(lsg, x, A, B, bounds, torch.bfloat16)
+    mma = p.run()
+    assert row_norm_err(mma.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, NO_MMA)
     base = p.run()
     assert row_norm_err(base.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 1)
@@ -535,11 +542,12 @@ def test_rank64_multirow_tiles_large_hidden(lsg, h):
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("pop", [UNIFORM, SKEWED])
 def test_rank64_multirow_tiles_bitwise_one_row(lsg, dtype, pop):
-    """Rank 64 with shared adapters runs 8-row tiles (one weight read per tile): bitwise
-    the one-row-per-cluster result, for every cluster size."""
+    """Rank 64 with shared adapters on the CUDA-core kernel (MMA pair off) runs 8-row tiles
+    (one weight read per tile): bitwise the one-row-per-cluster result, for every cluster size."""
     bounds, _, _ = segments_for(pop, 64, 91)
     x, A, B = random_problem(5120, 5120, 64, bounds, 92)
     p = Problem(lsg, x, A, B, bounds, dtype)
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, NO_MMA)
     base = p.run()
     assert row_norm_err(base.double().cpu().numpy(), p.reference()) <= tol(dtype)
     lsg.set_option(lsg.LSG_OPT_FORCE_TILE_ROWS, 1)
@@ -876,3 +884,72 @@ def test_tp_nccl_allgather_single_rank_comm(lsg):
     tpmod.tp_sgmv_nccl(y, p.x, tpmod.tp_pool(p.pool.a, p.pool.b, 1, 0), p.seg_starts, p.seg_slot, 0, 0, 1, comm)
     torch.cuda.synchronize()
     assert torch.equal(y, base)
+
+
+# ---------------------------------------------------------------------------------
+# Segment-tile MMA pair (K7, sgmv_mma.cuh): shared-adapter and prefill segments
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", [(4096, 4096, 16), (4096, 4096, 32), (5120, 5120, 64), (4096, 2048, 64),
+                                   (8192, 8192, 16)])
+@pytest.mark.parametrize("pop", [UNIFORM, SKEWED, IDENTICAL])
+def test_mma_pair_shared_adapters_match_oracle(lsg, dtype, shape, pop):
+    """Every segment on the MMA pair (LSG_OPT_MMA_MIN_ROWS = 1; rank 64's default when rows
+    share adapters): within tolerance of the fp64 oracle, run-to-run identical, and y
+    accumulates onto y_old."""
+    h_in, h_out, r = shape
+    bounds, _, _ = segments_for(pop, 64, 500 + pop)
+    x, A, B = random_problem(h_in, h_out, r, bounds, 501 + pop)
+    y0 = oracle().rng(502).fill_pm1(64 * h_out).reshape(64, h_out)
+    p = Problem(lsg, x, A, B, bounds, dtype, y0=y0)
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, 1)
+    y = p.run()
+    assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(dtype)
+    assert torch.equal(p.run(), y)
+    if r == 64:  # the automatic choice is the same pair
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, 0)
+        assert torch.equal(p.run(), y)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("r", [16, 32, 64])
+@pytest.mark.parametrize("lens", [[128] + [1] * 31, [300, 17, 1, 5, 2, 16], [2048, 3, 1]])
+def test_mma_pair_long_segments_match_oracle(lsg, dtype, r, lens):
+    """LSG_OPT_TC_LEGACY = 3: the MMA pair takes the long (prefill) segments as well; with
+    LSG_OPT_MMA_MIN_ROWS = 2 the 1-row segments stay on the CUDA-core kernel in the same call."""
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(4096, 4096, r, bounds, 600 + r)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 3)
+    for lo in (1, 2):
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, lo)
+        y = p.run()
+        assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(dtype), lo
+
+
+def test_mma_pair_no_adapter_segments_untouched_and_scattered_slots(lsg):
+    """Slot -1 segments leave y untouched on the MMA pair; scattered slots of a multi-layer
+    pool at a non-zero layer index correctly."""
+    lens = [9, 16, 17, 1, 33, 4]
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    slots = [7, -1, 2, 11, -1, 0]
+    x, A, B = random_problem(5120, 5120, 64, bounds, 610)
+    y0 = oracle().rng(611).fill_pm1(sum(lens) * 5120).reshape(sum(lens), 5120)
+    p = Problem(lsg, x, A, B, bounds, torch.float16, slots=slots, num_slots=12, layers=3, layer=2, y0=y0)
+    y = p.run()
+    ref = p.reference()
+    assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(torch.float16)
+    for s in (1, 4):
+        a, b = int(bounds[s]), int(bounds[s + 1])
+        assert torch.equal(y[a:b], p.y0[a:b]), s
+
+
+def test_mma_pair_many_tiles_and_workspace_bound(lsg):
+    """Hundreds of 16-row tiles (the tile bound grows with the segment count) through the
+    caller-workspace entry (lsg_sgmv_workspace_size is an upper bound)."""
+    lens = [(29 * i) % 61 + 2 for i in range(120)]
+    bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    x, A, B = random_problem(1024, 2048, 64, bounds, 620)
+    p = Problem(lsg, x, A, B, bounds, torch.bfloat16)
+    y = p.run()
+    assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
