@@ -232,10 +232,21 @@ int mma_split(int nstages, int tiles) {
     if (nstages % d == 0 && static_cast<int64_t>(tiles) * d <= 160) best = d;
   return best;
 }
-// workspace bound: tiles * kparts <= max(160, tiles)
+// workspace bound: tiles * kparts (and tiles * ncol) <= max(160, tiles): the partials plus
+// one 128-byte weight descriptor per CTA of each kernel
 size_t mma_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg, int lo) {
-  const int tiles = mma_tile_bound(s_n, n_seg, lo);
-  return static_cast<size_t>(std::max(160, tiles)) * kMmaM * t->rank * sizeof(float);
+  const size_t ctas = static_cast<size_t>(std::max(160, mma_tile_bound(s_n, n_seg, lo)));
+  return ctas * kMmaM * t->rank * sizeof(float) + 2 * ctas * 128;
+}
+bool encode_map_2d(CUtensorMap* m, int dtype, const void* base, uint64_t cols, uint64_t rows, uint64_t ld_elems,
+                   uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld_elems * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode_tiled_fn()(m, dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 constexpr uint32_t kMmaSmemTarget = 100 * 1024;  // two CTAs per SM
 int mma_stages(uint32_t fixed, uint32_t stage, int nst) {
@@ -246,15 +257,23 @@ bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_
                  const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg, int s_n,
                  int layer, void* ws, size_t ws_bytes) {
   if (rr.mma_lo == 0) return false;
-  if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0) return false;
+  if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
   tiles = mma_tile_bound(s_n, n_seg, rr.mma_lo);
   if (tiles > kMaxGridY) return false;
   if (ws == nullptr || !aligned16(ws) || ws_bytes < mma_ws_bytes(tbl, s_n, n_seg, rr.mma_lo)) return false;
   const int R = tbl->rank;
   mp = MmaParams{};
+  // activations: per-call maps; weights: templates (any valid base; the kernels patch in
+  // each slot's address), A [h_in][R] rows swizzled by their own width, B [R][h_out] SW128
+  const CUtensorMapSwizzle swa = R == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : R == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B;
+  if (!encode_map_2d(&mp.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx, kMmaKC, kMmaM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_map_2d(&mp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy, kMmaKC, kMmaM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_map_2d(&mp.tmap_a, tbl->dtype, x, R, tbl->h_in, R, R, kMmaKC, swa) ||
+      !encode_map_2d(&mp.tmap_b, tbl->dtype, x, tbl->h_out, R, tbl->h_out, kMmaKC, R, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   mp.y = y;
-  mp.x = x;
-  mp.ldx = ldx;
   mp.ldy = ldy;
   mp.a_ptr = tbl->a_ptr;
   mp.b_ptr = tbl->b_ptr;
@@ -263,6 +282,9 @@ bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_
   mp.seg_starts = seg_starts;
   mp.seg_slot = seg_slot;
   mp.ws = static_cast<float*>(ws);
+  const size_t ctas = static_cast<size_t>(std::max(160, tiles));
+  mp.maps_p = static_cast<uint8_t*>(ws) + ctas * kMmaM * R * sizeof(float);
+  mp.maps_e = mp.maps_p + ctas * 128;
   mp.n_seg = n_seg;
   mp.s_n = s_n;
   mp.num_slots = tbl->num_slots;

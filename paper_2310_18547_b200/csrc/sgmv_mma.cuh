@@ -8,35 +8,42 @@
 //
 //   partials  grid (kparts, tile bound), 128 threads.  CTA (ks, t) computes the partial
 //             P_ks[16][R] = x[tile rows, K slice ks] . A[K slice ks, :] over its K slice of
-//             KS = h_in / kparts columns, in stages of 64 columns (x 16 x 64 and A 64 x R,
-//             both cp.async'd into XOR-swizzled shared memory so ldmatrix is conflict-free;
-//             the A stages of the whole ring are requested BEFORE the PDL wait).  Warp w
-//             takes k16-step w of every stage; the four warp accumulators are summed in warp
-//             order and P_ks goes to the workspace [tile][ks][16][R] fp32 (L2-resident).
+//             KS = h_in / kparts columns, in stages of 64 columns (x 16 x 64 and A 64 x R)
+//             moved by 2-D TMA into swizzled shared memory (the hardware swizzle makes the
+//             ldmatrix fragment loads conflict-free); the A stages of the whole ring are
+//             requested BEFORE the PDL wait.  Warp w takes k16-step w of every stage; the
+//             four warp accumulators are summed in warp order and P_ks goes to the workspace
+//             [tile][ks][16][R] fp32 (L2-resident).
 //   expand    grid (ncol, tile bound), 128 threads.  CTA (j, t) stages its B column slice
-//             (R x NC) and y_old (16 x NC) before its PDL wait -- the partials kernel
+//             (R x NC) and y_old (16 x NC) by TMA before its PDL wait -- the partials kernel
 //             triggers its dependents only after its own wait, so every kernel before it has
 //             completed and y_old is final -- then sums the tile's partials in ks order
-//             (v, fp32), splits v into 16-bit hi + lo (hi = rn(v), lo = rn(v - hi)) and
-//             runs D = hi.B + lo.B on the tensor cores (the lo term keeps v's fp32
-//             precision), adds y_old in fp32 and rounds once.  Stores are 16-byte vectors of
-//             the tile's valid rows only.
+//             (v, fp32), splits v into 16-bit hi + lo (hi = rn(v), lo = rn(v - hi)) and runs
+//             D = hi.B + lo.B on the tensor cores (the lo term keeps v's fp32 precision),
+//             adds y_old in fp32 and rounds once.  Stores are 16-byte vectors of the tile's
+//             valid rows only.
+//
+// Adapter weights are addressed through per-slot pointers (a_ptr[slot]), so their TMA
+// descriptors are made on the device: the host encodes one template per operand (shape,
+// strides, box, swizzle) and every CTA patches the global address of its slot into a copy
+// (tensormap.replace in shared memory, then tensormap.cp_fenceproxy to its own 128-byte
+// global scratch, fence.proxy.tensormap acquire) before its first weight load.
 //
 // Why this shape: a shared-adapter segment is weight-bound (h=5120 r=64: 1.25 MiB of A+B
 // per segment against 8 rows x 20 KiB of activations), so the weights of one tile are
 // spread over kparts x ncol CTAs (about one per SM) instead of one cluster; long prefill
 // segments are activation-bound and get one CTA per 16-row tile with the whole K (or N)
 // range streamed through a ring.  The same two kernels cover both with different splits
-// (lsg_api.cu: mma_plan).
+// (lsg_api.cu: prepare_mma).
 //
-// Canonical arithmetic for these rows (deterministic; depends only on the shape, never on
-// the batch composition or the launch): v = sum over parts ks ascending of
-// (sum over warps w ascending of the MMA chain of k16-steps w, w+4, ... of part ks);
-// y = rn(fp32(hi.B + lo.B) + y_old).  Within tolerance of the CUDA-core rows, not bitwise.
+// Canonical arithmetic for these rows (deterministic; depends only on the shape and the
+// split, never on the batch composition): v = sum over parts ks ascending of (sum over warps
+// w ascending of the MMA chain of k16-steps w, w+4, ... of part ks); y = rn(fp32(hi.B +
+// lo.B) + y_old).  Within tolerance of the CUDA-core rows, not bitwise.
 #pragma once
 
 #include "sgmv_device.cuh"
-#include "sgmv_tc.cuh"  // LSG_TC_TRACE
+#include "sgmv_tc.cuh"  // TMA helpers, LSG_TC_TRACE
 
 namespace lsg {
 
@@ -45,17 +52,21 @@ constexpr int kMmaThreads = 128;  // 4 warps
 constexpr int kMmaKC = 64;        // columns per pipeline stage (4 k16-steps: one per warp)
 
 struct MmaParams {
+  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 16, SW128
+  CUtensorMap tmap_y;  // y [s_n, h_out], box 64 x 16, SW128
+  CUtensorMap tmap_a;  // template: A of one layer [h_in, R], box R x 64, swizzle = R * 2 bytes
+  CUtensorMap tmap_b;  // template: B of one layer [R, h_out], box 64 x R, SW128
   void* y;
-  const void* x;
-  int64_t ldx;
   int64_t ldy;
   const void* const* a_ptr;
   const void* const* b_ptr;
-  int64_t a_off;  // layer * a_layer_stride
+  int64_t a_off;  // layer * a_layer_stride (elements)
   int64_t b_off;
   const int32_t* seg_starts;
   const int32_t* seg_slot;
-  float* ws;  // [tile bound][kparts][16][R] fp32 partials
+  float* ws;        // [tile bound][kparts][16][R] fp32 partials
+  uint8_t* maps_p;  // 128-byte descriptor scratch per partials CTA
+  uint8_t* maps_e;  // ... per expand CTA
   int32_t n_seg, s_n, num_slots, h_in, h_out;
   int32_t kparts;    // K slices (gridDim.x of the partials kernel)
   int32_t ncol;      // column slices (gridDim.x of the expand kernel)
@@ -113,24 +124,28 @@ __device__ __forceinline__ uint32_t add2_round<__nv_bfloat16>(uint32_t y, float 
   return *reinterpret_cast<const uint32_t*>(&r);
 }
 
-// 16-byte cp.async that zero-fills instead of reading when !valid (rows past a tile's end)
-__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-// arrive on `bar` once all of this thread's earlier cp.async copies have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Swizzle of a row of CPR 16-byte chunks (CPR = 2, 4, 8): chunk c of row k lives at chunk
-// c ^ mma_swz<CPR>(k).  Any 8 consecutive rows (aligned) then hit 8 distinct 16-byte bank
-// groups for a fixed logical chunk -- ldmatrix (plain or .trans) is conflict-free.
-template <int CPR>
-__device__ __forceinline__ int mma_swz(int k) {
-  static_assert(CPR == 2 || CPR == 4 || CPR == 8, "chunks per row");
-  return (k >> (CPR == 8 ? 0 : CPR == 4 ? 1 : 2)) & (CPR - 1);
+// ---- device-made TMA descriptors for per-slot weights -------------------------------------
+// Warp-wide (tensormap.cp_fenceproxy is .sync.aligned): copy the template `tmpl` (kernel
+// parameter) into `smem_map` (128 bytes, 128-aligned), patch its global address, publish it
+// to `gmem_map` (this CTA's scratch) with a release fence, then acquire it for the TMA
+// proxy.  Returns with `gmem_map` usable by this warp's lane 0.
+__device__ __forceinline__ void make_slot_tmap(const CUtensorMap* tmpl, uint8_t* smem_map, uint8_t* gmem_map,
+                                               const void* base, int lane) {
+  if (lane < 8) reinterpret_cast<uint4*>(smem_map)[lane] = reinterpret_cast<const uint4*>(tmpl)[lane];
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("tensormap.replace.tile.global_address.shared::cta.b1024.b64 [%0], %1;" ::"r"(smem_u32(smem_map)),
+                 "l"(reinterpret_cast<uint64_t>(base))
+                 : "memory");
+  __syncwarp();
+  asm volatile(
+      "tensormap.cp_fenceproxy.global.shared::cta.tensormap::generic.release.gpu.sync.aligned [%0], [%1], 128;" ::"l"(
+          reinterpret_cast<uint64_t>(gmem_map)),
+      "r"(smem_u32(smem_map))
+      : "memory");
+  if (lane == 0)
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(gmem_map))
+                 : "memory");
 }
 
 // Tile t -> (segment, tile within it) over the segments with min_rows <= len < max_rows,
@@ -164,29 +179,32 @@ __device__ __forceinline__ void mma_tile_of(const int32_t* seg_starts, int n_seg
 }
 
 // ---- shared-memory plans (host and device) -----------------------------------------------
+// Stage sizes are multiples of 1024 bytes (the 128-byte swizzle atom), buffers 1024-aligned.
 __host__ __device__ constexpr uint32_t mma_part_stage_bytes(int R) { return kMmaM * kMmaKC * 2 + kMmaKC * R * 2; }
 __host__ __device__ constexpr uint32_t mma_exp_stage_bytes(int R) { return R * kMmaKC * 2 + kMmaM * kMmaKC * 2; }
-// partials: [ring stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, barriers
+// partials: [ring stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, map, barriers
 __host__ __device__ constexpr uint32_t mma_part_smem(int R, int stages) {
-  return stages * mma_part_stage_bytes(R) + 4 * kMmaM * R * 4 + 2 * 8 * 32 + 128;
+  return 1024 + stages * mma_part_stage_bytes(R) + 4 * kMmaM * R * 4 + 128 + 8 * 32;
 }
-// expand: [ring stages][B 128R B | y 2 KB], v hi / lo (16 x R 16-bit each), barriers
+// expand: [ring stages][B 128R B | y 2 KB], v hi / lo (16 x R 16-bit each), map, barriers
 __host__ __device__ constexpr uint32_t mma_exp_smem(int R, int stages) {
-  return stages * mma_exp_stage_bytes(R) + 2 * kMmaM * R * 2 + 2 * 8 * 32 + 128;
+  return 1024 + stages * mma_exp_stage_bytes(R) + 2 * kMmaM * R * 2 + 128 + 8 * 32;
 }
 constexpr int kMmaMaxStages = 32;
 
 template <typename T, int R>
 __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid_constant__ MmaParams p) {
   static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
-  constexpr int CPR = R / 8;                     // 16-byte chunks per A row
+  constexpr int ROWB = R * 2;                    // bytes per A row (= its TMA swizzle span)
   constexpr uint32_t kXB = kMmaM * kMmaKC * 2;   // x stage bytes
   constexpr uint32_t kSB = mma_part_stage_bytes(R);
   constexpr int NT = R / 8;                      // n8 tiles of the accumulator
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
   const int S = p.stages_p;
-  float* red = reinterpret_cast<float*>(smem + S * kSB);                     // [4][16][R]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kSB + 4 * kMmaM * R * 4);  // [S] stage landed
+  float* red = reinterpret_cast<float*>(smem + S * kSB);     // [4][16][R]
+  uint8_t* smap = smem + S * kSB + 4 * kMmaM * R * 4;        // 128 B
+  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);  // [S] stage landed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ks = static_cast<int>(blockIdx.x);
   const int KS = p.h_in / p.kparts, nst = KS / kMmaKC;
@@ -201,8 +219,8 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
       s_tile = tin;
     }
   }
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], kMmaThreads);
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -217,39 +235,28 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
     return;
   }
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
-  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
   const int k0 = ks * KS;
-  const T* A = static_cast<const T*>(p.a_ptr[slot]) + p.a_off + static_cast<int64_t>(k0) * R;
-  const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx + k0;
-
-  auto load_a = [&](int s) {  // stage s of A: 64 rows x R, swizzled
-    uint8_t* dst = smem + (s % S) * kSB + kXB;
-    const T* src = A + static_cast<int64_t>(s) * kMmaKC * R;
-    for (int i = tid; i < kMmaKC * CPR; i += kMmaThreads) {
-      const int k = i / CPR, c = i - k * CPR;
-      cp_async16(dst + k * (R * 2) + ((c ^ mma_swz<CPR>(k)) << 4), src + static_cast<int64_t>(i) * 8);
-    }
-  };
-  auto load_x = [&](int s) {  // stage s of x: 16 rows x 64 columns, swizzled, zero rows past the tile
-    uint8_t* dst = smem + (s % S) * kSB;
-    const int m = tid >> 3, c = tid & 7;  // 128 threads = 16 rows x 8 chunks
-    cp_async16_zfill(dst + m * 128 + ((c ^ (m & 7)) << 4), X + static_cast<int64_t>(m < rows ? m : 0) * p.ldx +
-                                                                 s * kMmaKC + c * 8,
-                     m < rows);
-  };
-  // weights first (before the PDL wait): the whole ring of A stages
   const int pre = min(S, nst);
-  for (int s = 0; s < pre; ++s) load_a(s);
+  uint8_t* gmap = p.maps_p + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 128;
+  const CUtensorMap* amap = reinterpret_cast<const CUtensorMap*>(gmap);
+  if (warp == 0) {
+    // weights first (before the PDL wait): this slot's A descriptor, then the ring's A stages
+    make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
+    if (lane == 0) {
+      for (int s = 0; s < pre; ++s) {
+        mbar_arrive_expect_tx(&full[s], kSB);
+        tma_load_2d(smem + s * kSB + kXB, amap, 0, k0 + s * kMmaKC, &full[s]);
+      }
+    }
+  }
   LSG_TC_TRACE(0, 1);
   pdl_wait();  // x may come from the preceding kernel
-  LSG_TC_TRACE(0, 2);
   // Dependents (the expand) start now: every kernel before this one has completed, so the
   // expand may stage y_old before its own wait (it waits only for these partials).
   pdl_launch_dependents();
-  for (int s = 0; s < pre; ++s) {
-    load_x(s);
-    cp_async_arrive(&full[s]);
-  }
+  LSG_TC_TRACE(0, 2);
+  if (tid == 0)
+    for (int s = 0; s < pre; ++s) tma_load_2d(smem + s * kSB, &p.tmap_x, k0 + s * kMmaKC, r0, &full[s]);
 
   float acc[NT][4];
 #pragma unroll
@@ -262,23 +269,24 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
     if (s == 0) LSG_TC_TRACE(0, 3);
     const uint32_t xs = smem_u32(smem + b * kSB), as = xs + kXB;
     uint32_t a[4];
-    {  // x rows 0..15, k16-step `warp` of this stage: chunks 2w, 2w+1
+    {  // x rows 0..15, k16-step `warp` of this stage: chunks 2w, 2w+1 (128-byte rows, SW128)
       const int c = 2 * warp + lc;
       ldsm_x4(xs + lr * 128 + ((c ^ (lr & 7)) << 4), a[0], a[1], a[2], a[3]);
     }
 #pragma unroll
-    for (int j = 0; j < NT; j += 2) {  // A rows 16w..16w+15, n8 tiles j, j+1
+    for (int j = 0; j < NT; j += 2) {  // A rows 16w..16w+15, n8 tiles j, j+1 (ROWB-byte rows, swizzled)
       const int k = 16 * warp + lr, c = j + lc;
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(as + k * (R * 2) + ((c ^ mma_swz<CPR>(k)) << 4), b0, b1, b2, b3);
+      ldsm_x4_t(as + k * ROWB + ((c ^ swz<ROWB>(k)) << 4), b0, b1, b2, b3);
       mma16816<T>(acc[j], a, b0, b1);
       mma16816<T>(acc[j + 1], a, b2, b3);
     }
     __syncthreads();  // every warp is done with buffer b
-    if (s + S < nst) {
-      load_a(s + S);
-      load_x(s + S);
-      cp_async_arrive(&full[b]);
+    if (s + S < nst && tid == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&full[b], kSB);
+      tma_load_2d(smem + b * kSB + kXB, amap, 0, k0 + (s + S) * kMmaKC, &full[b]);
+      tma_load_2d(smem + b * kSB, &p.tmap_x, k0 + (s + S) * kMmaKC, r0, &full[b]);
     }
   }
   // ---- sum the four warp accumulators in warp order, write the partial ------------------
@@ -309,14 +317,16 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
 template <typename T, int R>
 __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_constant__ MmaParams p) {
   static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
-  constexpr int CPR = R / 8;
+  constexpr int ROWV = R * 2;               // bytes per v row
   constexpr uint32_t kBB = R * kMmaKC * 2;  // B stage bytes (R rows x 64 columns)
   constexpr uint32_t kSB = mma_exp_stage_bytes(R);
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
   const int S = p.stages_e;
   uint8_t* vhi = smem + S * kSB;
   uint8_t* vlo = vhi + kMmaM * R * 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(vlo + kMmaM * R * 2);
+  uint8_t* smap = vlo + kMmaM * R * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NC = p.h_out / p.ncol, nst = NC / kMmaKC;
   const int n0 = static_cast<int>(blockIdx.x) * NC;
@@ -331,8 +341,8 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
       s_tile = tin;
     }
   }
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], kMmaThreads);
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -346,28 +356,20 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
   }
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
   const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
-  const T* Bg = static_cast<const T*>(p.b_ptr[slot]) + p.b_off + n0;
   T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy + n0;
-
-  auto load_b = [&](int s) {  // stage s of B: R rows x 64 columns, swizzled
-    uint8_t* dst = smem + (s % S) * kSB;
-    for (int i = tid; i < R * 8; i += kMmaThreads) {
-      const int k = i >> 3, c = i & 7;
-      cp_async16(dst + k * 128 + ((c ^ (k & 7)) << 4), Bg + static_cast<int64_t>(k) * p.h_out + s * kMmaKC + c * 8);
-    }
-  };
-  auto load_y = [&](int s) {  // stage s of y_old: 16 rows x 64 columns, swizzled
-    uint8_t* dst = smem + (s % S) * kSB + kBB;
-    const int m = tid >> 3, c = tid & 7;
-    cp_async16_zfill(dst + m * 128 + ((c ^ (m & 7)) << 4),
-                     Yg + static_cast<int64_t>(m < rows ? m : 0) * p.ldy + s * kMmaKC + c * 8, m < rows);
-  };
+  uint8_t* gmap = p.maps_e + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 128;
+  const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap);
   // B and y_old of the whole ring before the PDL wait (y_old is final: see the header)
   const int pre = min(S, nst);
-  for (int s = 0; s < pre; ++s) {
-    load_b(s);
-    load_y(s);
-    cp_async_arrive(&full[s]);
+  if (warp == 0) {
+    make_slot_tmap(&p.tmap_b, smap, gmap, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
+    if (lane == 0) {
+      for (int s = 0; s < pre; ++s) {
+        mbar_arrive_expect_tx(&full[s], kSB);
+        tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &full[s]);
+        tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &full[s]);
+      }
+    }
   }
   LSG_TC_TRACE(1, 1);
   pdl_wait();  // the partials
@@ -377,10 +379,24 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
     const float* src = p.ws + static_cast<int64_t>(blockIdx.y) * p.kparts * kMmaM * R;
     for (int i = tid * 8; i < kMmaM * R; i += kMmaThreads * 8) {
       float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int q = 0; q < p.kparts; ++q) {
-        const float4 u = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i);
-        const float4 w = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i + 4);
-        f[0] += u.x, f[1] += u.y, f[2] += u.z, f[3] += u.w, f[4] += w.x, f[5] += w.y, f[6] += w.z, f[7] += w.w;
+      int q = 0;
+      for (; q + 4 <= p.kparts; q += 4) {  // four parts' loads in flight, summed in order
+        float4 u[4][2];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          u[e][0] = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q + e) * kMmaM * R + i);
+          u[e][1] = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q + e) * kMmaM * R + i + 4);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          f[0] += u[e][0].x, f[1] += u[e][0].y, f[2] += u[e][0].z, f[3] += u[e][0].w;
+          f[4] += u[e][1].x, f[5] += u[e][1].y, f[6] += u[e][1].z, f[7] += u[e][1].w;
+        }
+      }
+      for (; q < p.kparts; ++q) {
+        const float4 u0 = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i);
+        const float4 u1 = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i + 4);
+        f[0] += u0.x, f[1] += u0.y, f[2] += u0.z, f[3] += u0.w, f[4] += u1.x, f[5] += u1.y, f[6] += u1.z, f[7] += u1.w;
       }
       float hf[8], lo[8];
       const uint4 hi = Cvt<T>::pack8(f);
@@ -388,7 +404,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
 #pragma unroll
       for (int e = 0; e < 8; ++e) lo[e] = f[e] - hf[e];
       const int m = i / R, c = (i - m * R) >> 3;
-      const uint32_t off = m * (R * 2) + ((c ^ mma_swz<CPR>(m)) << 4);
+      const uint32_t off = m * ROWV + ((c ^ swz<ROWV>(m)) << 4);
       *reinterpret_cast<uint4*>(vhi + off) = hi;
       *reinterpret_cast<uint4*>(vlo + off) = Cvt<T>::pack8(lo);
     }
@@ -401,7 +417,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
 #pragma unroll
   for (int kk = 0; kk < R / 16; ++kk) {
     const int c = 2 * kk + lc;
-    const uint32_t off = lr * (R * 2) + ((c ^ mma_swz<CPR>(lr)) << 4);
+    const uint32_t off = lr * ROWV + ((c ^ swz<ROWV>(lr)) << 4);
     ldsm_x4(smem_u32(vhi + off), ah[kk][0], ah[kk][1], ah[kk][2], ah[kk][3]);
     ldsm_x4(smem_u32(vlo + off), al[kk][0], al[kk][1], al[kk][2], al[kk][3]);
   }
@@ -411,7 +427,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
     mbar_wait(&full[b], (s / S) & 1);
     uint8_t* bs = smem + b * kSB;
     uint8_t* ys = bs + kBB;
-    // warp w: columns 16w .. 16w+15 of the stage (n8 tiles 2w, 2w+1)
+    // warp w: columns 16w .. 16w+15 of the stage (n8 tiles 2w, 2w+1); B rows are 128 B, SW128
     float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
     for (int kk = 0; kk < R / 16; ++kk) {
@@ -443,10 +459,11 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
     }
     __syncthreads();  // buffer b is free
     if (s == 0) LSG_TC_TRACE(1, 4);
-    if (s + S < nst) {
-      load_b(s + S);
-      load_y(s + S);
-      cp_async_arrive(&full[b]);
+    if (s + S < nst && tid == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&full[b], kSB);
+      tma_load_2d(bs, bmap, n0 + (s + S) * kMmaKC, 0, &full[b]);
+      tma_load_2d(ys, &p.tmap_y, n0 + (s + S) * kMmaKC, r0, &full[b]);
     }
   }
   LSG_TC_TRACE(1, 5);
