@@ -302,7 +302,8 @@ typedef enum {
   LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation (A/B measurements): 0 (default) the
                                    cluster-free partials + expand pair; 1 the first fused cluster kernel
                                    (rank 16); 2 the streamed cluster kernel (ranks 16 / 32); 3 the
-                                   segment-tile MMA pair (16-row tiles, mma.sync) */
+                                   segment-tile MMA pair (16-row tiles, mma.sync); 4 the one-pass
+                                   streaming kernel (a CTA per 16-row tile) */
   LSG_OPT_MMA_MIN_ROWS = 11     /* segments with at least this many rows (and below the long-segment
                                    threshold) take the segment-tile MMA pair; 0 (default) = auto: rank 64
                                    calls whose rows share adapters (total_rows > num_segments) send every

@@ -69,6 +69,8 @@ int launch_tc_expand(int dtype, int rank, const TcExpandParams& p, int tiles, cu
 struct TcFusedParams;
 int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStream_t st);
 struct MmaParams;
+struct StreamParams;
+int launch_stream(int dtype, int rank, const StreamParams& p, int tiles, cudaStream_t st);
 int launch_mma_pair(int dtype, int rank, const MmaParams& p, int tiles, cudaStream_t st);
 struct Tc3PartParams;
 struct Tc3ExpParams;

@@ -27,6 +27,7 @@
 #include "sgmv_tc2.cuh"
 #include "sgmv_tc3.cuh"
 #include "sgmv_mma.cuh"
+#include "sgmv_stream.cuh"
 
 namespace lsg {
 
@@ -177,10 +178,20 @@ bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
 bool tc3_ok(const lsg_weight_table* t) {
   return !cur().tc_split && cur().tc_legacy == 0 && tc_nq(t) > 0 && t->h_out % kTcNT == 0;
 }
+// K9 streaming kernel (sgmv_stream.cuh): LSG_OPT_TC_LEGACY = 4
+bool stream_ok(const lsg_weight_table* t) {
+  return !cur().tc_split && cur().tc_legacy == 4 && (t->rank == 16 || t->rank == 32 || t->rank == 64) &&
+         t->h_in % 1024 == 0 && t->h_out % 1024 == 0 && t->a_layer_stride % 8 == 0 &&
+         t->b_layer_stride % 8 == 0;
+}
+int stream_tiles(int s_n, int n_seg) {  // 16-row tiles of the segments with >= tc_min_rows rows
+  return std::max(1, s_n / 16 + std::min(n_seg, s_n / tc_min_rows()));
+}
 size_t tc3_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg) {
   return static_cast<size_t>(tc_tile_bound(s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
 }
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
+  if (tc_nq(t) > 0 && s_n >= tc_min_rows() && stream_ok(t)) return static_cast<size_t>(stream_tiles(s_n, s_n)) * 256;
   if (tc_nq(t) > 0 && s_n >= tc_min_rows() && tc3_ok(t)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows());
   // the fused kernels keep v on chip
   if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) || tc_fused_c(t, nullptr) > 0)) return 0;
@@ -223,20 +234,46 @@ RowRanges row_ranges(const lsg_weight_table* t, int n_seg, int s_n) {
 int mma_tile_bound(int s_n, int n_seg, int lo) {
   return std::max(1, s_n / kMmaM + std::min(n_seg, s_n / std::max(lo, 1)));
 }
-// K / column splits: about one CTA per SM for each of the two kernels (the tile bound
-// overestimates the real tiles), the largest divisor of the 64-column stage count that
-// keeps tiles x split <= 160.
-int mma_split(int nstages, int tiles) {
-  int best = 1;
-  for (int d = 1; d <= nstages; ++d)
-    if (nstages % d == 0 && static_cast<int64_t>(tiles) * d <= 160) best = d;
+// K / column splits: a divisor d of the 64-column stage count whose slice (nstages / d
+// stages) is resident in shared memory at once (<= max_st), the largest with tiles x d <=
+// target (the tile bound overestimates the real tiles), else the smallest that fits.
+int mma_split(int nstages, int tiles, int max_st, int target) {
+  int best = 0;
+  for (int d = 1; d <= nstages; ++d) {
+    if (nstages % d != 0 || nstages / d > max_st) continue;
+    if (best == 0 || static_cast<int64_t>(tiles) * d <= target) best = d;
+  }
   return best;
 }
-// workspace bound: tiles * kparts (and tiles * ncol) <= max(160, tiles): the partials plus
-// one 128-byte weight descriptor per CTA of each kernel
+constexpr int kMmaPartTarget = 160, kMmaExpTarget = 320;  // CTAs per kernel
+constexpr uint32_t kMmaPartSmemTarget = 150 * 1024;       // one partials CTA + one expand CTA per SM
+constexpr uint32_t kMmaSmemTarget = 110 * 1024;           // expand: two CTAs per SM
+// resident stages per CTA within the shared-memory target
+int mma_part_max_st(int R) {
+  return std::min<int>(kMmaMaxStagesDecl, (kMmaPartSmemTarget - mma_part_smem(R, 0)) / mma_part_stage_bytes(R));
+}
+int mma_exp_max_st(int R, int kparts) {
+  return std::min<int>(kMmaMaxStagesDecl, (kMmaSmemTarget - mma_exp_smem(R, 0, kparts)) / mma_exp_stage_bytes(R));
+}
+// workspace bound (the splits give tiles * d <= max(target, tiles * nstages / max_st)): the
+// partials plus one 128-byte weight descriptor per CTA of each kernel
+// smallest K split whose slice is resident (the split never exceeds max(target, tiles * it))
+int mma_min_kparts(const lsg_weight_table* t) {
+  const int n = t->h_in / kMmaKC, mx = mma_part_max_st(t->rank);
+  for (int d = 1; d <= n; ++d)
+    if (n % d == 0 && n / d <= mx) return d;
+  return n;
+}
+size_t mma_part_ctas(const lsg_weight_table* t, int tiles) {
+  return std::max<size_t>(kMmaPartTarget, static_cast<size_t>(tiles) * mma_min_kparts(t));
+}
+size_t mma_exp_ctas(const lsg_weight_table* t, int tiles) {
+  return std::max<size_t>(kMmaExpTarget, static_cast<size_t>(tiles) * (t->h_out / kMmaKC));
+}
 size_t mma_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg, int lo) {
-  const size_t ctas = static_cast<size_t>(std::max(160, mma_tile_bound(s_n, n_seg, lo)));
-  return ctas * kMmaM * t->rank * sizeof(float) + 2 * ctas * 128;
+  const int tiles = mma_tile_bound(s_n, n_seg, lo);
+  const size_t pctas = mma_part_ctas(t, tiles), ectas = mma_exp_ctas(t, tiles);
+  return pctas * kMmaM * t->rank * sizeof(float) + (pctas + ectas) * 128;
 }
 bool encode_map_2d(CUtensorMap* m, int dtype, const void* base, uint64_t cols, uint64_t rows, uint64_t ld_elems,
                    uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
@@ -247,11 +284,6 @@ bool encode_map_2d(CUtensorMap* m, int dtype, const void* base, uint64_t cols, u
   return encode_tiled_fn()(m, dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                            2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-constexpr uint32_t kMmaSmemTarget = 100 * 1024;  // two CTAs per SM
-int mma_stages(uint32_t fixed, uint32_t stage, int nst) {
-  const int fit = static_cast<int>((kMmaSmemTarget - fixed) / stage);
-  return std::max(1, std::min({nst, kMmaMaxStages, fit}));
 }
 bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_t ldy, const void* x, int64_t ldx,
                  const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg, int s_n,
@@ -275,25 +307,34 @@ bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_
     return false;
   mp.y = y;
   mp.ldy = ldy;
+  mp.x = x;
+  mp.ldx = ldx;
   mp.a_ptr = tbl->a_ptr;
   mp.b_ptr = tbl->b_ptr;
   mp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
   mp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
   mp.seg_starts = seg_starts;
   mp.seg_slot = seg_slot;
+  mp.kparts = mma_split(tbl->h_in / kMmaKC, tiles, mma_part_max_st(R), kMmaPartTarget);
+
+  if (mp.kparts == 0) return false;
+  mp.pc = 1;  // the largest cluster (<= 8) that divides the K split: one partial per cluster
+  for (int c = kMmaMaxPc; c >= 2; --c)
+    if (mp.kparts % c == 0) {
+      mp.pc = c;
+      break;
+    }
+  mp.ncol = mma_split(tbl->h_out / kMmaKC, tiles, mma_exp_max_st(R, mp.kparts / mp.pc), kMmaExpTarget);
+  if (mp.ncol == 0) return false;
   mp.ws = static_cast<float*>(ws);
-  const size_t ctas = static_cast<size_t>(std::max(160, tiles));
-  mp.maps_p = static_cast<uint8_t*>(ws) + ctas * kMmaM * R * sizeof(float);
-  mp.maps_e = mp.maps_p + ctas * 128;
+  const size_t pctas = mma_part_ctas(tbl, tiles);
+  mp.maps_p = static_cast<uint8_t*>(ws) + pctas * kMmaM * R * sizeof(float);
+  mp.maps_e = mp.maps_p + pctas * 128;
   mp.n_seg = n_seg;
   mp.s_n = s_n;
   mp.num_slots = tbl->num_slots;
   mp.h_in = tbl->h_in;
   mp.h_out = tbl->h_out;
-  mp.kparts = mma_split(tbl->h_in / kMmaKC, tiles);
-  mp.ncol = mma_split(tbl->h_out / kMmaKC, tiles);
-  mp.stages_p = mma_stages(mma_part_smem(R, 0), mma_part_stage_bytes(R), tbl->h_in / mp.kparts / kMmaKC);
-  mp.stages_e = mma_stages(mma_exp_smem(R, 0), mma_exp_stage_bytes(R), tbl->h_out / mp.ncol / kMmaKC);
   mp.min_rows = rr.mma_lo;
   mp.max_rows = rr.mma_hi;
   mp.trace = g_trace;
@@ -361,6 +402,8 @@ struct LongPlan {
   Tc2Params tp;
   Tc3PartParams pp;
   Tc3ExpParams xp;
+  StreamParams sp9;
+  int stream9 = 0;   // 1: the one-pass streaming kernel (sgmv_stream.cuh)
   int tc3 = 0;       // 1: the cluster-free partials + expand pair (sgmv_tc3.cuh), the default
   int nq = 0, tiles = 0;
   int fused_c = 0;   // > 0: one first-generation fused tensor-core launch, clusters of fused_c CTAs
@@ -421,6 +464,42 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   const int nq = tc_nq(tbl);
   if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
+  if (stream_ok(tbl)) {
+    const int tiles = stream_tiles(s_n, n_seg), R = tbl->rank;
+    if (ws == nullptr || !aligned16(ws) || ws_bytes < static_cast<size_t>(tiles) * 256) return false;
+    StreamParams& q = lp.sp9;
+    q = StreamParams{};
+    if (!encode_map_2d(&q.tmap_a, tbl->dtype, x, 64, static_cast<uint64_t>(tbl->h_in) * R / 64, 64, 64, 256,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_map_2d(&q.tmap_b, tbl->dtype, x, tbl->h_out, R, tbl->h_out, 64, R, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    lp.stream9 = 1;
+    lp.tiles = tiles;
+    q.x = x;
+    q.y = y;
+    q.ldx = ldx;
+    q.ldy = ldy;
+    q.a_ptr = tbl->a_ptr;
+    q.b_ptr = tbl->b_ptr;
+    q.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+    q.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
+    q.seg_starts = seg_starts;
+    q.seg_slot = seg_slot;
+    q.maps = static_cast<uint8_t*>(ws);
+    q.n_seg = n_seg;
+    q.s_n = s_n;
+    q.num_slots = tbl->num_slots;
+    q.h_in = tbl->h_in;
+    q.h_out = tbl->h_out;
+    const int kc = R == 16 ? 1024 : 512, nst = tbl->h_in / kc + tbl->h_out / kc;
+    const uint32_t fixed = R == 16 ? stream_fixed(16) : R == 32 ? stream_fixed(32) : stream_fixed(64);
+    const uint32_t slotb = R == 16 ? stream_slot_bytes(16) : R == 32 ? stream_slot_bytes(32) : stream_slot_bytes(64);
+    q.stages = std::max(1, std::min({nst, kStreamMaxStages, static_cast<int>((kStreamSmem - fixed) / slotb)}));
+    q.min_rows = tc_min_rows();
+    q.trace = g_trace;
+    q.trace_ctas = g_trace_ctas;
+    return true;
+  }
   if (tc3_ok(tbl)) {
     if (ws == nullptr || !aligned16(ws) || ws_bytes < tc3_ws_bytes(tbl, s_n, n_seg)) return false;
     Tc3PartParams& pp = lp.pp;
@@ -567,6 +646,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
 }
 
 int launch_long_segments(const LongPlan& lp, int dtype, int rank, cudaStream_t cs) {
+  if (lp.stream9) return launch_stream(dtype, rank, lp.sp9, lp.tiles, cs);
   if (lp.tc3) {
     const int st = launch_tc3_parts(dtype, rank, lp.pp, lp.tiles, cs);
     if (st != LSG_OK) return st;
@@ -1202,7 +1282,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       g_opt_tc_min_rows = value;
       return LSG_OK;
     case LSG_OPT_TC_LEGACY:
-      if (value < 0 || value > 3) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0 .. 3");
+      if (value < 0 || value > 4) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0 .. 4");
       g_opt_tc_legacy = value;
       return LSG_OK;
     case LSG_OPT_MMA_MIN_ROWS:

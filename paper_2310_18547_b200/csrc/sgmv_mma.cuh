@@ -10,18 +10,19 @@
 //             P_ks[16][R] = x[tile rows, K slice ks] . A[K slice ks, :] over its K slice of
 //             KS = h_in / kparts columns, in stages of 64 columns (x 16 x 64 and A 64 x R)
 //             moved by 2-D TMA into swizzled shared memory (the hardware swizzle makes the
-//             ldmatrix fragment loads conflict-free); the A stages of the whole ring are
-//             requested BEFORE the PDL wait.  Warp w takes k16-step w of every stage; the
-//             four warp accumulators are summed in warp order and P_ks goes to the workspace
-//             [tile][ks][16][R] fp32 (L2-resident).
+//             ldmatrix fragment loads conflict-free).  Every stage of the slice is resident
+//             at once (the host sizes the split so it fits); the A stages are requested
+//             BEFORE the PDL wait and the tile's x rows are prefetched into L2 there.  Warp w
+//             takes stages w, w+4, ...; the four warp accumulators are summed in warp order
+//             and P_ks goes to the workspace [tile][ks][16][R] fp32 (L2-resident).
 //   expand    grid (ncol, tile bound), 128 threads.  CTA (j, t) stages its B column slice
 //             (R x NC) and y_old (16 x NC) by TMA before its PDL wait -- the partials kernel
 //             triggers its dependents only after its own wait, so every kernel before it has
-//             completed and y_old is final -- then sums the tile's partials in ks order
-//             (v, fp32), splits v into 16-bit hi + lo (hi = rn(v), lo = rn(v - hi)) and runs
-//             D = hi.B + lo.B on the tensor cores (the lo term keeps v's fp32 precision),
-//             adds y_old in fp32 and rounds once.  Stores are 16-byte vectors of the tile's
-//             valid rows only.
+//             completed and y_old is final -- then bulk-copies the tile's partials, sums them
+//             in ks order (v, fp32), splits v into 16-bit hi + lo (hi = rn(v), lo = rn(v -
+//             hi)) and runs hi.B and lo.B on the tensor cores (the lo term keeps v's fp32
+//             precision), adds y_old in fp32 and rounds once.  Warp w takes stages w, w+4, ...
+//             with its own epilogue; stores are 16-byte vectors of the tile's valid rows only.
 //
 // Adapter weights are addressed through per-slot pointers (a_ptr[slot]), so their TMA
 // descriptors are made on the device: the host encodes one template per operand (shape,
@@ -32,14 +33,14 @@
 // Why this shape: a shared-adapter segment is weight-bound (h=5120 r=64: 1.25 MiB of A+B
 // per segment against 8 rows x 20 KiB of activations), so the weights of one tile are
 // spread over kparts x ncol CTAs (about one per SM) instead of one cluster; long prefill
-// segments are activation-bound and get one CTA per 16-row tile with the whole K (or N)
-// range streamed through a ring.  The same two kernels cover both with different splits
-// (lsg_api.cu: prepare_mma).
+// segments are activation-bound and get many small CTAs per 16-row tile.  The same two
+// kernels cover both with different splits (lsg_api.cu: prepare_mma).
 //
 // Canonical arithmetic for these rows (deterministic; depends only on the shape and the
 // split, never on the batch composition): v = sum over parts ks ascending of (sum over warps
-// w ascending of the MMA chain of k16-steps w, w+4, ... of part ks); y = rn(fp32(hi.B +
-// lo.B) + y_old).  Within tolerance of the CUDA-core rows, not bitwise.
+// w ascending of the MMA chain over the k16-steps of stages w, w+4, ... of part ks);
+// y = rn((fp32(hi.B) + fp32(lo.B)) + y_old).  Within tolerance of the CUDA-core rows, not
+// bitwise.
 #pragma once
 
 #include "sgmv_device.cuh"
@@ -49,7 +50,8 @@ namespace lsg {
 
 constexpr int kMmaM = 16;         // rows per tile (one m16 block)
 constexpr int kMmaThreads = 128;  // 4 warps
-constexpr int kMmaKC = 64;        // columns per pipeline stage (4 k16-steps: one per warp)
+constexpr int kMmaKC = 64;        // columns per stage (4 k16-steps)
+constexpr int kMmaMaxStagesDecl = 32;  // stages per CTA (all resident; barriers reserved for this many)
 
 struct MmaParams {
   CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 16, SW128
@@ -58,6 +60,8 @@ struct MmaParams {
   CUtensorMap tmap_b;  // template: B of one layer [R, h_out], box 64 x R, SW128
   void* y;
   int64_t ldy;
+  const void* x;  // for the L2 prefetch of the tile's rows
+  int64_t ldx;
   const void* const* a_ptr;
   const void* const* b_ptr;
   int64_t a_off;  // layer * a_layer_stride (elements)
@@ -69,9 +73,8 @@ struct MmaParams {
   uint8_t* maps_e;  // ... per expand CTA
   int32_t n_seg, s_n, num_slots, h_in, h_out;
   int32_t kparts;    // K slices (gridDim.x of the partials kernel)
+  int32_t pc;        // partials cluster size: pc consecutive K slices sum over DSMEM (kparts / pc partials)
   int32_t ncol;      // column slices (gridDim.x of the expand kernel)
-  int32_t stages_p;  // ring depth of the partials kernel
-  int32_t stages_e;  // ring depth of the expand kernel
   int32_t min_rows;  // segments with min_rows <= len < max_rows take this path
   int32_t max_rows;
   unsigned long long* trace;  // phase stamps (instrumented builds only, LSG_TC_TRACE layout)
@@ -179,18 +182,23 @@ __device__ __forceinline__ void mma_tile_of(const int32_t* seg_starts, int n_seg
 }
 
 // ---- shared-memory plans (host and device) -----------------------------------------------
-// Stage sizes are multiples of 1024 bytes (the 128-byte swizzle atom), buffers 1024-aligned.
+// Every stage of a CTA's slice is resident at once (the host picks the K / column splits so
+// that it fits): no ring, no refill.  Stage sizes are multiples of 1024 bytes (the 128-byte
+// swizzle atom), buffers 1024-aligned.
 __host__ __device__ constexpr uint32_t mma_part_stage_bytes(int R) { return kMmaM * kMmaKC * 2 + kMmaKC * R * 2; }
 __host__ __device__ constexpr uint32_t mma_exp_stage_bytes(int R) { return R * kMmaKC * 2 + kMmaM * kMmaKC * 2; }
-// partials: [ring stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, map, barriers
-__host__ __device__ constexpr uint32_t mma_part_smem(int R, int stages) {
-  return 1024 + stages * mma_part_stage_bytes(R) + 4 * kMmaM * R * 4 + 128 + 8 * 32;
+constexpr int kMmaMaxPc = 8;  // partials cluster size (portable)
+// partials: [stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, the cluster leader's
+// receive buffer pc x 16 x R fp32, map, barriers
+__host__ __device__ constexpr uint32_t mma_part_smem(int R, int stages, int pc = kMmaMaxPc) {
+  return 1024 + stages * mma_part_stage_bytes(R) + (4 + pc) * kMmaM * R * 4 + 128 + 8 * (kMmaMaxStagesDecl + 2);
 }
-// expand: [ring stages][B 128R B | y 2 KB], v hi / lo (16 x R 16-bit each), map, barriers
-__host__ __device__ constexpr uint32_t mma_exp_smem(int R, int stages) {
-  return 1024 + stages * mma_exp_stage_bytes(R) + 2 * kMmaM * R * 2 + 128 + 8 * 32;
+// expand: [stages][B 128R B | y 2 KB], the tile's partials kparts x 16 x R fp32, v hi / lo
+// (16 x R 16-bit each), map, barriers
+__host__ __device__ constexpr uint32_t mma_exp_smem(int R, int stages, int kparts) {
+  return 1024 + stages * mma_exp_stage_bytes(R) + kparts * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 128 +
+         8 * (kMmaMaxStagesDecl + 2);
 }
-constexpr int kMmaMaxStages = 32;
 
 template <typename T, int R>
 __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid_constant__ MmaParams p) {
@@ -198,16 +206,16 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
   constexpr int ROWB = R * 2;                    // bytes per A row (= its TMA swizzle span)
   constexpr uint32_t kXB = kMmaM * kMmaKC * 2;   // x stage bytes
   constexpr uint32_t kSB = mma_part_stage_bytes(R);
-  constexpr int NT = R / 8;                      // n8 tiles of the accumulator
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = p.stages_p;
-  float* red = reinterpret_cast<float*>(smem + S * kSB);     // [4][16][R]
-  uint8_t* smap = smem + S * kSB + 4 * kMmaM * R * 4;        // 128 B
-  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);  // [S] stage landed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ks = static_cast<int>(blockIdx.x);
-  const int KS = p.h_in / p.kparts, nst = KS / kMmaKC;
+  const int KS = p.h_in / p.kparts, nst = KS / kMmaKC;  // nst <= kMmaMaxStages (host)
+  const int C = p.pc;
+  float* red = reinterpret_cast<float*>(smem + nst * kSB);   // [4][16][R]
+  float* recv = red + 4 * kMmaM * R;                         // [C][16][R] (cluster leader)
+  uint8_t* smap = reinterpret_cast<uint8_t*>(recv + C * kMmaM * R);  // 128 B
+  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);  // [nst] stage landed, [nst] partials in
   LSG_TC_TRACE(0, 0);
 
   __shared__ int s_seg, s_tile;
@@ -220,13 +228,14 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
     }
   }
   if (tid == 32) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i <= nst; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
   const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
-  // CTAs without work leave at once; the first row of the grid still waits for the preceding
-  // grid (and triggers) so this grid's completion implies the predecessor's.
+  // CTAs without work leave at once (a whole cluster: its CTAs share the tile); the first row
+  // of the grid still waits for the preceding grid (and triggers) so this grid's completion
+  // implies the predecessor's.
   if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {
     if (blockIdx.y == 0) {
       pdl_wait();
@@ -234,74 +243,96 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
     }
     return;
   }
+  const uint32_t crank = C > 1 ? cluster_ctarank() : 0u;
+  if (C > 1) cluster_arrive_relaxed();  // this CTA's barriers are initialised
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
+  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
   const int k0 = ks * KS;
-  const int pre = min(S, nst);
   uint8_t* gmap = p.maps_p + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 128;
   const CUtensorMap* amap = reinterpret_cast<const CUtensorMap*>(gmap);
   if (warp == 0) {
-    // weights first (before the PDL wait): this slot's A descriptor, then the ring's A stages
+    // weights first (before the PDL wait): this slot's A descriptor, then every A stage
     make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
     if (lane == 0) {
-      for (int s = 0; s < pre; ++s) {
+      for (int s = 0; s < nst; ++s) {
         mbar_arrive_expect_tx(&full[s], kSB);
         tma_load_2d(smem + s * kSB + kXB, amap, 0, k0 + s * kMmaKC, &full[s]);
       }
     }
+  } else if (warp == 1 && lane < rows) {
+    // the tile's x rows into L2 now (a prefetch is only a hint: safe while the preceding
+    // kernel still runs), so after the wait they come from L2
+    bulk_prefetch_l2(static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + lane) * p.ldx + k0,
+                     static_cast<uint32_t>(KS * 2));
   }
   LSG_TC_TRACE(0, 1);
-  pdl_wait();  // x may come from the preceding kernel
-  // Dependents (the expand) start now: every kernel before this one has completed, so the
-  // expand may stage y_old before its own wait (it waits only for these partials).
+  // The expand may start now (once every partials CTA is resident): it builds its weight
+  // descriptor and streams B before its own wait; y_old only after it.
   pdl_launch_dependents();
+  pdl_wait();  // x may come from the preceding kernel
   LSG_TC_TRACE(0, 2);
   if (tid == 0)
-    for (int s = 0; s < pre; ++s) tma_load_2d(smem + s * kSB, &p.tmap_x, k0 + s * kMmaKC, r0, &full[s]);
+    for (int s = 0; s < nst; ++s) tma_load_2d(smem + s * kSB, &p.tmap_x, k0 + s * kMmaKC, r0, &full[s]);
 
-  float acc[NT][4];
+  // Swapped operands: P^T[R][rows] = A^T . x^T -- the rank is the MMA's M (m16 tiles of A^T
+  // by ldmatrix.trans from A's [k][r] rows), the tile's rows its N (n8 tiles from x's rows):
+  // a tile of <= 8 rows runs one n8 tile, half the MMAs of a 16-row M.
+  constexpr int MT = R / 16;  // m16 tiles of the rank
+  const bool two = rows > 8;  // second n8 tile (rows 8..15)
+  float acc[MT][2][4];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  // lane's ldmatrix row / chunk within a 16 x 16 block
-  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = lane >> 4;
-  for (int s = 0; s < nst; ++s) {
-    const int b = s % S;
-    mbar_wait(&full[b], (s / S) & 1);
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0.f;
+  // lane's ldmatrix addressing: .trans A^T blocks (k row, r chunk) and x^T blocks (row, k chunk)
+  const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;
+  const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;
+  // warp w: stages w, w + 4, ... (all four k16-steps of each), no block barrier
+  for (int s = warp; s < nst; s += 4) {
+    mbar_wait(&full[s], 0);
     if (s == 0) LSG_TC_TRACE(0, 3);
-    const uint32_t xs = smem_u32(smem + b * kSB), as = xs + kXB;
-    uint32_t a[4];
-    {  // x rows 0..15, k16-step `warp` of this stage: chunks 2w, 2w+1 (128-byte rows, SW128)
-      const int c = 2 * warp + lc;
-      ldsm_x4(xs + lr * 128 + ((c ^ (lr & 7)) << 4), a[0], a[1], a[2], a[3]);
-    }
+    const uint32_t xs = smem_u32(smem + s * kSB), as = xs + kXB;
 #pragma unroll
-    for (int j = 0; j < NT; j += 2) {  // A rows 16w..16w+15, n8 tiles j, j+1 (ROWB-byte rows, swizzled)
-      const int k = 16 * warp + lr, c = j + lc;
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(as + k * ROWB + ((c ^ swz<ROWB>(k)) << 4), b0, b1, b2, b3);
-      mma16816<T>(acc[j], a, b0, b1);
-      mma16816<T>(acc[j + 1], a, b2, b3);
-    }
-    __syncthreads();  // every warp is done with buffer b
-    if (s + S < nst && tid == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&full[b], kSB);
-      tma_load_2d(smem + b * kSB + kXB, amap, 0, k0 + (s + S) * kMmaKC, &full[b]);
-      tma_load_2d(smem + b * kSB, &p.tmap_x, k0 + (s + S) * kMmaKC, r0, &full[b]);
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t b[4];  // x^T: {b0, b1} of rows 0..7, {b2, b3} of rows 8..15 (128-byte rows, SW128)
+      {
+        const int c = 2 * kk + xc;
+        ldsm_x4(xs + xr * 128 + ((c ^ (xr & 7)) << 4), b[0], b[1], b[2], b[3]);
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {  // A^T rows 16i.., k 16kk.. (ROWB-byte rows of A, swizzled)
+        const int k = 16 * kk + ak, c = 2 * i + ac;
+        uint32_t a[4];
+        ldsm_x4_t(as + k * ROWB + ((c ^ swz<ROWB>(k)) << 4), a[0], a[1], a[2], a[3]);
+        mma16816<T>(acc[i][0], a, b[0], b[1]);
+        if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
+      }
     }
   }
   // ---- sum the four warp accumulators in warp order, write the partial ------------------
   LSG_TC_TRACE(0, 4);
-  {
+  {  // D^T fragment (r = 16i + g (+8), rows 8j + 2t (+1)) -> red[warp][row][r]
     const int g = lane >> 2, t = lane & 3;
     float* rw = red + warp * kMmaM * R;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      *reinterpret_cast<float2*>(rw + g * R + j * 8 + 2 * t) = make_float2(acc[j][0], acc[j][1]);
-      *reinterpret_cast<float2*>(rw + (g + 8) * R + j * 8 + 2 * t) = make_float2(acc[j][2], acc[j][3]);
-    }
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m0 = 8 * j + 2 * t, r = 16 * i + g;
+        rw[m0 * R + r] = acc[i][j][0];
+        rw[(m0 + 1) * R + r] = acc[i][j][1];
+        rw[m0 * R + r + 8] = acc[i][j][2];
+        rw[(m0 + 1) * R + r + 8] = acc[i][j][3];
+      }
   }
   __syncthreads();
-  float* dst = p.ws + (static_cast<int64_t>(blockIdx.y) * p.kparts + ks) * kMmaM * R;
+  // this CTA's partial: the warp sum in warp order.  Clusters of pc K slices: every CTA
+  // pushes it into the leader's receive buffer (st.async, completing on the leader's barrier
+  // nst), the leader sums the pc partials in rank (= K slice) order and writes one.
+  const int nparts = p.kparts / C;
+  float* dst = p.ws + (static_cast<int64_t>(blockIdx.y) * nparts + ks / C) * kMmaM * R;
+  if (C > 1 && crank == 0 && tid == 0) mbar_arrive_expect_tx(&full[nst], static_cast<uint32_t>((C - 1) * kMmaM * R * 4));
+  if (C > 1) cluster_wait();  // the leader's barrier is initialised
   for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
     float4 s4 = *reinterpret_cast<const float4*>(red + i);
 #pragma unroll
@@ -309,8 +340,27 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
       const float4 o = *reinterpret_cast<const float4*>(red + w * kMmaM * R + i);
       s4.x += o.x, s4.y += o.y, s4.z += o.z, s4.w += o.w;
     }
-    *reinterpret_cast<float4*>(dst + i) = s4;
+    if (C == 1)
+      *reinterpret_cast<float4*>(dst + i) = s4;
+    else if (crank == 0)
+      *reinterpret_cast<float4*>(recv + i) = s4;
+    else
+      st_async_v4(mapa_u32(recv + crank * kMmaM * R + i, 0u), s4.x, s4.y, s4.z, s4.w, mapa_u32(&full[nst], 0u));
   }
+  if (C > 1 && crank == 0) {
+    mbar_wait(&full[nst], 0);
+    __syncthreads();  // the leader's own partial
+    for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
+      float4 s4 = *reinterpret_cast<const float4*>(recv + i);
+      for (int c = 1; c < C; ++c) {
+        const float4 o = *reinterpret_cast<const float4*>(recv + c * kMmaM * R + i);
+        s4.x += o.x, s4.y += o.y, s4.z += o.z, s4.w += o.w;
+      }
+      *reinterpret_cast<float4*>(dst + i) = s4;
+    }
+  }
+  // the expand reads these partials with bulk copies (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   LSG_TC_TRACE(0, 5);
 }
 
@@ -320,16 +370,18 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
   constexpr int ROWV = R * 2;               // bytes per v row
   constexpr uint32_t kBB = R * kMmaKC * 2;  // B stage bytes (R rows x 64 columns)
   constexpr uint32_t kSB = mma_exp_stage_bytes(R);
+  constexpr uint32_t kPB = kMmaM * R * 4;   // one partial
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = p.stages_e;
-  uint8_t* vhi = smem + S * kSB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NC = p.h_out / p.ncol, nst = NC / kMmaKC;  // nst <= kMmaMaxStages (host)
+  const int n0 = static_cast<int>(blockIdx.x) * NC;
+  const int nparts = p.kparts / p.pc;                        // partials per tile
+  float* part = reinterpret_cast<float*>(smem + nst * kSB);  // [nparts][16][R]
+  uint8_t* vhi = smem + nst * kSB + nparts * kPB;
   uint8_t* vlo = vhi + kMmaM * R * 2;
   uint8_t* smap = vlo + kMmaM * R * 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NC = p.h_out / p.ncol, nst = NC / kMmaKC;
-  const int n0 = static_cast<int>(blockIdx.x) * NC;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);  // [nst] stages, [nst] partials
   LSG_TC_TRACE(1, 0);
 
   __shared__ int s_seg, s_tile;
@@ -342,7 +394,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
     }
   }
   if (tid == 32) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i <= nst; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -359,43 +411,33 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
   T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy + n0;
   uint8_t* gmap = p.maps_e + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 128;
   const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap);
-  // B and y_old of the whole ring before the PDL wait (y_old is final: see the header)
-  const int pre = min(S, nst);
+  // B of every stage before the PDL wait (weights are never written by a kernel)
   if (warp == 0) {
     make_slot_tmap(&p.tmap_b, smap, gmap, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
     if (lane == 0) {
-      for (int s = 0; s < pre; ++s) {
+      for (int s = 0; s < nst; ++s) {
         mbar_arrive_expect_tx(&full[s], kSB);
         tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &full[s]);
-        tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &full[s]);
       }
     }
   }
   LSG_TC_TRACE(1, 1);
-  pdl_wait();  // the partials
+  pdl_wait();  // the partials (and, through the partials kernel's own wait, y_old)
   pdl_launch_dependents();
   LSG_TC_TRACE(1, 2);
+  if (tid == 0) {  // y_old of every stage, then the tile's partials (one bulk copy each, barrier nst)
+    for (int s = 0; s < nst; ++s) tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &full[s]);
+    const float* src = p.ws + static_cast<int64_t>(blockIdx.y) * nparts * kMmaM * R;
+    mbar_arrive_expect_tx(&full[nst], static_cast<uint32_t>(nparts) * kPB);
+    for (int q = 0; q < nparts; ++q) bulk_g2s(part + q * kMmaM * R, src + q * kMmaM * R, kPB, &full[nst]);
+  }
+  mbar_wait(&full[nst], 0);
   {  // v = sum of the partials in ks order -> 16-bit hi + lo, swizzled rows of R values
-    const float* src = p.ws + static_cast<int64_t>(blockIdx.y) * p.kparts * kMmaM * R;
     for (int i = tid * 8; i < kMmaM * R; i += kMmaThreads * 8) {
       float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      int q = 0;
-      for (; q + 4 <= p.kparts; q += 4) {  // four parts' loads in flight, summed in order
-        float4 u[4][2];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          u[e][0] = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q + e) * kMmaM * R + i);
-          u[e][1] = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q + e) * kMmaM * R + i + 4);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          f[0] += u[e][0].x, f[1] += u[e][0].y, f[2] += u[e][0].z, f[3] += u[e][0].w;
-          f[4] += u[e][1].x, f[5] += u[e][1].y, f[6] += u[e][1].z, f[7] += u[e][1].w;
-        }
-      }
-      for (; q < p.kparts; ++q) {
-        const float4 u0 = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i);
-        const float4 u1 = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(q) * kMmaM * R + i + 4);
+      for (int q = 0; q < nparts; ++q) {
+        const float4 u0 = *reinterpret_cast<const float4*>(part + q * kMmaM * R + i);
+        const float4 u1 = *reinterpret_cast<const float4*>(part + q * kMmaM * R + i + 4);
         f[0] += u0.x, f[1] += u0.y, f[2] += u0.z, f[3] += u0.w, f[4] += u1.x, f[5] += u1.y, f[6] += u1.z, f[7] += u1.w;
       }
       float hf[8], lo[8];
@@ -411,59 +453,63 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
   }
   __syncthreads();
   LSG_TC_TRACE(1, 3);
-  // A fragments of v (hi and lo) for every k16-step: R/16 steps
-  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = lane >> 4;
-  uint32_t ah[R / 16][4], al[R / 16][4];
+  // Swapped operands: y^T[cols][rows] = B^T . v^T -- the output columns are the MMA's M (m16
+  // tiles of B^T by ldmatrix.trans from B's [k][n] rows), the tile's rows its N: a tile of
+  // <= 8 rows runs one n8 tile.  v^T fragments (hi and lo) for every k16-step, from v's rows.
+  const bool two = rows > 8;
+  const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;
+  const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;
+  uint32_t vh[R / 16][4], vl[R / 16][4];  // {b0, b1} rows 0..7, {b2, b3} rows 8..15
 #pragma unroll
   for (int kk = 0; kk < R / 16; ++kk) {
-    const int c = 2 * kk + lc;
-    const uint32_t off = lr * ROWV + ((c ^ swz<ROWV>(lr)) << 4);
-    ldsm_x4(smem_u32(vhi + off), ah[kk][0], ah[kk][1], ah[kk][2], ah[kk][3]);
-    ldsm_x4(smem_u32(vlo + off), al[kk][0], al[kk][1], al[kk][2], al[kk][3]);
+    const int c = 2 * kk + xc;
+    const uint32_t off = xr * ROWV + ((c ^ swz<ROWV>(xr)) << 4);
+    ldsm_x4(smem_u32(vhi + off), vh[kk][0], vh[kk][1], vh[kk][2], vh[kk][3]);
+    ldsm_x4(smem_u32(vlo + off), vl[kk][0], vl[kk][1], vl[kk][2], vl[kk][3]);
   }
   const int g = lane >> 2, t = lane & 3;
-  for (int s = 0; s < nst; ++s) {
-    const int b = s % S;
-    mbar_wait(&full[b], (s / S) & 1);
-    uint8_t* bs = smem + b * kSB;
+  // warp w: stages w, w + 4, ... -- all 64 columns (4 m16 tiles) of each, its own epilogue
+  // and stores, no block barrier
+  for (int s = warp; s < nst; s += 4) {
+    mbar_wait(&full[s], 0);
+    if (s == 0) LSG_TC_TRACE(1, 4);
+    uint8_t* bs = smem + s * kSB;
     uint8_t* ys = bs + kBB;
-    // warp w: columns 16w .. 16w+15 of the stage (n8 tiles 2w, 2w+1); B rows are 128 B, SW128
-    float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-    for (int kk = 0; kk < R / 16; ++kk) {
-      const int k = 16 * kk + lr, c = 2 * warp + lc;
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(smem_u32(bs + k * 128 + ((c ^ (k & 7)) << 4)), b0, b1, b2, b3);
-      mma16816<T>(d[0], ah[kk], b0, b1);
-      mma16816<T>(d[1], ah[kk], b2, b3);
-      mma16816<T>(d[0], al[kk], b0, b1);
-      mma16816<T>(d[1], al[kk], b2, b3);
-    }
-    // epilogue in place: y = rn(D + y_old), rows g and g + 8, columns 2t, 2t+1 of chunk 2w + j
+    for (int i = 0; i < 4; ++i) {  // columns 16i .. 16i + 15 of the stage (B rows are 128 B, SW128)
+      float dh[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      float dl[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = 2 * warp + j;
+      for (int kk = 0; kk < R / 16; ++kk) {
+        const int k = 16 * kk + ak, c = 2 * i + ac;
+        uint32_t a[4];
+        ldsm_x4_t(smem_u32(bs + k * 128 + ((c ^ (k & 7)) << 4)), a[0], a[1], a[2], a[3]);
+        mma16816<T>(dh[0], a, vh[kk][0], vh[kk][1]);
+        mma16816<T>(dl[0], a, vl[kk][0], vl[kk][1]);
+        if (two) {
+          mma16816<T>(dh[1], a, vh[kk][2], vh[kk][3]);
+          mma16816<T>(dl[1], a, vl[kk][2], vl[kk][3]);
+        }
+      }
+      // epilogue in place: y = rn((hi.B + lo.B) + y_old) for (col 16i + g (+8), row 8j + 2t (+1))
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = g + 8 * h;
-        uint32_t* q = reinterpret_cast<uint32_t*>(ys + m * 128 + ((c ^ (m & 7)) << 4) + 4 * t);
-        *q = add2_round<T>(*q, d[j][2 * h], d[j][2 * h + 1]);
+      for (int j = 0; j < 2; ++j) {
+        if (j == 1 && !two) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int m = 8 * j + 2 * t + (e & 1), col = 16 * i + g + (e >> 1) * 8;
+          T* q = reinterpret_cast<T*>(ys + m * 128 + (((col >> 3) ^ (m & 7)) << 4) + (col & 7) * 2);
+          *q = Cvt<T>::from_f(dh[j][e] + dl[j][e] + Cvt<T>::to_f(*q));
+        }
       }
     }
-    __syncthreads();  // the stage's y tile is complete
-    {  // 16-byte stores of the valid rows: thread = (row, chunk)
-      const int m = tid >> 3, c = tid & 7;
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {  // 16-byte stores of the valid rows: lane = (row, chunk)
+      const int m = it * 4 + (lane >> 3), c = lane & 7;
       if (m < rows)
         st_global_v4(Yg + static_cast<int64_t>(m) * p.ldy + s * kMmaKC + c * 8,
                      *reinterpret_cast<const uint4*>(ys + m * 128 + ((c ^ (m & 7)) << 4)));
-    }
-    __syncthreads();  // buffer b is free
-    if (s == 0) LSG_TC_TRACE(1, 4);
-    if (s + S < nst && tid == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&full[b], kSB);
-      tma_load_2d(bs, bmap, n0 + (s + S) * kMmaKC, 0, &full[b]);
-      tma_load_2d(ys, &p.tmap_y, n0 + (s + S) * kMmaKC, r0, &full[b]);
     }
   }
   LSG_TC_TRACE(1, 5);

@@ -1,0 +1,330 @@
+// sgmv_stream.cuh -- K9: one-pass streaming tensor-core kernel for long (prefill) segments.
+//
+// One CTA per 16-row tile of a long segment (grid = tile bound).  The tile's whole LoRA
+// site runs in one CTA, so no v round trip through global memory and no second launch:
+//
+//   shrink   v^T[R][16] = A^T . x^T over h_in in stages of KC columns (1024 at rank 16, else
+//            512): x as one 1-D bulk copy per row (KC * 2 bytes, rows padded by 16 bytes) and
+//            A by 2-D TMA over its 128-byte view rows (SW128)
+//   expand   y^T[cols][16] = B^T . (v_hi + v_lo)^T over h_out in stages of KC columns: B
+//            (R x 64 boxes, SW128) and y_old (one bulk copy per row); y = rn(D + y_old)
+//            written back in place and stored with one 1-D bulk store per row (the
+//            segment's rows only)
+//
+// Warp roles: warp 4 is the producer (builds this slot's A / B descriptors, then keeps a ring
+// of S stage slots full: weights are requested before the PDL wait, activations after it),
+// warps 0..3 consume -- shrink: a quarter of the k16-steps of every stage (the four warp sums
+// added in warp order at the end); expand: a quarter of the 64-column boxes.  Stage slots
+// are released through `empty` mbarriers (one arrive per consumer warp), so the x stream of
+// the shrink, the weight stream and the y_old / y streams of the expand run back to back
+// with no block-wide barrier except the one that turns the warp sums into v.
+//
+// The operands are swapped (the rank / the output columns are the MMA's M, the tile's rows
+// its N), so a tile of <= 8 rows runs one n8 tile; mma.sync m16n8k16 with fp32 accumulation.
+// Why a CTA per 16-row tile: prefill segments are activation-bound (h=4096, r=16: 16 KiB of
+// x and 32 KiB of y traffic per row against 256 KiB of weights per segment), so the weights
+// are re-read per tile from L2 while x / y stream once from HBM; 2048 rows = 128 CTAs.
+//
+// Canonical arithmetic for these rows: v = (sum over warps w ascending of the MMA chain over
+// warp w's k16-steps of every stage, stages ascending); y = rn((fp32(hi.B) + fp32(lo.B)) +
+// y_old).  Deterministic; within tolerance of the CUDA-core rows, not bitwise.
+#pragma once
+
+#include "sgmv_mma.cuh"
+
+namespace lsg {
+
+// 1-D bulk copy shared -> global (bulk async-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void named_barrier_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// phase stamp from any one thread (the producer warp's lane 0 included)
+#define LSG_STREAM_TRACE(i)                                                                        \
+  do {                                                                                             \
+    if (LSG_TC_TRACE_ON) {                                                                         \
+      const int cta_ = blockIdx.x;                                                                 \
+      if (cta_ < p.trace_ctas / 2) {                                                               \
+        unsigned long long gt_;                                                                    \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                                   \
+        p.trace[(p.trace_ctas + cta_) * 16 + (i)] = gt_;                                           \
+      }                                                                                            \
+    }                                                                                              \
+  } while (0)
+
+constexpr int kStreamThreads = 160;   // 4 consumer warps + 1 producer warp
+constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
+constexpr int kStreamSmem = 220 * 1024;
+
+// Stage geometry per rank: KC columns per stage (x / y_old rows move as one 1-D bulk copy
+// of KC * 2 bytes each -- >= 1 KiB pieces keep HBM streaming at full rate, 128-byte
+// tensor-box rows do not: scripts/tma_probe.cu), activation rows padded by 16 bytes so
+// ldmatrix is conflict-free, weights (A or B of the stage) first in the slot.
+__host__ __device__ constexpr int stream_kc(int R) { return R == 16 ? 1024 : 512; }
+__host__ __device__ constexpr uint32_t stream_pitch(int R) { return stream_kc(R) * 2 + 16; }
+__host__ __device__ constexpr uint32_t stream_wbytes(int R) { return stream_kc(R) * R * 2; }
+__host__ __device__ constexpr uint32_t stream_slot_bytes(int R) {
+  return (stream_wbytes(R) + kMmaM * stream_pitch(R) + 1023u) & ~1023u;
+}
+__host__ __device__ constexpr uint32_t stream_fixed(int R) {
+  return 1024 + 4 * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 + 16 * kStreamMaxStages;
+}
+__host__ __device__ constexpr uint32_t stream_smem(int R, int stages) {
+  return stream_fixed(R) + stages * stream_slot_bytes(R);
+}
+
+struct StreamParams {
+  CUtensorMap tmap_a;  // template: A of one layer viewed as [h_in * R / 64][64], box 64 x 256, SW128
+  CUtensorMap tmap_b;  // template: B of one layer [R, h_out], box 64 x R, SW128
+  const void* x;
+  void* y;
+  int64_t ldx;
+  int64_t ldy;
+  const void* const* a_ptr;
+  const void* const* b_ptr;
+  int64_t a_off;  // layer * a_layer_stride (elements)
+  int64_t b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  uint8_t* maps;  // 2 x 128-byte descriptor scratch per CTA
+  int32_t n_seg, s_n, num_slots, h_in, h_out;
+  int32_t stages;    // ring slots
+  int32_t min_rows;  // segments with >= min_rows rows take this kernel
+  unsigned long long* trace;
+  int32_t trace_ctas;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __grid_constant__ StreamParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
+  constexpr int ROWV = R * 2;                 // bytes per v row
+  constexpr int KC = stream_kc(R);
+  constexpr uint32_t PITCH = stream_pitch(R);
+  constexpr uint32_t kWB = stream_wbytes(R);  // weights of a stage (A: KC rows x R, B: R rows x KC)
+  constexpr uint32_t kSB = stream_slot_bytes(R);
+  constexpr int MT = R / 16;                  // m16 tiles of the rank
+  constexpr int KPR = 64 / R;                 // A rows per 128-byte view row
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int S = p.stages;
+  float* red = reinterpret_cast<float*>(smem + S * kSB);  // [4][16][R]
+  uint8_t* vhi = reinterpret_cast<uint8_t*>(red + 4 * kMmaM * R);
+  uint8_t* vlo = vhi + kMmaM * R * 2;
+  uint8_t* smap = vlo + kMmaM * R * 2;                       // 2 x 128 B
+  uint64_t* full = reinterpret_cast<uint64_t*>(smap + 256);  // [S]
+  uint64_t* empty = full + kStreamMaxStages;                 // [S]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nk = p.h_in / KC, nn = p.h_out / KC, nst = nk + nn;
+  // dependents (the short-segment kernel of this call, the next call) may start at once:
+  // every write of this kernel comes after its PDL wait
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) LSG_STREAM_TRACE(0);
+
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    mma_tile_of(p.seg_starts, p.n_seg, blockIdx.x, lane, p.min_rows, 0x7fffffff, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
+  if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {
+    if (blockIdx.x == 0) pdl_wait();  // this grid's completion implies the predecessor's
+    return;
+  }
+  const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
+  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
+
+  if (warp == 4) {  // ---------------------------------------------------------------- producer
+    uint8_t* gmap = p.maps + static_cast<int64_t>(blockIdx.x) * 256;
+    make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
+    make_slot_tmap(&p.tmap_b, smap + 128, gmap + 128, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
+    if (lane == 0) {
+      const CUtensorMap* amap = reinterpret_cast<const CUtensorMap*>(gmap);
+      const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap + 128);
+      const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx;
+      const T* Y = static_cast<const T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
+      const uint32_t bytes = kWB + static_cast<uint32_t>(rows) * KC * 2;
+      auto weights = [&](int i) {
+        uint8_t* sb = smem + (i % S) * kSB;
+        if (i < nk) {  // A rows [i*KC, (i+1)*KC) = view rows [i*KC/KPR, ...), boxes of 256 view rows
+          for (int b = 0; b < KC / KPR / 256; ++b)
+            tma_load_2d(sb + b * 256 * 128, amap, 0, i * (KC / KPR) + b * 256, &full[i % S]);
+        } else {
+          const int n0 = (i - nk) * KC;
+          for (int b = 0; b < KC / 64; ++b) tma_load_2d(sb + b * (R * 128), bmap, n0 + b * 64, 0, &full[i % S]);
+        }
+      };
+      auto acts = [&](int i) {  // x (shrink) or y_old (expand): one bulk copy per row of the tile
+        uint8_t* sb = smem + (i % S) * kSB + kWB;
+        const T* src = i < nk ? X + i * KC : Y + (i - nk) * KC;
+        const int64_t ld = i < nk ? p.ldx : p.ldy;
+        for (int m = 0; m < rows; ++m) bulk_g2s(sb + m * PITCH, src + m * ld, KC * 2, &full[i % S]);
+      };
+      const int pre = min(S, nst);
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], bytes);
+        weights(i);
+      }
+      LSG_STREAM_TRACE(1);
+      pdl_wait();  // x and y_old may come from the preceding kernel
+      LSG_STREAM_TRACE(2);
+      for (int i = 0; i < pre; ++i) acts(i);
+      for (int i = S; i < nst; ++i) {
+        mbar_wait(&empty[i % S], ((i / S) - 1) & 1);
+        mbar_arrive_expect_tx(&full[i % S], bytes);
+        weights(i);
+        acts(i);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------------ consumers
+  pdl_wait();  // (returns at once by the time any y is written)
+  const bool two = rows > 8;  // second n8 tile (rows 8..15)
+  const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;  // row-major 16 x 16 blocks
+  const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;  // .trans blocks of [k][n] rows
+  float acc[MT][2][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0.f;
+  for (int s = 0; s < nk; ++s) {  // ---- shrink: k16-steps [w * KC/64, (w+1) * KC/64) of every stage
+    mbar_wait(&full[s % S], (s / S) & 1);
+    if (s == 0 && tid == 0) LSG_STREAM_TRACE(3);
+    const uint32_t as = smem_u32(smem + (s % S) * kSB), xs = as + kWB;
+#pragma unroll 4
+    for (int q = 0; q < KC / 64; ++q) {
+      const int kk = warp * (KC / 64) + q;
+      uint32_t b[4];  // x^T: {b0, b1} rows 0..7, {b2, b3} rows 8..15 (padded rows)
+      ldsm_x4(xs + xr * PITCH + (2 * kk + xc) * 16, b[0], b[1], b[2], b[3]);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {  // A^T block (rank 16i.., k 16kk..) from the 128-byte view rows
+        const int k = 16 * kk + ak, c = (k % KPR) * (R / 8) + 2 * i + ac, vq = k / KPR;
+        uint32_t a[4];
+        ldsm_x4_t(as + vq * 128 + ((c ^ (vq & 7)) << 4), a[0], a[1], a[2], a[3]);
+        mma16816<T>(acc[i][0], a, b[0], b[1]);
+        if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(&empty[s % S]);
+  }
+  {  // ---- v = sum of the warp partials in warp order -> 16-bit hi + lo
+    const int g = lane >> 2, t = lane & 3;
+    float* rw = red + warp * kMmaM * R;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m0 = 8 * j + 2 * t, r = 16 * i + g;
+        rw[m0 * R + r] = acc[i][j][0];
+        rw[(m0 + 1) * R + r] = acc[i][j][1];
+        rw[m0 * R + r + 8] = acc[i][j][2];
+        rw[(m0 + 1) * R + r + 8] = acc[i][j][3];
+      }
+  }
+  named_barrier_sync(1, 128);
+  if (tid == 0) LSG_STREAM_TRACE(4);
+  for (int i = tid * 8; i < kMmaM * R; i += 128 * 8) {
+    float f[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = ((red[i + e] + red[kMmaM * R + i + e]) + red[2 * kMmaM * R + i + e]) +
+                                       red[3 * kMmaM * R + i + e];
+    float hf[8], lo[8];
+    const uint4 hi = Cvt<T>::pack8(f);
+    Cvt<T>::unpack8(hi, hf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) lo[e] = f[e] - hf[e];
+    const int m = i / R, c = (i - m * R) >> 3;
+    const uint32_t off = m * ROWV + ((c ^ swz<ROWV>(m)) << 4);
+    *reinterpret_cast<uint4*>(vhi + off) = hi;
+    *reinterpret_cast<uint4*>(vlo + off) = Cvt<T>::pack8(lo);
+  }
+  named_barrier_sync(1, 128);
+  uint32_t vh[R / 16][4], vl[R / 16][4];  // v^T fragments: {b0, b1} rows 0..7, {b2, b3} rows 8..15
+#pragma unroll
+  for (int kk = 0; kk < R / 16; ++kk) {
+    const int c = 2 * kk + xc;
+    const uint32_t off = xr * ROWV + ((c ^ swz<ROWV>(xr)) << 4);
+    ldsm_x4(smem_u32(vhi + off), vh[kk][0], vh[kk][1], vh[kk][2], vh[kk][3]);
+    ldsm_x4(smem_u32(vlo + off), vl[kk][0], vl[kk][1], vl[kk][2], vl[kk][3]);
+  }
+  const int g = lane >> 2, t = lane & 3;
+  T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
+  constexpr int BPW = KC / 64 / 4;  // 64-column boxes per warp per stage
+  for (int j = 0; j < nn; ++j) {  // ---- expand: boxes [w * BPW, (w+1) * BPW) of every stage
+    const int s = nk + j;
+    mbar_wait(&full[s % S], (s / S) & 1);
+    uint8_t* bs = smem + (s % S) * kSB;
+    uint8_t* ys = bs + kWB;
+#pragma unroll 1
+    for (int bq = warp * BPW; bq < (warp + 1) * BPW; ++bq) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // columns 64bq + 16i .. + 15
+        float dh[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        float dl[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < R / 16; ++kk) {
+          const int k = 16 * kk + ak, c = 2 * i + ac;
+          uint32_t a[4];
+          ldsm_x4_t(smem_u32(bs + bq * (R * 128) + k * 128 + ((c ^ (k & 7)) << 4)), a[0], a[1], a[2], a[3]);
+          mma16816<T>(dh[0], a, vh[kk][0], vh[kk][1]);
+          mma16816<T>(dl[0], a, vl[kk][0], vl[kk][1]);
+          if (two) {
+            mma16816<T>(dh[1], a, vh[kk][2], vh[kk][3]);
+            mma16816<T>(dl[1], a, vl[kk][2], vl[kk][3]);
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          if (jj == 1 && !two) break;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int m = 8 * jj + 2 * t + (e & 1), col = 64 * bq + 16 * i + g + (e >> 1) * 8;
+            T* q = reinterpret_cast<T*>(ys + m * PITCH + col * 2);
+            *q = Cvt<T>::from_f((dh[jj][e] + dl[jj][e]) + Cvt<T>::to_f(*q));
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();     // epilogue writes -> the bulk stores
+    named_barrier_sync(1, 128);   // the stage's y tile is complete
+    if (lane == 0) {              // warp w stores rows 4w .. 4w + 3 (the segment's rows only)
+      for (int m = 4 * warp; m < 4 * warp + 4 && m < rows; ++m)
+        bulk_s2g(Yg + static_cast<int64_t>(m) * p.ldy + j * KC, ys + m * PITCH, KC * 2);
+      bulk_commit_group();
+      // the previous stage's slot is free once its stores have read it (this one stays in flight)
+      bulk_wait_group_read<1>();
+      if (j > 0) mbar_arrive_local(&empty[(s - 1) % S]);
+    }
+  }
+  if (lane == 0) {  // the last stage's stores
+    bulk_wait_group_read<0>();
+    mbar_arrive_local(&empty[(nst - 1) % S]);
+  }
+  if (tid == 0) LSG_STREAM_TRACE(5);
+}
+
+}  // namespace lsg

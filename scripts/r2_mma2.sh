@@ -1,6 +1,6 @@
 #!/bin/bash
 # MMA pair (TMA version): parity, benches, traces
-cd $GRAFT_REPO_ROOT; o=gpurun_out/mma2; mkdir -p $o
+cd $GRAFT_REPO_ROOT; o=gpurun_out/mma5; mkdir -p $o
 timeout 900 python -m pytest tests/test_sgmv_gpu.py -q -m gpu -x -k "mma or rank64 or grouped_sites_rank64 or baseline_shapes" > $o/pytest.log 2>&1; tail -3 $o/pytest.log
 B="python bench.py --no-extras --no-e2e --no-cpu-baseline --no-traffic --steps 20 --warmup 3"
 j() { echo "== $*" >> $o/bench.txt; timeout 300 $B "$@" 2>>$o/bench.err | python -c "

@@ -19,6 +19,7 @@ EXPAND = ["entry", "weights_staged", "pdl_wait_done", "y_landed", "d2_ready", "e
 
 
 MMA_P = ["entry", "a_issued", "pdl_wait_done", "stage0_landed", "mma_done", "end"]
+STREAM = ["entry", "weights_issued", "pdl_wait_done", "stage0_landed", "v_ready", "end"]
 MMA_E = ["entry", "b_y_issued", "pdl_wait_done", "v_ready", "stage0_stored", "end"]
 FUSED = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "v_ready", "chunk0_ready", "chunk1_ready",
          "end"]
@@ -79,8 +80,11 @@ def main():
     allt = buf.view(2 * ctas, 16).cpu().double()
     t0 = None
     names = (MMA_P, MMA_E) if mma else (SHRINK, EXPAND)
+    if a.gen == 4:
+        two, names = False, None
     groups = ((("shrink", names[0], allt[ctas:ctas + ctas // 2]), ("expand", names[1], allt[ctas + ctas // 2:]))
-              if two else (("fused", FUSED, allt[ctas:ctas + ctas // 2]),))
+              if two else (("stream" if a.gen == 4 else "fused", STREAM if a.gen == 4 else FUSED,
+                            allt[ctas:ctas + ctas // 2]),))
     for name, phases, part in groups:
         tv = part[part[:, len(phases) - 1] != 0]
         if not tv.numel():

@@ -913,14 +913,16 @@ def test_mma_pair_shared_adapters_match_oracle(lsg, dtype, shape, pop):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("r", [16, 32, 64])
-@pytest.mark.parametrize("lens", [[128] + [1] * 31, [300, 17, 1, 5, 2, 16], [2048, 3, 1]])
-def test_mma_pair_long_segments_match_oracle(lsg, dtype, r, lens):
-    """LSG_OPT_TC_LEGACY = 3: the MMA pair takes the long (prefill) segments as well; with
+@pytest.mark.parametrize("lens", [[128] + [1] * 31, [300, 17, 1, 5, 2, 16], [2048, 3, 1], [129, 135, 7]])
+@pytest.mark.parametrize("gen", [3, 4])
+def test_mma_pair_long_segments_match_oracle(lsg, dtype, r, lens, gen):
+    """LSG_OPT_TC_LEGACY = 3: the MMA pair takes the long (prefill) segments as well; = 4: the
+    one-pass streaming kernel takes them (MMA pair for the medium ones); with
     LSG_OPT_MMA_MIN_ROWS = 2 the 1-row segments stay on the CUDA-core kernel in the same call."""
     bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
     x, A, B = random_problem(4096, 4096, r, bounds, 600 + r)
     p = Problem(lsg, x, A, B, bounds, dtype)
-    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 3)
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, gen)
     for lo in (1, 2):
         lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, lo)
         y = p.run()
