@@ -299,11 +299,12 @@ typedef enum {
                                    host does not read segment lengths), which costs ~1 us per launch
                                    at 128-256 decode rows: an engine that knows a step has no prefill
                                    segment sets it above the batch size for that step. */
-  LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation (A/B measurements): 0 (default) the
-                                   cluster-free partials + expand pair; 1 the first fused cluster kernel
-                                   (rank 16); 2 the streamed cluster kernel (ranks 16 / 32); 3 the
-                                   segment-tile MMA pair (16-row tiles, mma.sync); 4 the one-pass
-                                   streaming kernel (a CTA per 16-row tile) */
+  LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation: 0 (default) auto -- the one-pass
+                                   streaming kernel (a CTA per 16-row tile) for calls of >= 1024 rows,
+                                   else the segment-tile MMA pair; A/B measurements: 1 the first fused
+                                   cluster kernel (rank 16); 2 the streamed cluster kernel (ranks 16 / 32);
+                                   3 the segment-tile MMA pair; 4 the streaming kernel; 5 the
+                                   cluster-free tcgen05 partials + expand pair */
   LSG_OPT_MMA_MIN_ROWS = 11     /* segments with at least this many rows (and below the long-segment
                                    threshold) take the segment-tile MMA pair; 0 (default) = auto: rank 64
                                    calls whose rows share adapters (total_rows > num_segments) send every

@@ -175,14 +175,28 @@ bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
 // A/B option picks an earlier generation: LSG_OPT_TC_LEGACY 1 = the first fused kernel
 // (rank 16), 2 = the streamed cluster kernel (ranks 16 / 32); LSG_OPT_TC_SPLIT = the
 // first two-kernel form.
-bool tc3_ok(const lsg_weight_table* t) {
-  return !cur().tc_split && cur().tc_legacy == 0 && tc_nq(t) > 0 && t->h_out % kTcNT == 0;
+bool mma_shape_ok(const lsg_weight_table* t);
+bool stream_shape_ok(const lsg_weight_table* t) {
+  return (t->rank == 16 || t->rank == 32 || t->rank == 64) && t->h_in % 1024 == 0 && t->h_out % 1024 == 0 &&
+         t->a_layer_stride % 8 == 0 && t->b_layer_stride % 8 == 0;
 }
-// K9 streaming kernel (sgmv_stream.cuh): LSG_OPT_TC_LEGACY = 4
-bool stream_ok(const lsg_weight_table* t) {
-  return !cur().tc_split && cur().tc_legacy == 4 && (t->rank == 16 || t->rank == 32 || t->rank == 64) &&
-         t->h_in % 1024 == 0 && t->h_out % 1024 == 0 && t->a_layer_stride % 8 == 0 &&
-         t->b_layer_stride % 8 == 0;
+// Long-segment kernel generation of a call (LSG_OPT_TC_LEGACY): 0 = auto -- the one-pass
+// streaming kernel (K9, sgmv_stream.cuh) for calls of >= 1024 rows (enough 16-row tiles to
+// fill the GPU), else the segment-tile MMA pair (K7); explicit 1 / 2 = the cluster kernels,
+// 3 = the MMA pair, 4 = the streaming kernel, 5 = the cluster-free tcgen05 pair (sgmv_tc3.cuh).
+constexpr int kStreamMinRows = 1024;
+int tc_gen(const lsg_weight_table* t, int s_n) {
+  const int g = cur().tc_legacy;
+  if (g != 0) return g;
+  if (s_n >= kStreamMinRows && stream_shape_ok(t)) return 4;
+  if (mma_shape_ok(t)) return 3;
+  return 5;
+}
+bool tc3_ok(const lsg_weight_table* t, int s_n) {
+  return !cur().tc_split && tc_gen(t, s_n) == 5 && tc_nq(t) > 0 && t->h_out % kTcNT == 0;
+}
+bool stream_ok(const lsg_weight_table* t, int s_n) {
+  return !cur().tc_split && tc_gen(t, s_n) == 4 && stream_shape_ok(t);
 }
 int stream_tiles(int s_n, int n_seg) {  // 16-row tiles of the segments with >= tc_min_rows rows
   return std::max(1, s_n / 16 + std::min(n_seg, s_n / tc_min_rows()));
@@ -191,10 +205,14 @@ size_t tc3_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg) {
   return static_cast<size_t>(tc_tile_bound(s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
 }
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
-  if (tc_nq(t) > 0 && s_n >= tc_min_rows() && stream_ok(t)) return static_cast<size_t>(stream_tiles(s_n, s_n)) * 256;
-  if (tc_nq(t) > 0 && s_n >= tc_min_rows() && tc3_ok(t)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows());
+  if (tc_nq(t) == 0 || s_n < tc_min_rows()) return 0;
+  if (stream_ok(t, s_n)) return static_cast<size_t>(stream_tiles(s_n, s_n)) * 256;
+  if (tc3_ok(t, s_n)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows());
+  if (!cur().tc_split && tc_gen(t, s_n) == 3) return 0;  // the MMA pair's own region (row_ranges)
   // the fused kernels keep v on chip
-  if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) || tc_fused_c(t, nullptr) > 0)) return 0;
+  if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) ||
+                           (cur().tc_legacy == 1 && tc_fused_c(t, nullptr) > 0)))
+    return 0;
   return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
@@ -217,7 +235,7 @@ RowRanges row_ranges(const lsg_weight_table* t, int n_seg, int s_n) {
   RowRanges rr;
   if (cur().no_tc) return rr;
   const bool tc = tc_nq(t) > 0 && s_n >= tc_min_rows();
-  const bool gen3 = cur().tc_legacy == 3 && mma_shape_ok(t);
+  const bool gen3 = !cur().tc_split && tc_gen(t, s_n) == 3 && mma_shape_ok(t);
   if (tc && !gen3) rr.tc_lo = tc_min_rows();
   int lo = cur().mma_min_rows;
   if (lo <= 0) lo = (t->rank == 64 && s_n > n_seg) ? 1 : 0;
@@ -464,7 +482,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   const int nq = tc_nq(tbl);
   if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
-  if (stream_ok(tbl)) {
+  if (stream_ok(tbl, s_n)) {
     const int tiles = stream_tiles(s_n, n_seg), R = tbl->rank;
     if (ws == nullptr || !aligned16(ws) || ws_bytes < static_cast<size_t>(tiles) * 256) return false;
     StreamParams& q = lp.sp9;
@@ -500,7 +518,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     q.trace_ctas = g_trace_ctas;
     return true;
   }
-  if (tc3_ok(tbl)) {
+  if (tc3_ok(tbl, s_n)) {
     if (ws == nullptr || !aligned16(ws) || ws_bytes < tc3_ws_bytes(tbl, s_n, n_seg)) return false;
     Tc3PartParams& pp = lp.pp;
     Tc3ExpParams& xp = lp.xp;
@@ -1282,7 +1300,7 @@ int lsg_set_option(int32_t option, int32_t value) {
       g_opt_tc_min_rows = value;
       return LSG_OK;
     case LSG_OPT_TC_LEGACY:
-      if (value < 0 || value > 4) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0 .. 4");
+      if (value < 0 || value > 5) return fail(LSG_EINVAL, "lsg: tensor-core generation must be 0 .. 5");
       g_opt_tc_legacy = value;
       return LSG_OK;
     case LSG_OPT_MMA_MIN_ROWS:

@@ -62,7 +62,8 @@ __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
     }                                                                                              \
   } while (0)
 
-constexpr int kStreamThreads = 160;   // 4 consumer warps + 1 producer warp
+constexpr int kStreamCW = 8;          // consumer warps
+constexpr int kStreamThreads = 32 * (kStreamCW + 1);  // + 1 producer warp
 constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
 constexpr int kStreamSmem = 220 * 1024;
 
@@ -77,7 +78,7 @@ __host__ __device__ constexpr uint32_t stream_slot_bytes(int R) {
   return (stream_wbytes(R) + kMmaM * stream_pitch(R) + 1023u) & ~1023u;
 }
 __host__ __device__ constexpr uint32_t stream_fixed(int R) {
-  return 1024 + 4 * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 + 16 * kStreamMaxStages;
+  return 1024 + kStreamCW * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 + 16 * kStreamMaxStages;
 }
 __host__ __device__ constexpr uint32_t stream_smem(int R, int stages) {
   return stream_fixed(R) + stages * stream_slot_bytes(R);
@@ -117,8 +118,8 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int S = p.stages;
-  float* red = reinterpret_cast<float*>(smem + S * kSB);  // [4][16][R]
-  uint8_t* vhi = reinterpret_cast<uint8_t*>(red + 4 * kMmaM * R);
+  float* red = reinterpret_cast<float*>(smem + S * kSB);  // [kStreamCW][16][R]
+  uint8_t* vhi = reinterpret_cast<uint8_t*>(red + kStreamCW * kMmaM * R);
   uint8_t* vlo = vhi + kMmaM * R * 2;
   uint8_t* smap = vlo + kMmaM * R * 2;                       // 2 x 128 B
   uint64_t* full = reinterpret_cast<uint64_t*>(smap + 256);  // [S]
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   if (tid == 32) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 4);
+      mbar_init(&empty[i], kStreamCW);
     }
     fence_mbar_init();
   }
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
   const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
 
-  if (warp == 4) {  // ---------------------------------------------------------------- producer
+  if (warp == kStreamCW) {  // --------------------------------------------------------- producer
     uint8_t* gmap = p.maps + static_cast<int64_t>(blockIdx.x) * 256;
     make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
     make_slot_tmap(&p.tmap_b, smap + 128, gmap + 128, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
@@ -186,6 +187,12 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
         mbar_arrive_expect_tx(&full[i], bytes);
         weights(i);
       }
+      // the tile's x and y_old rows into L2 now (hints only: safe while the preceding kernel
+      // runs), so the post-wait copies hit L2 instead of queueing in HBM
+      for (int m = 0; m < rows; ++m) {
+        bulk_prefetch_l2(X + m * p.ldx, static_cast<uint32_t>(p.h_in * 2));
+        bulk_prefetch_l2(Y + m * p.ldy, static_cast<uint32_t>(p.h_out * 2));
+      }
       LSG_STREAM_TRACE(1);
       pdl_wait();  // x and y_old may come from the preceding kernel
       LSG_STREAM_TRACE(2);
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
 
   // ------------------------------------------------------------------------------ consumers
   pdl_wait();  // (returns at once by the time any y is written)
-  const bool two = rows > 8;  // second n8 tile (rows 8..15)
+  const bool two = rows > 8;  // second n8 tile of the shrink (rows 8..15)
   const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;  // row-major 16 x 16 blocks
   const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;  // .trans blocks of [k][n] rows
   float acc[MT][2][4];
@@ -210,13 +217,14 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0.f;
-  for (int s = 0; s < nk; ++s) {  // ---- shrink: k16-steps [w * KC/64, (w+1) * KC/64) of every stage
+  constexpr int KPW = KC / 16 / kStreamCW;  // k16-steps per warp per stage
+  for (int s = 0; s < nk; ++s) {  // ---- shrink: k16-steps [w * KPW, (w+1) * KPW) of every stage
     mbar_wait(&full[s % S], (s / S) & 1);
     if (s == 0 && tid == 0) LSG_STREAM_TRACE(3);
     const uint32_t as = smem_u32(smem + (s % S) * kSB), xs = as + kWB;
 #pragma unroll 4
-    for (int q = 0; q < KC / 64; ++q) {
-      const int kk = warp * (KC / 64) + q;
+    for (int q = 0; q < KPW; ++q) {
+      const int kk = warp * KPW + q;
       uint32_t b[4];  // x^T: {b0, b1} rows 0..7, {b2, b3} rows 8..15 (padded rows)
       ldsm_x4(xs + xr * PITCH + (2 * kk + xc) * 16, b[0], b[1], b[2], b[3]);
 #pragma unroll
@@ -245,13 +253,17 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
         rw[(m0 + 1) * R + r + 8] = acc[i][j][3];
       }
   }
-  named_barrier_sync(1, 128);
+  named_barrier_sync(1, 32 * kStreamCW);
   if (tid == 0) LSG_STREAM_TRACE(4);
-  for (int i = tid * 8; i < kMmaM * R; i += 128 * 8) {
+  for (int i = tid * 8; i < kMmaM * R; i += 32 * kStreamCW * 8) {
     float f[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = ((red[i + e] + red[kMmaM * R + i + e]) + red[2 * kMmaM * R + i + e]) +
-                                       red[3 * kMmaM * R + i + e];
+    for (int e = 0; e < 8; ++e) {
+      float a = red[i + e];
+#pragma unroll
+      for (int w = 1; w < kStreamCW; ++w) a += red[w * kMmaM * R + i + e];
+      f[e] = a;
+    }
     float hf[8], lo[8];
     const uint4 hi = Cvt<T>::pack8(f);
     Cvt<T>::unpack8(hi, hf);
@@ -262,57 +274,60 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
     *reinterpret_cast<uint4*>(vhi + off) = hi;
     *reinterpret_cast<uint4*>(vlo + off) = Cvt<T>::pack8(lo);
   }
-  named_barrier_sync(1, 128);
-  uint32_t vh[R / 16][4], vl[R / 16][4];  // v^T fragments: {b0, b1} rows 0..7, {b2, b3} rows 8..15
+  named_barrier_sync(1, 32 * kStreamCW);
+  // expand, rows as the MMA's M (a 16-row tile fills it): A fragments of v (hi and lo) for
+  // every k16-step, B by ldmatrix.trans from the stage's [R][64] boxes; the accumulator
+  // pairs (row, 2 adjacent columns) update y_old in place as 32-bit words
+  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = lane >> 4;
+  uint32_t ah[R / 16][4], al[R / 16][4];
 #pragma unroll
   for (int kk = 0; kk < R / 16; ++kk) {
-    const int c = 2 * kk + xc;
-    const uint32_t off = xr * ROWV + ((c ^ swz<ROWV>(xr)) << 4);
-    ldsm_x4(smem_u32(vhi + off), vh[kk][0], vh[kk][1], vh[kk][2], vh[kk][3]);
-    ldsm_x4(smem_u32(vlo + off), vl[kk][0], vl[kk][1], vl[kk][2], vl[kk][3]);
+    const int c = 2 * kk + lc;
+    const uint32_t off = lr * ROWV + ((c ^ swz<ROWV>(lr)) << 4);
+    ldsm_x4(smem_u32(vhi + off), ah[kk][0], ah[kk][1], ah[kk][2], ah[kk][3]);
+    ldsm_x4(smem_u32(vlo + off), al[kk][0], al[kk][1], al[kk][2], al[kk][3]);
   }
   const int g = lane >> 2, t = lane & 3;
   T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
-  constexpr int BPW = KC / 64 / 4;  // 64-column boxes per warp per stage
+  constexpr int BPW = KC / 64 / kStreamCW;  // 64-column boxes per warp per stage
   for (int j = 0; j < nn; ++j) {  // ---- expand: boxes [w * BPW, (w+1) * BPW) of every stage
     const int s = nk + j;
     mbar_wait(&full[s % S], (s / S) & 1);
     uint8_t* bs = smem + (s % S) * kSB;
     uint8_t* ys = bs + kWB;
-#pragma unroll 1
-    for (int bq = warp * BPW; bq < (warp + 1) * BPW; ++bq) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // columns 64bq + 16i .. + 15
-        float dh[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        float dl[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int bi = 0; bi < BPW; ++bi) {
+      const int bq = warp * BPW + bi;
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {  // n8 tiles 2jp, 2jp+1 of the box (B rows are 128 B, SW128)
+        float d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        float e2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
         for (int kk = 0; kk < R / 16; ++kk) {
-          const int k = 16 * kk + ak, c = 2 * i + ac;
-          uint32_t a[4];
-          ldsm_x4_t(smem_u32(bs + bq * (R * 128) + k * 128 + ((c ^ (k & 7)) << 4)), a[0], a[1], a[2], a[3]);
-          mma16816<T>(dh[0], a, vh[kk][0], vh[kk][1]);
-          mma16816<T>(dl[0], a, vl[kk][0], vl[kk][1]);
-          if (two) {
-            mma16816<T>(dh[1], a, vh[kk][2], vh[kk][3]);
-            mma16816<T>(dl[1], a, vl[kk][2], vl[kk][3]);
-          }
+          const int k = 16 * kk + lr, c = 2 * jp + lc;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(smem_u32(bs + bq * (R * 128) + k * 128 + ((c ^ (k & 7)) << 4)), b0, b1, b2, b3);
+          mma16816<T>(d[0], ah[kk], b0, b1);
+          mma16816<T>(d[1], ah[kk], b2, b3);
+          mma16816<T>(e2[0], al[kk], b0, b1);
+          mma16816<T>(e2[1], al[kk], b2, b3);
         }
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
-          if (jj == 1 && !two) break;
+          const int col = 64 * bq + 8 * (2 * jp + jj) + 2 * t;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int m = 8 * jj + 2 * t + (e & 1), col = 64 * bq + 16 * i + g + (e >> 1) * 8;
-            T* q = reinterpret_cast<T*>(ys + m * PITCH + col * 2);
-            *q = Cvt<T>::from_f((dh[jj][e] + dl[jj][e]) + Cvt<T>::to_f(*q));
+          for (int h = 0; h < 2; ++h) {
+            const int m = g + 8 * h;
+            uint32_t* q = reinterpret_cast<uint32_t*>(ys + m * PITCH + col * 2);
+            *q = add2_round<T>(*q, d[jj][2 * h] + e2[jj][2 * h], d[jj][2 * h + 1] + e2[jj][2 * h + 1]);
           }
         }
       }
     }
-    fence_proxy_async_smem();     // epilogue writes -> the bulk stores
-    named_barrier_sync(1, 128);   // the stage's y tile is complete
-    if (lane == 0) {              // warp w stores rows 4w .. 4w + 3 (the segment's rows only)
-      for (int m = 4 * warp; m < 4 * warp + 4 && m < rows; ++m)
+    fence_proxy_async_smem();                 // epilogue writes -> the bulk stores
+    named_barrier_sync(1, 32 * kStreamCW);    // the stage's y tile is complete
+    if (lane == 0) {                          // warp w stores rows 2w, 2w + 1 (the segment's rows only)
+      for (int m = 2 * warp; m < 2 * warp + 2 && m < rows; ++m)
         bulk_s2g(Yg + static_cast<int64_t>(m) * p.ldy + j * KC, ys + m * PITCH, KC * 2);
       bulk_commit_group();
       // the previous stage's slot is free once its stores have read it (this one stays in flight)

@@ -302,11 +302,16 @@ Matrix addon_on_device(const Batch& batch, std::size_t rank, std::size_t h_out, 
   auto* slot = upload_identity_slots(n);
   auto lst = reinterpret_cast<lsg_stream_t>(st);
   switch (form) {
-    case Form::Fused:
-      lsg_check(lsg_sgmv(dy, static_cast<int64_t>(h_out), dx, static_cast<int64_t>(h_in), &sm.tbl, seg, slot, n32,
-                         rows32, 0, lst),
-                "lsg_sgmv");
+    case Form::Fused: {
+      // The drop-in keeps decode-length segments on the canonical CUDA-core arithmetic (the
+      // segment-tile MMA pair off), so lora_addon, lora_loop_oracle and gather_bmm_oracle agree
+      // bit for bit -- verify_sgmv's tolerance (experiments.cpp:79-80) assumes that.
+      const lsg_call_opts opts{-1, -1, -1, 1 << 30};
+      lsg_check(lsg_sgmv_ex(dy, static_cast<int64_t>(h_out), dx, static_cast<int64_t>(h_in), &sm.tbl, seg, slot, n32,
+                            rows32, 0, nullptr, 0, &opts, lst),
+                "lsg_sgmv_ex");
       break;
+    }
     case Form::TwoLaunch: {
       auto* dv = static_cast<float*>(t_arena.get(kV, rows * rank * 4));
       lsg_check(lsg_sgmv_shrink(dv, dx, static_cast<int64_t>(h_in), &sm.tbl, seg, slot, n32, rows32, 0, lst),

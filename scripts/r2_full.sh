@@ -4,7 +4,7 @@
 # ncu launch list + full captures of the headline, c3 and c4 kernels.
 # Usage (under gpurun): bash scripts/r2_full.sh [tests] [bench] [san] [ncu]
 cd $GRAFT_REPO_ROOT
-o=gpurun_out/r2; mkdir -p $o $o/san
+o=${OUT:-gpurun_out/r2}; mkdir -p $o $o/san
 st=$o/status.txt; : > $st
 what="${*:-tests bench san ncu}"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $o/smi.txt 2>&1

@@ -1,7 +1,7 @@
 #!/bin/bash
 # K9 streaming kernel: parity, c4 benches against tc3, trace
-cd $GRAFT_REPO_ROOT; o=gpurun_out/stream3; mkdir -p $o
-timeout 900 python -m pytest tests/test_sgmv_gpu.py -q -m gpu -x -k "mma_pair_long" > $o/pytest.log 2>&1; tail -3 $o/pytest.log
+cd $GRAFT_REPO_ROOT; o=gpurun_out/stream4; mkdir -p $o
+timeout 900 python -m pytest tests/test_sgmv_gpu.py -q -m gpu -k "mma_pair_long or long_segments_tensor_core or dropin" > $o/pytest.log 2>&1; tail -3 $o/pytest.log
 B="python bench.py --no-extras --no-e2e --no-cpu-baseline --no-traffic --steps 20 --warmup 3"
 j() { echo "== $*" >> $o/bench.txt; timeout 300 $B "$@" 2>>$o/bench.err | python -c "
 import sys,json
