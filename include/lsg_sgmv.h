@@ -316,7 +316,8 @@ int lsg_get_option(int32_t option);
 /* Launch configuration the next call with these scalars would use (for
  * tests and the benchmark's roofline bookkeeping).  path: 0 fast, 1 generic. */
 typedef struct lsg_launch_info {
-  int32_t path;
+  int32_t path;         /* 0 CUDA-core fast path, 1 generic, 2 every segment on the segment-tile MMA pair
+                           (cluster = K-split cluster, tile_rows = 16, row_splits = K split) */
   int32_t cluster;
   int32_t tile_rows;
   int32_t row_splits;

@@ -303,6 +303,20 @@ bool encode_map_2d(CUtensorMap* m, int dtype, const void* base, uint64_t cols, u
                            2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// K split, its cluster (the largest <= 8 dividing it: one partial per cluster) and column split
+bool mma_splits(const lsg_weight_table* tbl, int tiles, int& kparts, int& pc, int& ncol) {
+  const int R = tbl->rank;
+  kparts = mma_split(tbl->h_in / kMmaKC, tiles, mma_part_max_st(R), kMmaPartTarget);
+  if (kparts == 0) return false;
+  pc = 1;
+  for (int c = kMmaMaxPc; c >= 2; --c)
+    if (kparts % c == 0) {
+      pc = c;
+      break;
+    }
+  ncol = mma_split(tbl->h_out / kMmaKC, tiles, mma_exp_max_st(R, kparts / pc), kMmaExpTarget);
+  return ncol > 0;
+}
 bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_t ldy, const void* x, int64_t ldx,
                  const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg, int s_n,
                  int layer, void* ws, size_t ws_bytes) {
@@ -333,17 +347,7 @@ bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_
   mp.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
   mp.seg_starts = seg_starts;
   mp.seg_slot = seg_slot;
-  mp.kparts = mma_split(tbl->h_in / kMmaKC, tiles, mma_part_max_st(R), kMmaPartTarget);
-
-  if (mp.kparts == 0) return false;
-  mp.pc = 1;  // the largest cluster (<= 8) that divides the K split: one partial per cluster
-  for (int c = kMmaMaxPc; c >= 2; --c)
-    if (mp.kparts % c == 0) {
-      mp.pc = c;
-      break;
-    }
-  mp.ncol = mma_split(tbl->h_out / kMmaKC, tiles, mma_exp_max_st(R, mp.kparts / mp.pc), kMmaExpTarget);
-  if (mp.ncol == 0) return false;
+  if (!mma_splits(tbl, tiles, mp.kparts, mp.pc, mp.ncol)) return false;
   mp.ws = static_cast<float*>(ws);
   const size_t pctas = mma_part_ctas(tbl, tiles);
   mp.maps_p = static_cast<uint8_t*>(ws) + pctas * kMmaM * R * sizeof(float);
@@ -487,12 +491,11 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     if (ws == nullptr || !aligned16(ws) || ws_bytes < static_cast<size_t>(tiles) * 256) return false;
     StreamParams& q = lp.sp9;
     q = StreamParams{};
-    if (!encode_map_2d(&q.tmap_a, tbl->dtype, x, 64, static_cast<uint64_t>(tbl->h_in) * R / 64, 64, 64, 256,
+    const int abox = R == 16 ? stream_a_box_rows(16) : R == 32 ? stream_a_box_rows(32) : stream_a_box_rows(64);
+    if (!encode_map_2d(&q.tmap_a, tbl->dtype, x, 64, static_cast<uint64_t>(tbl->h_in) * R / 64, 64, 64, abox,
                        CU_TENSOR_MAP_SWIZZLE_128B) ||
         !encode_map_2d(&q.tmap_b, tbl->dtype, x, tbl->h_out, R, tbl->h_out, 64, R, CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
-    lp.stream9 = 1;
-    lp.tiles = tiles;
     q.x = x;
     q.y = y;
     q.ldx = ldx;
@@ -509,10 +512,14 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     q.num_slots = tbl->num_slots;
     q.h_in = tbl->h_in;
     q.h_out = tbl->h_out;
-    const int kc = R == 16 ? 1024 : 512, nst = tbl->h_in / kc + tbl->h_out / kc;
+    const int kc = R == 16 ? stream_kc(16) : stream_kc(32), nst = tbl->h_in / kc + tbl->h_out / kc;
     const uint32_t fixed = R == 16 ? stream_fixed(16) : R == 32 ? stream_fixed(32) : stream_fixed(64);
     const uint32_t slotb = R == 16 ? stream_slot_bytes(16) : R == 32 ? stream_slot_bytes(32) : stream_slot_bytes(64);
-    q.stages = std::max(1, std::min({nst, kStreamMaxStages, static_cast<int>((kStreamSmem - fixed) / slotb)}));
+    // >= 2 slots: the expand releases a slot only after the NEXT stage's stores are issued
+    q.stages = std::min({nst, kStreamMaxStages, static_cast<int>((kStreamSmem - fixed) / slotb)});
+    if (q.stages < 2 || nst < 2) return false;
+    lp.stream9 = 1;
+    lp.tiles = tiles;
     q.min_rows = tc_min_rows();
     q.trace = g_trace;
     q.trace_ctas = g_trace_ctas;
@@ -1340,6 +1347,20 @@ int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t 
     return LSG_OK;
   }
   const Plan pl = make_plan(tbl, kernel, num_segments, total_rows, fast_shape_ok(tbl));
+  if (kernel == kKFused && pl.path == 0) {  // every segment on the segment-tile MMA pair (K7)?
+    const RowRanges rr = row_ranges(tbl, num_segments, total_rows);
+    int kp = 0, pc = 0, nc = 0;
+    const int tiles = rr.mma_lo > 0 ? mma_tile_bound(total_rows, num_segments, rr.mma_lo) : 0;
+    if (rr.mma_lo == 1 && rr.mma_hi == kRowsInf && mma_splits(tbl, tiles, kp, pc, nc)) {
+      info->path = 2;
+      info->cluster = pc;
+      info->tile_rows = kMmaM;
+      info->row_splits = kp;
+      info->grid_ctas = tiles * (kp + nc);
+      info->smem_bytes = static_cast<int>(mma_part_smem(tbl->rank, tbl->h_in / kp / kMmaKC, pc));
+      return LSG_OK;
+    }
+  }
   info->path = pl.path;
   info->cluster = pl.path ? 1 : pl.cluster;
   info->tile_rows = pl.path ? 1 : pl.mt;

@@ -65,13 +65,22 @@ __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
 constexpr int kStreamCW = 8;          // consumer warps
 constexpr int kStreamThreads = 32 * (kStreamCW + 1);  // + 1 producer warp
 constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
-constexpr int kStreamSmem = 220 * 1024;
+#ifndef LSG_STREAM_SMEM
+#define LSG_STREAM_SMEM (220 * 1024)
+#endif
+#ifndef LSG_STREAM_KC16
+#define LSG_STREAM_KC16 1024
+#endif
+constexpr int kStreamSmem = LSG_STREAM_SMEM;
 
 // Stage geometry per rank: KC columns per stage (x / y_old rows move as one 1-D bulk copy
 // of KC * 2 bytes each -- >= 1 KiB pieces keep HBM streaming at full rate, 128-byte
 // tensor-box rows do not: scripts/tma_probe.cu), activation rows padded by 16 bytes so
 // ldmatrix is conflict-free, weights (A or B of the stage) first in the slot.
-__host__ __device__ constexpr int stream_kc(int R) { return R == 16 ? 1024 : 512; }
+__host__ __device__ constexpr int stream_kc(int R) { return R == 16 ? LSG_STREAM_KC16 : 512; }
+// rows of A's 128-byte view per stage, and per TMA box (<= 256)
+__host__ __device__ constexpr int stream_a_view_rows(int R) { return stream_kc(R) * R / 64; }
+__host__ __device__ constexpr int stream_a_box_rows(int R) { return stream_a_view_rows(R) < 256 ? stream_a_view_rows(R) : 256; }
 __host__ __device__ constexpr uint32_t stream_pitch(int R) { return stream_kc(R) * 2 + 16; }
 __host__ __device__ constexpr uint32_t stream_wbytes(int R) { return stream_kc(R) * R * 2; }
 __host__ __device__ constexpr uint32_t stream_slot_bytes(int R) {
@@ -168,9 +177,10 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       const uint32_t bytes = kWB + static_cast<uint32_t>(rows) * KC * 2;
       auto weights = [&](int i) {
         uint8_t* sb = smem + (i % S) * kSB;
-        if (i < nk) {  // A rows [i*KC, (i+1)*KC) = view rows [i*KC/KPR, ...), boxes of 256 view rows
-          for (int b = 0; b < KC / KPR / 256; ++b)
-            tma_load_2d(sb + b * 256 * 128, amap, 0, i * (KC / KPR) + b * 256, &full[i % S]);
+        if (i < nk) {  // A rows [i*KC, (i+1)*KC) = view rows [i*KC/KPR, ...), boxes of ABOX view rows
+          constexpr int ABOX = stream_a_box_rows(R);
+          for (int b = 0; b < KC / KPR / ABOX; ++b)
+            tma_load_2d(sb + b * ABOX * 128, amap, 0, i * (KC / KPR) + b * ABOX, &full[i % S]);
         } else {
           const int n0 = (i - nk) * KC;
           for (int b = 0; b < KC / 64; ++b) tma_load_2d(sb + b * (R * 128), bmap, n0 + b * 64, 0, &full[i % S]);
@@ -236,6 +246,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
         if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
       }
     }
+    fence_proxy_async_smem();  // this lane's ldmatrix reads before the slot's next bulk / TMA writes
     __syncwarp();
     if (lane == 0) mbar_arrive_local(&empty[s % S]);
   }

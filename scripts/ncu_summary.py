@@ -15,7 +15,10 @@ def main(rep, top=18):
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__cycles_active.avg",
             "sm__cycles_active.max", "gpc__cycles_elapsed.max", "launch__grid_size", "launch__cluster_dim_x",
             "launch__registers_per_thread", "smsp__warps_active.avg.pct_of_peak_sustained_active",
-            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum"]
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+            "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+            "launch__shared_mem_per_block_dynamic"]
     for k in keys:
         if k in m:
             print(f"{k:60s} {m[k][1]} {m[k][0]}")

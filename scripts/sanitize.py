@@ -11,6 +11,7 @@ the sanitizer but computes garbage still fails.  Families covered:
                      BGMV, grouped row) x tile rows 1 / 4 / 8, clusters 1..16, PDL on/off
   sgmv_tc_*          fused tensor-core kernel (rank 16), two-kernel form (rank 32 / split)
   sgmv_mma_*         segment-tile MMA pair (ranks 16 / 32 / 64, short and long segments)
+  sgmv_stream_kernel one-pass streaming kernel (ranks 16 / 32 / 64, partial tiles)
   dense_lora         tcgen05 GEMM with the LoRA epilogue
   build_segments     K6 builder, permute_rows gather / scatter
   sgmv_generic       odd shapes
@@ -116,7 +117,10 @@ def grouped_cases():
     bounds, _, _ = segments_for(UNIFORM, 12, 7)
     probs = [problem(512, 512, 16, bounds, 10 + i) for i in range(3)]
     ys = [torch.zeros(12, 512, dtype=torch.float16, device=dev) for _ in probs]
+    c = cap_cluster(probs[0][0], len(bounds) - 1, 12, 0)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c or 0)
     lsg.sgmv_multi(ys, [p[1] for p in probs], [p[0] for p in probs], probs[0][2], probs[0][3], 0)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, 0)
     for i, (p, y) in enumerate(zip(probs, ys)):
         check(f"grouped site {i}", y, p[4])
 
@@ -150,6 +154,21 @@ def mma_cases():
                 lsg.sgmv(y, x, pool, ss, sl, 0)
                 check(f"mma pair r{r} lens{lens} pdl{pdl}", y, ref)
     for opt in (lsg._lib.LSG_OPT_MMA_MIN_ROWS, lsg._lib.LSG_OPT_TC_LEGACY, lsg.LSG_OPT_PDL):
+        lsg.set_option(opt, 0)
+
+
+def stream_cases():
+    lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, 4)
+    for r in (16, 32, 64):
+        for lens in ((130, 3, 1), (1, 140, 16, 300)):
+            bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+            pool, x, ss, sl, ref = problem(1024, 2048, r, bounds, 60 + r)
+            for pdl in (0, 1):
+                lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+                y = torch.zeros(int(bounds[-1]), 2048, dtype=torch.float16, device=dev)
+                lsg.sgmv(y, x, pool, ss, sl, 0)
+                check(f"streaming kernel r{r} lens{lens} pdl{pdl}", y, ref)
+    for opt in (lsg._lib.LSG_OPT_TC_LEGACY, lsg.LSG_OPT_PDL):
         lsg.set_option(opt, 0)
 
 
@@ -205,7 +224,7 @@ def main():
     if sys.argv[1:2] == ["one"]:
         one_cases()
         sys.exit(1 if failures else 0)
-    which = sys.argv[1:] or ["fused", "grouped", "tc", "mma", "dense", "builder", "generic"]
+    which = sys.argv[1:] or ["fused", "grouped", "tc", "mma", "stream", "dense", "builder", "generic"]
     for w in which:
         globals()[f"{w}_cases"]()
     print(f"sanitize cases done: {len(failures)} numerical failures", flush=True)

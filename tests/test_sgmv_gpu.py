@@ -162,7 +162,8 @@ def test_baseline_shapes_match_oracle(lsg, dtype, shape, pop):
     x, A, B = random_problem(h_in, h_out, r, bounds, 77 + pop)
     p = Problem(lsg, x, A, B, bounds, dtype)
     y = p.run()
-    assert lsg.query_launch(p.pool, len(bounds) - 1, 64)["path"] == 0  # the fast (cluster) path
+    # the fast (cluster) path, or for rank 64 with shared adapters the segment-tile MMA pair
+    assert lsg.query_launch(p.pool, len(bounds) - 1, 64)["path"] == (2 if r == 64 and pop != DISTINCT else 0)
     err = row_norm_err(y.double().cpu().numpy(), p.reference())
     assert err <= tol(dtype), err
 
