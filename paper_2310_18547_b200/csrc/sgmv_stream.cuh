@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
         if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
       }
     }
-    fence_proxy_async_smem();  // this lane's ldmatrix reads before the slot's next bulk / TMA writes
+    // (every lane's ldmatrix reads of the slot have completed: the MMAs that consume them were
+    // issued before this point, and __syncwarp orders the warp before lane 0's release)
     __syncwarp();
     if (lane == 0) mbar_arrive_local(&empty[s % S]);
   }

@@ -92,8 +92,12 @@ def fused_cases():
                             check(f"fused r{r} pop{pop} c{c} mt{mt} row{row_mode} pdl{pdl}", y, ref)
                     v = torch.empty(batch, r, dtype=torch.float32, device=dev)
                     y = torch.zeros(batch, 256, dtype=torch.float16, device=dev)
+                    if c == 0 and any(lsg.query_launch(pool, len(bounds) - 1, batch, k)["cluster"] > MAX_C
+                                      for k in (lsg.KERNEL_SHRINK, lsg.KERNEL_EXPAND)):
+                        lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, MAX_C)
                     lsg.sgmv_shrink(v, x, pool, ss, sl, 0)
                     lsg.sgmv_expand(y, v, pool, ss, sl, 0)
+                    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, c)
                     check(f"two-launch r{r} pop{pop} c{c} mt{mt}", y, ref)
             for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg._lib.LSG_OPT_NO_ROW_MODE,
                         lsg.LSG_OPT_PDL):

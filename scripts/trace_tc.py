@@ -18,9 +18,11 @@ SHRINK = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "partials_in",
 EXPAND = ["entry", "weights_staged", "pdl_wait_done", "y_landed", "d2_ready", "end"]
 
 
-MMA_P = ["entry", "a_issued", "pdl_wait_done", "stage0_landed", "mma_done", "end"]
+MMA_P = ["entry", "a_issued", "pdl_wait_done", "stage0_landed", "mma_done", "end"] + [
+    f"stage{i}_landed" for i in range(10)]
+MMA_E = ["entry", "b_y_issued", "pdl_wait_done", "v_ready", "stage0_landed", "end"] + [
+    f"stage{i}_landed" for i in range(8)] + ["partials_landed"]
 STREAM = ["entry", "weights_issued", "pdl_wait_done", "stage0_landed", "v_ready", "end"]
-MMA_E = ["entry", "b_y_issued", "pdl_wait_done", "v_ready", "stage0_stored", "end"]
 FUSED = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "v_ready", "chunk0_ready", "chunk1_ready",
          "end"]
 
@@ -86,7 +88,7 @@ def main():
               if two else (("stream" if a.gen == 4 else "fused", STREAM if a.gen == 4 else FUSED,
                             allt[ctas:ctas + ctas // 2]),))
     for name, phases, part in groups:
-        tv = part[part[:, len(phases) - 1] != 0]
+        tv = part[part[:, min(len(phases), 6) - 1] != 0]
         if not tv.numel():
             print(f"{name}: no traced CTAs")
             continue
