@@ -301,7 +301,8 @@ typedef enum {
                                    segment sets it above the batch size for that step. */
   LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation: 0 (default) auto -- the one-pass
                                    streaming kernel (a CTA per 16-row tile) for calls of >= 1024 rows,
-                                   else the segment-tile MMA pair; A/B measurements: 1 the first fused
+                                   else the cluster-free tcgen05 pair (the segment-tile MMA pair where
+                                   that does not apply); A/B measurements: 1 the first fused
                                    cluster kernel (rank 16); 2 the streamed cluster kernel (ranks 16 / 32);
                                    3 the segment-tile MMA pair; 4 the streaming kernel; 5 the
                                    cluster-free tcgen05 partials + expand pair */

@@ -182,13 +182,15 @@ bool stream_shape_ok(const lsg_weight_table* t) {
 }
 // Long-segment kernel generation of a call (LSG_OPT_TC_LEGACY): 0 = auto -- the one-pass
 // streaming kernel (K9, sgmv_stream.cuh) for calls of >= 1024 rows (enough 16-row tiles to
-// fill the GPU), else the segment-tile MMA pair (K7); explicit 1 / 2 = the cluster kernels,
+// fill the GPU), else the cluster-free tcgen05 pair (sgmv_tc3.cuh; the MMA pair K7 where it
+// does not apply); explicit 1 / 2 = the cluster kernels,
 // 3 = the MMA pair, 4 = the streaming kernel, 5 = the cluster-free tcgen05 pair (sgmv_tc3.cuh).
 constexpr int kStreamMinRows = 1024;
 int tc_gen(const lsg_weight_table* t, int s_n) {
   const int g = cur().tc_legacy;
   if (g != 0) return g;
   if (s_n >= kStreamMinRows && stream_shape_ok(t)) return 4;
+  if (tc_nq(t) > 0 && t->h_out % kTcNT == 0) return 5;  // measured: c4-128 10.8 us vs 12.3 on K7
   if (mma_shape_ok(t)) return 3;
   return 5;
 }
@@ -976,6 +978,10 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   p.trace = g_trace;
   p.trace_ctas = g_trace_ctas;
   p.n_sites = n_sites > 1 ? n_sites : 0;
+  // behind the long / shared-segment kernels (K9, K7's expand and the tcgen05 pair's expand all
+  // trigger only after their own PDL wait) the short-segment kernel starts and computes while
+  // they run (disjoint rows), waiting for them only at the end
+  p.late_wait = (pl.tile_scan && (use_mma || (use_tc && (lp.stream9 || lp.tc3)))) ? 1 : 0;
   for (int i = 0; i < p.n_sites; ++i)
     p.sites[i] = SiteParams{sites[i].y, sites[i].x, sites[i].tbl->a_ptr, sites[i].tbl->b_ptr, sites[i].ldx,
                             sites[i].ldy};

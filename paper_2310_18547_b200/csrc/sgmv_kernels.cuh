@@ -91,6 +91,10 @@ struct FastParams {
   int32_t tile_scan;  // 1: cluster blockIdx.y = global tile index, mapped to (segment, tile) on device
   int32_t skip_long;  // >0: segments with at least this many rows belong to the tensor-core kernel
   int32_t n_sites;    // grouped launch: sites[0, n_sites) share the segment plan (kItemRowMulti)
+  int32_t late_wait;  // tile-scan launches behind a long-segment kernel that triggers only after its
+                      // own PDL wait: skip the wait before the activations (this launch's rows are
+                      // disjoint from that kernel's, and its predecessors have completed) and wait
+                      // at the end instead, so this grid's completion still implies the predecessor's
   SiteParams sites[kMaxSites];
 };
 
@@ -494,7 +498,11 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
     }
     // x, v and y may be produced by the preceding kernel: wait for it here
     // (returns at once after the first item).
-    pdl_wait();
+    if constexpr (ITEM == kItemTileScan) {
+      if (!p.late_wait) pdl_wait();
+    } else {
+      pdl_wait();
+    }
     LSG_TRACE(3);
 
     for (int t = first_tile; t < ntiles; t += tile_step, phase ^= 1u) {
@@ -747,7 +755,12 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
         else __syncthreads();
       }
     }
-    if (last_item || static_cast<int64_t>(item) + gridDim.y >= p.s_n) return;
+    if (last_item || static_cast<int64_t>(item) + gridDim.y >= p.s_n) {
+      if constexpr (ITEM == kItemTileScan) {
+        if (p.late_wait) pdl_wait();
+      }
+      return;
+    }
     first_item = false;
   }
 }

@@ -135,9 +135,9 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   uint64_t* empty = full + kStreamMaxStages;                 // [S]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nk = p.h_in / KC, nn = p.h_out / KC, nst = nk + nn;
-  // dependents (the short-segment kernel of this call, the next call) may start at once:
-  // every write of this kernel comes after its PDL wait
-  pdl_launch_dependents();
+  // Dependents are triggered only after this kernel's own PDL wait (every thread, below): the
+  // short-segment kernel of the same call then starts while this one runs and skips its own
+  // wait (late_wait), since its rows are disjoint and every kernel before this one is complete.
   if (threadIdx.x == 0) LSG_STREAM_TRACE(0);
 
   __shared__ int s_seg, s_tile;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
   if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {
     if (blockIdx.x == 0) pdl_wait();  // this grid's completion implies the predecessor's
-    return;
+    return;  // (an exited CTA counts as triggered)
   }
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
   const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       }
       LSG_STREAM_TRACE(1);
       pdl_wait();  // x and y_old may come from the preceding kernel
+      pdl_launch_dependents();
       LSG_STREAM_TRACE(2);
       for (int i = 0; i < pre; ++i) acts(i);
       for (int i = S; i < nst; ++i) {
@@ -213,12 +214,16 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
         weights(i);
         acts(i);
       }
+    } else {
+      pdl_wait();
+      pdl_launch_dependents();
     }
     return;
   }
 
   // ------------------------------------------------------------------------------ consumers
   pdl_wait();  // (returns at once by the time any y is written)
+  pdl_launch_dependents();
   const bool two = rows > 8;  // second n8 tile of the shrink (rows 8..15)
   const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;  // row-major 16 x 16 blocks
   const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;  // .trans blocks of [k][n] rows
