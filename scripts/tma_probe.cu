@@ -73,6 +73,49 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const __half* x, 
   out[blockIdx.x] = t1 - t0;
 }
 
+
+// K9-like stages: per stage, the tile's 16 activation rows (one 1-D bulk copy of KC*2 bytes each,
+// from a matrix larger than L2) plus 32 KB of weights from a small L2-resident matrix W, loaded as
+// wmode 0: none, 1: 16 x 1-D rows of 2 KB, 2: 16 x 2-D boxes (16 rows x 64 cols, SW128), 3: one 1-D 32 KB copy
+__global__ void probe2(const __grid_constant__ CUtensorMap wmap, const __half* x, const __half* w, int cols, int wmode,
+                       int depth, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int KC = 1024, RT = 16;
+  const uint32_t act = RT * KC * 2, wb = 32768, stage = act + wb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + depth * stage);
+  const int nst = cols / KC;
+  const int r0 = blockIdx.x * RT;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < depth; ++i) mb_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  auto issue = [&](int s) {
+    uint8_t* dst = smem + (s % depth) * stage;
+    uint64_t* b = &bars[s % depth];
+    mb_expect(b, act + (wmode ? wb : 0));
+    if (wmode == 1) {
+      for (int k = 0; k < 16; ++k) bulk(dst + act + k * 2048, w + k * 4096 + (s % 4) * KC, 2048, b);
+    } else if (wmode == 2) {
+      for (int q = 0; q < 16; ++q) tma2d(dst + act + q * 2048, &wmap, (s % 4) * KC + q * 64, 0, b);
+    } else if (wmode == 3) {
+      bulk(dst + act, w + (s % 4) * 16384, wb, b);
+    }
+    for (int m = 0; m < RT; ++m) bulk(dst + m * KC * 2, x + static_cast<int64_t>(r0 + m) * cols + s * KC, KC * 2, b);
+  };
+  for (int s = 0; s < depth && s < nst; ++s) issue(s);
+  for (int s = 0; s < nst; ++s) {
+    mb_wait(&bars[s % depth], (s / depth) & 1);
+    if (s + depth < nst) issue(s + depth);
+  }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  out[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   const int rows = 2048, cols = 4096, tiles = rows / 16;
   const size_t bytes = static_cast<size_t>(rows) * cols * 2;
@@ -127,6 +170,39 @@ int main() {
     const double us = ms * 1e3 / iters;
     printf("mode %d rows/CTA %2d piece %5d B depth %d ctas %4d: %7.2f us/launch %6.0f GB/s  per-CTA mean %.2f max %.2f us\n",
            c.mode, c.RT, c.KC * 2, c.depth, ctas, us, bytes / us / 1e3, sum / ctas / 1e3, mx / 1e3);
+  }
+  {  // K9-like stages
+    __half* w;
+    cudaMalloc(&w, 16 * 4096 * 2 * 4);
+    cudaMemset(w, 1, 16 * 4096 * 2 * 4);
+    CUtensorMap wmap;
+    cuuint64_t dims[2] = {4096, 16};
+    cuuint64_t str[1] = {4096 * 2};
+    cuuint32_t box[2] = {64, 16}, es[2] = {1, 1};
+    enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int depth = 3, smem = depth * (16 * 1024 * 2 + 32768) + 256, ctas = rows / 16;
+    cudaFuncSetAttribute(probe2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int wmode = 0; wmode < 4; ++wmode) {
+      for (int it = 0; it < 3; ++it) probe2<<<ctas, 32, smem>>>(wmap, xs[it], w, cols, wmode, depth, out);
+      cudaEventRecord(a);
+      const int iters = 32;
+      for (int it = 0; it < iters; ++it) probe2<<<ctas, 32, smem>>>(wmap, xs[it % nbuf], w, cols, wmode, depth, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      std::vector<unsigned long long> h(ctas);
+      cudaMemcpy(h.data(), out, ctas * 8, cudaMemcpyDeviceToHost);
+      double mx = 0, sum = 0;
+      for (auto v : h) {
+        mx = v > mx ? v : mx;
+        sum += v;
+      }
+      printf("K9-like stages (16 x 2 KB activation rows + 32 KB L2 weights as %s), depth 3: %.2f us/launch  per-CTA mean %.2f max %.2f us\n",
+             wmode == 0 ? "none" : wmode == 1 ? "16 x 1-D 2 KB rows" : wmode == 2 ? "16 x 2-D boxes (128-B rows)" : "one 1-D 32 KB copy",
+             ms * 1e3 / iters, sum / ctas / 1e3, mx / 1e3);
+    }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
