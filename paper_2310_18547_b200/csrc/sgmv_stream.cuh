@@ -34,6 +34,14 @@
 
 namespace lsg {
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 // 1-D bulk copy shared -> global (bulk async-group completion)
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
@@ -95,7 +103,10 @@ __host__ __device__ constexpr uint32_t stream_smem(int R, int stages) {
 
 struct StreamParams {
   CUtensorMap tmap_a;  // template: A of one layer viewed as [h_in * R / 64][64], box 64 x 256, SW128
-  CUtensorMap tmap_b;  // template: B of one layer [R, h_out], box 64 x R, SW128
+  CUtensorMap tmap_b;  // template: B of one layer as 3-D {64 columns, R rows, h_out / 64 column blocks}
+                       // (strides h_out * 2, 128 bytes), box 64 x R x KC/64, SW128: ONE copy per
+                       // stage lands the stage's [column block][R][64] layout (the per-stage copy
+                       // count, not the bytes, is what L2 weight traffic costs: tma_probe.cu)
   const void* x;
   void* y;
   int64_t ldx;
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
             tma_load_2d(sb + b * ABOX * 128, amap, 0, i * (KC / KPR) + b * ABOX, &full[i % S]);
         } else {
           const int n0 = (i - nk) * KC;
-          for (int b = 0; b < KC / 64; ++b) tma_load_2d(sb + b * (R * 128), bmap, n0 + b * 64, 0, &full[i % S]);
+          tma_load_3d(sb, bmap, 0, 0, n0 / 64, &full[i % S]);
         }
       };
       auto acts = [&](int i) {  // x (shrink) or y_old (expand): one bulk copy per row of the tile

@@ -30,6 +30,13 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
                "l"(src), "r"(bytes), "r"(su32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -77,7 +84,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const __half* x, 
 // K9-like stages: per stage, the tile's 16 activation rows (one 1-D bulk copy of KC*2 bytes each,
 // from a matrix larger than L2) plus 32 KB of weights from a small L2-resident matrix W, loaded as
 // wmode 0: none, 1: 16 x 1-D rows of 2 KB, 2: 16 x 2-D boxes (16 rows x 64 cols, SW128), 3: one 1-D 32 KB copy
-__global__ void probe2(const __grid_constant__ CUtensorMap wmap, const __half* x, const __half* w, int cols, int wmode,
+__global__ void probe2(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap wmap3, const __half* x, const __half* w, int cols, int wmode,
                        int depth, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KC = 1024, RT = 16;
@@ -103,6 +110,8 @@ __global__ void probe2(const __grid_constant__ CUtensorMap wmap, const __half* x
       for (int q = 0; q < 16; ++q) tma2d(dst + act + q * 2048, &wmap, (s % 4) * KC + q * 64, 0, b);
     } else if (wmode == 3) {
       bulk(dst + act, w + (s % 4) * 16384, wb, b);
+    } else if (wmode == 4) {  // one 3-D box: 16 column blocks x 16 rows x 64 columns
+      tma3d(dst + act, &wmap3, 0, 0, (s % 4) * 16, b);
     }
     for (int m = 0; m < RT; ++m) bulk(dst + m * KC * 2, x + static_cast<int64_t>(r0 + m) * cols + s * KC, KC * 2, b);
   };
@@ -182,12 +191,21 @@ int main() {
     enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int depth = 3, smem = depth * (16 * 1024 * 2 + 32768) + 256, ctas = rows / 16;
+    CUtensorMap wmap3;
+    {
+      cuuint64_t d3[3] = {64, 16, 4096 / 64};
+      cuuint64_t s3[2] = {4096 * 2, 128};
+      cuuint32_t b3[3] = {64, 16, 16}, e3[3] = {1, 1, 1};
+      CUresult r3 = enc(&wmap3, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, w, d3, s3, b3, e3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      printf("3-D weight map (strides 8192, 128 B): encode %s\n", r3 == CUDA_SUCCESS ? "ok" : "FAILED");
+    }
     cudaFuncSetAttribute(probe2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int wmode = 0; wmode < 4; ++wmode) {
-      for (int it = 0; it < 3; ++it) probe2<<<ctas, 32, smem>>>(wmap, xs[it], w, cols, wmode, depth, out);
+    for (int wmode = 0; wmode < 5; ++wmode) {
+      for (int it = 0; it < 3; ++it) probe2<<<ctas, 32, smem>>>(wmap, wmap3, xs[it], w, cols, wmode, depth, out);
       cudaEventRecord(a);
       const int iters = 32;
-      for (int it = 0; it < iters; ++it) probe2<<<ctas, 32, smem>>>(wmap, xs[it % nbuf], w, cols, wmode, depth, out);
+      for (int it = 0; it < iters; ++it) probe2<<<ctas, 32, smem>>>(wmap, wmap3, xs[it % nbuf], w, cols, wmode, depth, out);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms = 0;
@@ -200,7 +218,7 @@ int main() {
         sum += v;
       }
       printf("K9-like stages (16 x 2 KB activation rows + 32 KB L2 weights as %s), depth 3: %.2f us/launch  per-CTA mean %.2f max %.2f us\n",
-             wmode == 0 ? "none" : wmode == 1 ? "16 x 1-D 2 KB rows" : wmode == 2 ? "16 x 2-D boxes (128-B rows)" : "one 1-D 32 KB copy",
+             wmode == 0 ? "none" : wmode == 1 ? "16 x 1-D 2 KB rows" : wmode == 2 ? "16 x 2-D boxes (128-B rows)" : wmode == 3 ? "one 1-D 32 KB copy" : "one 3-D box",
              ms * 1e3 / iters, sum / ctas / 1e3, mx / 1e3);
     }
   }
