@@ -95,7 +95,7 @@ __host__ __device__ constexpr uint32_t stream_slot_bytes(int R) {
   return (stream_wbytes(R) + kMmaM * stream_pitch(R) + 1023u) & ~1023u;
 }
 __host__ __device__ constexpr uint32_t stream_fixed(int R) {
-  return 1024 + kStreamCW * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 + 16 * kStreamMaxStages;
+  return 1024 + kStreamCW * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 + 16 * kStreamMaxStages + 16;
 }
 __host__ __device__ constexpr uint32_t stream_smem(int R, int stages) {
   return stream_fixed(R) + stages * stream_slot_bytes(R);
@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   uint8_t* smap = vlo + kMmaM * R * 2;                       // 2 x 128 B
   uint64_t* full = reinterpret_cast<uint64_t*>(smap + 256);  // [S]
   uint64_t* empty = full + kStreamMaxStages;                 // [S]
+  uint64_t* bmap_ready = empty + kStreamMaxStages;           // warp 0 built the B descriptor
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nk = p.h_in / KC, nn = p.h_out / KC, nst = nk + nn;
   // Dependents are triggered only after this kernel's own PDL wait (every thread, below): the
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kStreamCW);
     }
+    mbar_init(bmap_ready, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -176,11 +178,25 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
   const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
 
-  if (warp == kStreamCW) {  // --------------------------------------------------------- producer
-    uint8_t* gmap = p.maps + static_cast<int64_t>(blockIdx.x) * 256;
-    make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
+  // Rank 16: A's stage rows are one contiguous 1-D copy (linear 32-byte rows: a 2-way ldmatrix
+  // conflict, no descriptor to build), so the producer streams weights from its first
+  // instruction; the B descriptor is built by warp 0 meanwhile, the activation rows are
+  // prefetched into L2 by warp 1 (hints only: safe while the preceding kernel runs).
+  constexpr bool kALin = R == 16;
+  uint8_t* gmap = p.maps + static_cast<int64_t>(blockIdx.x) * 256;
+  if (warp == 0) {
     make_slot_tmap(&p.tmap_b, smap + 128, gmap + 128, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
+    if (lane == 0) mbar_arrive_local(bmap_ready);
+  } else if (warp == 1) {
+    const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx;
+    const T* Y = static_cast<const T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
+    if (lane < rows) bulk_prefetch_l2(X + lane * p.ldx, static_cast<uint32_t>(p.h_in * 2));
+    else if (lane >= 16 && lane - 16 < rows) bulk_prefetch_l2(Y + (lane - 16) * p.ldy, static_cast<uint32_t>(p.h_out * 2));
+  }
+  if (warp == kStreamCW) {  // --------------------------------------------------------- producer
+    if constexpr (!kALin) make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
     if (lane == 0) {
+      const T* Ag = static_cast<const T*>(p.a_ptr[slot]) + p.a_off;
       const CUtensorMap* amap = reinterpret_cast<const CUtensorMap*>(gmap);
       const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap + 128);
       const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx;
@@ -188,12 +204,19 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       const uint32_t bytes = kWB + static_cast<uint32_t>(rows) * KC * 2;
       auto weights = [&](int i) {
         uint8_t* sb = smem + (i % S) * kSB;
-        if (i < nk) {  // A rows [i*KC, (i+1)*KC) = view rows [i*KC/KPR, ...), boxes of ABOX view rows
+        if (kALin && i < nk) {  // A rows [i*KC, (i+1)*KC): one contiguous copy
+          bulk_g2s(sb, Ag + static_cast<int64_t>(i) * KC * R, KC * R * 2, &full[i % S]);
+        } else if (i < nk) {  // A rows [i*KC, (i+1)*KC) = view rows [i*KC/KPR, ...), boxes of ABOX view rows
           constexpr int ABOX = stream_a_box_rows(R);
           for (int b = 0; b < KC / KPR / ABOX; ++b)
             tma_load_2d(sb + b * ABOX * 128, amap, 0, i * (KC / KPR) + b * ABOX, &full[i % S]);
         } else {
           const int n0 = (i - nk) * KC;
+          if (i == nk || i < S) {  // the descriptor warp 0 built: acquire it for the TMA proxy
+            mbar_wait(bmap_ready, 0);
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(bmap))
+                         : "memory");
+          }
           tma_load_3d(sb, bmap, 0, 0, n0 / 64, &full[i % S]);
         }
       };
@@ -207,12 +230,6 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       for (int i = 0; i < pre; ++i) {
         mbar_arrive_expect_tx(&full[i], bytes);
         weights(i);
-      }
-      // the tile's x and y_old rows into L2 now (hints only: safe while the preceding kernel
-      // runs), so the post-wait copies hit L2 instead of queueing in HBM
-      for (int m = 0; m < rows; ++m) {
-        bulk_prefetch_l2(X + m * p.ldx, static_cast<uint32_t>(p.h_in * 2));
-        bulk_prefetch_l2(Y + m * p.ldy, static_cast<uint32_t>(p.h_out * 2));
       }
       LSG_STREAM_TRACE(1);
       pdl_wait();  // x and y_old may come from the preceding kernel
@@ -255,9 +272,14 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       ldsm_x4(xs + xr * PITCH + (2 * kk + xc) * 16, b[0], b[1], b[2], b[3]);
 #pragma unroll
       for (int i = 0; i < MT; ++i) {  // A^T block (rank 16i.., k 16kk..) from the 128-byte view rows
-        const int k = 16 * kk + ak, c = (k % KPR) * (R / 8) + 2 * i + ac, vq = k / KPR;
         uint32_t a[4];
-        ldsm_x4_t(as + vq * 128 + ((c ^ (vq & 7)) << 4), a[0], a[1], a[2], a[3]);
+        if constexpr (kALin) {  // linear rows of R
+          const int k = 16 * kk + ak;
+          ldsm_x4_t(as + k * (R * 2) + (2 * i + ac) * 16, a[0], a[1], a[2], a[3]);
+        } else {
+          const int k = 16 * kk + ak, c = (k % KPR) * (R / 8) + 2 * i + ac, vq = k / KPR;
+          ldsm_x4_t(as + vq * 128 + ((c ^ (vq & 7)) << 4), a[0], a[1], a[2], a[3]);
+        }
         mma16816<T>(acc[i][0], a, b[0], b[1]);
         if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
       }

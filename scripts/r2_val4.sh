@@ -1,5 +1,5 @@
 #!/bin/bash
-cd $GRAFT_REPO_ROOT; o=gpurun_out/val10; mkdir -p $o
+cd $GRAFT_REPO_ROOT; o=gpurun_out/val11; mkdir -p $o
 timeout 900 python -m pytest tests/test_sgmv_gpu.py -q -m gpu -p no:cacheprovider -k "long or mma or generations or mixed or pdl" > $o/pytest.log 2>&1; tail -2 $o/pytest.log; grep FAILED $o/pytest.log | head
 B="python bench.py --no-extras --no-e2e --no-cpu-baseline --no-traffic --steps 20 --warmup 3"
 for c in "--preset c4" "--preset c3"; do
