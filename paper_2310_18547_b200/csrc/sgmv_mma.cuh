@@ -266,10 +266,10 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
                      static_cast<uint32_t>(KS * 2));
   }
   LSG_TC_TRACE(0, 1);
-  // The expand may start now (once every partials CTA is resident): it builds its weight
-  // descriptor and streams B before its own wait; y_old only after it.
-  pdl_launch_dependents();
   pdl_wait();  // x may come from the preceding kernel
+  // The expand may start now: every kernel before this one has completed, so it may stage
+  // y_old (as well as B) before its own wait, which then covers only these partials.
+  pdl_launch_dependents();
   LSG_TC_TRACE(0, 2);
   if (tid == 0)
     for (int s = 0; s < nst; ++s) tma_load_2d(smem + s * kSB, &p.tmap_x, k0 + s * kMmaKC, r0, &full[s]);
@@ -411,22 +411,24 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
   T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy + n0;
   uint8_t* gmap = p.maps_e + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 128;
   const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap);
-  // B of every stage before the PDL wait (weights are never written by a kernel)
+  // B and y_old of every stage before the PDL wait (weights are never written by a kernel;
+  // y_old is final: the partials kernel triggered this launch only after its own wait)
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_arrive_expect_tx(&full[s], kSB);
+      tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &full[s]);
+    }
+  }
   if (warp == 0) {
     make_slot_tmap(&p.tmap_b, smap, gmap, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
-    if (lane == 0) {
-      for (int s = 0; s < nst; ++s) {
-        mbar_arrive_expect_tx(&full[s], kSB);
-        tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &full[s]);
-      }
-    }
+    if (lane == 0)
+      for (int s = 0; s < nst; ++s) tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &full[s]);
   }
   LSG_TC_TRACE(1, 1);
   pdl_wait();  // the partials (and, through the partials kernel's own wait, y_old)
   pdl_launch_dependents();
   LSG_TC_TRACE(1, 2);
-  if (tid == 0) {  // y_old of every stage, then the tile's partials (one bulk copy each, barrier nst)
-    for (int s = 0; s < nst; ++s) tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &full[s]);
+  if (tid == 0) {  // the tile's partials (one bulk copy each, barrier nst)
     const float* src = p.ws + static_cast<int64_t>(blockIdx.y) * nparts * kMmaM * R;
     mbar_arrive_expect_tx(&full[nst], static_cast<uint32_t>(nparts) * kPB);
     for (int q = 0; q < nparts; ++q) bulk_g2s(part + q * kMmaM * R, src + q * kMmaM * R, kPB, &full[nst]);
