@@ -18,7 +18,7 @@ static int launch_mma_inst(const MmaParams& p, int tiles, cudaStream_t st) {
     mark_configured(configured);
   }
   cudaError_t e = launch_ex(kp, dim3(static_cast<unsigned>(p.kparts), static_cast<unsigned>(tiles), 1),
-                            dim3(kMmaThreads), static_cast<int>(mma_part_smem(R, p.h_in / p.kparts / kMmaKC, p.pc)),
+                            dim3(32 * kMmaPW), static_cast<int>(mma_part_smem(R, p.h_in / p.kparts / kMmaKC, p.pc)),
                             p.pc > 1 ? p.pc : 0, st, &p);
   if (e != cudaSuccess) return cuda_fail(e, "sgmv_mma_part_kernel launch");
   e = launch_ex(ke, dim3(static_cast<unsigned>(p.ncol), static_cast<unsigned>(tiles), 1), dim3(kMmaThreads),

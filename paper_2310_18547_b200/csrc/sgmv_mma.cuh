@@ -49,7 +49,11 @@
 namespace lsg {
 
 constexpr int kMmaM = 16;         // rows per tile (one m16 block)
-constexpr int kMmaThreads = 128;  // 4 warps
+constexpr int kMmaThreads = 128;  // 4 warps (expand)
+#ifndef LSG_MMA_PART_WARPS
+#define LSG_MMA_PART_WARPS 4
+#endif
+constexpr int kMmaPW = LSG_MMA_PART_WARPS;  // partials kernel warps (stages split over them)
 constexpr int kMmaKC = 64;        // columns per stage (4 k16-steps)
 constexpr int kMmaMaxStagesDecl = 32;  // stages per CTA (all resident; barriers reserved for this many)
 
@@ -188,10 +192,10 @@ __device__ __forceinline__ void mma_tile_of(const int32_t* seg_starts, int n_seg
 __host__ __device__ constexpr uint32_t mma_part_stage_bytes(int R) { return kMmaM * kMmaKC * 2 + kMmaKC * R * 2; }
 __host__ __device__ constexpr uint32_t mma_exp_stage_bytes(int R) { return R * kMmaKC * 2 + kMmaM * kMmaKC * 2; }
 constexpr int kMmaMaxPc = 8;  // partials cluster size (portable)
-// partials: [stages][x 2 KB | A 128R B], warp partials 4 x 16 x R fp32, the cluster leader's
+// partials: [stages][x 2 KB | A 128R B], warp partials kMmaPW x 16 x R fp32, the cluster leader's
 // receive buffer pc x 16 x R fp32, map, barriers
 __host__ __device__ constexpr uint32_t mma_part_smem(int R, int stages, int pc = kMmaMaxPc) {
-  return 1024 + stages * mma_part_stage_bytes(R) + (4 + pc) * kMmaM * R * 4 + 128 + 8 * (kMmaMaxStagesDecl + 2);
+  return 1024 + stages * mma_part_stage_bytes(R) + (kMmaPW + pc) * kMmaM * R * 4 + 128 + 8 * (kMmaMaxStagesDecl + 2);
 }
 // expand: [stages][B 128R B | y 2 KB], the tile's partials kparts x 16 x R fp32, v hi / lo
 // (16 x R 16-bit each), map, barriers
@@ -201,7 +205,7 @@ __host__ __device__ constexpr uint32_t mma_exp_smem(int R, int stages, int kpart
 }
 
 template <typename T, int R>
-__global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid_constant__ MmaParams p) {
+__global__ void __launch_bounds__(32 * kMmaPW) sgmv_mma_part_kernel(const __grid_constant__ MmaParams p) {
   static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
   constexpr int ROWB = R * 2;                    // bytes per A row (= its TMA swizzle span)
   constexpr uint32_t kXB = kMmaM * kMmaKC * 2;   // x stage bytes
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
   const int KS = p.h_in / p.kparts, nst = KS / kMmaKC;  // nst <= kMmaMaxStages (host)
   const int C = p.pc;
   float* red = reinterpret_cast<float*>(smem + nst * kSB);   // [4][16][R]
-  float* recv = red + 4 * kMmaM * R;                         // [C][16][R] (cluster leader)
+  float* recv = red + kMmaPW * kMmaM * R;                    // [C][16][R] (cluster leader)
   uint8_t* smap = reinterpret_cast<uint8_t*>(recv + C * kMmaM * R);  // 128 B
   uint64_t* full = reinterpret_cast<uint64_t*>(smap + 128);  // [nst] stage landed, [nst] partials in
   LSG_TC_TRACE(0, 0);
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
   const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;
   const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;
   // warp w: stages w, w + 4, ... (all four k16-steps of each), no block barrier
-  for (int s = warp; s < nst; s += 4) {
+  for (int s = warp; s < nst; s += kMmaPW) {
     mbar_wait(&full[s], 0);
     if (s == 0) LSG_TC_TRACE(0, 3);
     const uint32_t xs = smem_u32(smem + s * kSB), as = xs + kXB;
@@ -333,10 +337,10 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
   float* dst = p.ws + (static_cast<int64_t>(blockIdx.y) * nparts + ks / C) * kMmaM * R;
   if (C > 1 && crank == 0 && tid == 0) mbar_arrive_expect_tx(&full[nst], static_cast<uint32_t>((C - 1) * kMmaM * R * 4));
   if (C > 1) cluster_wait();  // the leader's barrier is initialised
-  for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
+  for (int i = tid * 4; i < kMmaM * R; i += 32 * kMmaPW * 4) {
     float4 s4 = *reinterpret_cast<const float4*>(red + i);
 #pragma unroll
-    for (int w = 1; w < 4; ++w) {
+    for (int w = 1; w < kMmaPW; ++w) {
       const float4 o = *reinterpret_cast<const float4*>(red + w * kMmaM * R + i);
       s4.x += o.x, s4.y += o.y, s4.z += o.z, s4.w += o.w;
     }
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_part_kernel(const __grid
   if (C > 1 && crank == 0) {
     mbar_wait(&full[nst], 0);
     __syncthreads();  // the leader's own partial
-    for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
+    for (int i = tid * 4; i < kMmaM * R; i += 32 * kMmaPW * 4) {
       float4 s4 = *reinterpret_cast<const float4*>(recv + i);
       for (int c = 1; c < C; ++c) {
         const float4 o = *reinterpret_cast<const float4*>(recv + c * kMmaM * R + i);
