@@ -80,3 +80,24 @@ def test_reference_acceptance_with_b200_dropin():
     for i in (1, 2, 3):
         assert any(ln.startswith(f"PASS  {i}.") for ln in lines), r.stdout + r.stderr
     assert r.returncode == 0 and "all 8 criteria passed" in r.stdout, r.stdout + r.stderr
+
+
+def test_reference_simulator_with_b200_costs_cpu():
+    """the reference's own compare / calibration / cluster-replay experiments run with
+    the B200-fitted SGMV cost model (integration/sim_b200.cpp over the reference simulator built in
+    place); both passes complete and the multi-adapter advantage survives on B200 (Distinct ratio
+    well above 1, Identical = 1)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "sim_b200")
+    proj = "/root/reference/proj"
+    if not (os.path.exists(exe) and os.path.isdir(proj)):
+        pytest.skip("needs the reference tree and oracle/_ref/sim_b200 (built by __graft_entry__.build())")
+    out = subprocess.run([exe, proj, os.path.join(ROOT, "profiles", "round1", "b200_cost_params.json")],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = out.stdout.splitlines()
+    for label in ("A100", "B200"):
+        rows = [l for l in lines if l.strip().startswith(("distinct", "identical"))]
+        assert any(label in l for l in lines), label
+        assert len(rows) == 4, rows
+    b200 = lines[[i for i, l in enumerate(lines) if l.startswith("B200") and "compare_modes" in l][0] + 1]
+    assert float(b200.split("ratio")[1]) > 5.0, b200
