@@ -1,11 +1,6 @@
 #!/bin/bash
-cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/sync
-CS="/usr/local/cuda/bin/compute-sanitizer --kernel-name kns=sgmv --print-limit 4"
-i=0
-for args in "8 1 9 0 0 0 0" "8 1 9 2 0 0 0" "8 1 9 4 0 0 0" "8 1 9 16 0 0 0" "8 1 9 16 0 1 0" "8 3 9 16 0 0 0" "8 0 4 16 0 0 0" "16 1 9 0 0 0 0" "8 1 9 16 1 0 0" "8 1 9 16 8 0 0"; do
-  i=$((i+1))
-  echo "== one $args" > gpurun_out/sync/$i.log
-  timeout 300 $CS --tool synccheck python scripts/sanitize.py one $args >> gpurun_out/sync/$i.log 2>&1
-  timeout 300 $CS --tool memcheck python scripts/sanitize.py one $args >> gpurun_out/sync/$i.log 2>&1
-done
-
+# synccheck over every kernel family with clusters capped at 8 (profiles/round2/sanitizer.md)
+cd $GRAFT_REPO_ROOT; o=${OUT:-gpurun_out/sync}; mkdir -p $o
+F="--kernel-name kns=sgmv --kernel-name kns=dense --kernel-name kns=build_segments --kernel-name kns=permute"
+SAN_MAX_CLUSTER=8 timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool synccheck $F --print-limit 100 python scripts/sanitize.py > $o/san_synccheck.log 2>&1
+echo "synccheck rc=$?"; grep -E "ERROR SUMMARY|cases done" $o/san_synccheck.log

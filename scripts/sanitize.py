@@ -181,7 +181,10 @@ def dense_cases():
     pool, x, ss, sl, ref = problem(1024, 512, 16, bounds, 30)
     w = (torch.rand(1024, 512, device=dev) * 0.1 - 0.05).half()
     y = torch.empty(16, 512, dtype=torch.float16, device=dev)
+    if MAX_C < 16:  # its shrink launch (synccheck: clusters <= 8)
+        lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, MAX_C)
     lsg.dense_lora(y, x, w, pool, ss, sl, 0)
+    lsg.set_option(lsg.LSG_OPT_FORCE_CLUSTER, 0)
     check("dense_lora", y, x.double().cpu().numpy() @ w.double().cpu().numpy() + ref)
 
 
