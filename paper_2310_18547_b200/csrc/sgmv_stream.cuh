@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       for (int i = 0; i < pre; ++i) acts(i);
       for (int i = S; i < nst; ++i) {
         mbar_wait(&empty[i % S], ((i / S) - 1) & 1);
+        if (i == 3) LSG_STREAM_TRACE(14);
+        if (i == 5) LSG_STREAM_TRACE(15);
         mbar_arrive_expect_tx(&full[i % S], bytes);
         weights(i);
         acts(i);
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   for (int s = 0; s < nk; ++s) {  // ---- shrink: k16-steps [w * KPW, (w+1) * KPW) of every stage
     mbar_wait(&full[s % S], (s / S) & 1);
     if (s == 0 && tid == 0) LSG_STREAM_TRACE(3);
+    if (s < 8 && tid == 0) LSG_STREAM_TRACE(6 + s);
     const uint32_t as = smem_u32(smem + (s % S) * kSB), xs = as + kWB;
 #pragma unroll 4
     for (int q = 0; q < KPW; ++q) {
@@ -343,6 +346,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   for (int j = 0; j < nn; ++j) {  // ---- expand: boxes [w * BPW, (w+1) * BPW) of every stage
     const int s = nk + j;
     mbar_wait(&full[s % S], (s / S) & 1);
+    if (s < 8 && tid == 0) LSG_STREAM_TRACE(6 + s);
     uint8_t* bs = smem + (s % S) * kSB;
     uint8_t* ys = bs + kWB;
 #pragma unroll

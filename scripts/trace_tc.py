@@ -22,7 +22,8 @@ MMA_P = ["entry", "a_issued", "pdl_wait_done", "stage0_landed", "mma_done", "end
     f"stage{i}_landed" for i in range(10)]
 MMA_E = ["entry", "b_y_issued", "pdl_wait_done", "v_ready", "stage0_landed", "end"] + [
     f"stage{i}_landed" for i in range(8)] + ["partials_landed"]
-STREAM = ["entry", "weights_issued", "pdl_wait_done", "stage0_landed", "v_ready", "end"]
+STREAM = ["entry", "weights_issued", "pdl_wait_done", "stage0_landed", "v_ready", "end"] + [
+    f"stage{i}_landed" for i in range(8)] + ["stage3_issued", "stage5_issued"]
 FUSED = ["entry", "weights_staged", "pdl_wait_done", "d1_ready", "v_ready", "chunk0_ready", "chunk1_ready",
          "end"]
 
