@@ -15,4 +15,5 @@ for f in $root/paper_2310_18547_b200/csrc/*.cu; do
 done
 for p in ${pids[@]}; do wait $p; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libsgmv_b200.so $out/*.o
+rm -f $out/*.o  # only the library travels to the GPU box
 echo built $out/libsgmv_b200.so

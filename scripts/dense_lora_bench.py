@@ -41,8 +41,18 @@ def main():
         for l in range(L):
             torch.mm(xs[l], Ws[l], out=ys[l])
 
+    def gemm_kmajor():  # the same GEMM on W stored [h_out, h_in] (nn.Linear layout), for reference
+        for l in range(L):
+            torch.mm(xs[l], Ws[l].t(), out=ys[l])
+
+    if "--profile" in sys.argv:  # ncu: a few plain launches of each variant, no graph
+        for fn in (fused, unfused, gemm_only):
+            fn()
+        torch.cuda.synchronize()
+        return
     out = {}
-    for name, fn in (("fused_us", fused), ("unfused_us", unfused), ("cublas_gemm_only_us", gemm_only)):
+    for name, fn in (("fused_us", fused), ("unfused_us", unfused), ("cublas_gemm_only_us", gemm_only),
+                     ("cublas_gemm_w_kmajor_us", gemm_kmajor)):
         with torch.cuda.stream(st):
             fn()
         torch.cuda.synchronize()

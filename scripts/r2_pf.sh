@@ -1,0 +1,7 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; o=gpurun_out/pf; mkdir -p $o
+timeout 600 python -m pytest tests/test_sgmv_gpu.py -q -m gpu -p no:cacheprovider -k "prefetch" > $o/pytest.log 2>&1; tail -2 $o/pytest.log
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-traffic > $o/bench.json 2> $o/bench.err; tail -3 $o/bench.err
+python -c "
+import json; d=json.loads(open('$o/bench.json').read().strip().splitlines()[-1])
+print(json.dumps(d.get('decode_step'), indent=1))"

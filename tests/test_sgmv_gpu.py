@@ -7,6 +7,7 @@ test_experiments.cpp) plus the kernel-level invariants the B200 design adds
 from __future__ import annotations
 
 import json
+import sys
 import os
 
 import numpy as np
@@ -563,11 +564,14 @@ def test_rank64_multirow_tiles_bitwise_one_row(lsg, dtype, pop):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("pop,batch", [(DISTINCT, 64), (UNIFORM, 37), (IDENTICAL, 8)])
-def test_dense_lora_matches_oracle_dense_projection(lsg, dtype, pop, batch):
-    """lsg_dense_lora = dense_projection (sgmv.cpp:143-155): x.W + lora_addon, LoRA in the
-    GEMM epilogue; checked against the fp64 oracle and against cuBLAS + the SGMV kernel."""
-    h_in, h_out, r = 4096, 2048, 16
+@pytest.mark.parametrize("pop,batch,h_in,h_out", [(DISTINCT, 64, 4096, 2048), (UNIFORM, 37, 4096, 2048),
+                                                   (IDENTICAL, 8, 4096, 2048), (DISTINCT, 64, 1024, 4096),
+                                                   (SKEWED, 50, 640, 8192), (UNIFORM, 21, 256, 11008)])
+def test_dense_lora_matches_oracle_dense_projection(lsg, dtype, pop, batch, h_in, h_out):
+    """lsg_dense_lora = dense_projection (sgmv.cpp:143-155): x.W + lora_addon, the LoRA expand
+    folded into the GEMM's tensor-core accumulation; checked against the fp64 oracle and
+    against cuBLAS + the SGMV kernel.  The shapes cover K splits (clusters) of 8, 4, 2 and 1."""
+    r = 16
     bounds, _, _ = segments_for(pop, batch, 44)
     x, A, B = random_problem(h_in, h_out, r, bounds, 45)
     W = oracle().rng(46).fill_pm1(h_in * h_out).reshape(h_in, h_out) * 0.05
@@ -583,6 +587,30 @@ def test_dense_lora_matches_oracle_dense_projection(lsg, dtype, pop, batch):
     lsg.sgmv(y2, p.x, p.pool, p.seg_starts, p.seg_slot, 1)
     torch.cuda.synchronize()
     assert row_norm_err(y.double().cpu().numpy(), y2.double().cpu().numpy()) <= 2 * tol(dtype)
+    y3 = torch.full_like(y, float("nan"))  # deterministic: a second call is bit-identical
+    lsg.dense_lora(y3, p.x, Wq, p.pool, p.seg_starts, p.seg_slot, 1)
+    assert torch.equal(y3, y)
+
+
+def test_dense_lora_no_adapter_and_empty_segments(lsg):
+    """Segments without an adapter (slot -1, slot >= num_slots) and empty segments add nothing."""
+    dtype, h_in, h_out, r = torch.float16, 2048, 4096, 16
+    bounds = np.array([0, 5, 5, 9, 20, 20, 33, 40], dtype=np.uint64)
+    slots = [0, 1, -1, 2, 3, 7, 4]
+    x, A, B = random_problem(h_in, h_out, r, bounds, 47)
+    p = Problem(lsg, x, A, B, bounds, dtype, slots=[s if s < 5 else -1 for s in slots], num_slots=5)
+    p.seg_slot = torch.tensor(slots, dtype=torch.int32, device="cuda")
+    W = oracle().rng(48).fill_pm1(h_in * h_out).reshape(h_in, h_out) * 0.05
+    Wq = torch.tensor(W, dtype=torch.float64).to(dtype).cuda()
+    y = torch.full((40, h_out), float("nan"), dtype=dtype, device="cuda")
+    lsg.dense_lora(y, p.x, Wq, p.pool, p.seg_starts, p.seg_slot, 0)
+    torch.cuda.synchronize()
+    ref = p.xd @ Wq.double().cpu().numpy()
+    for s, slot in enumerate(slots):  # lora_addon (sgmv.cpp:112-121) restated for the empty / adapter-less segments
+        lo, hi = int(bounds[s]), int(bounds[s + 1])
+        if 0 <= slot < 5 and hi > lo:
+            ref[lo:hi] += p.xd[lo:hi] @ p.Ad[s] @ p.Bd[s]
+    assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(dtype)
 
 
 def test_dense_lora_rejects_unsupported(lsg):
@@ -960,3 +988,21 @@ def test_mma_pair_many_tiles_and_workspace_bound(lsg):
     p = Problem(lsg, x, A, B, bounds, torch.bfloat16)
     y = p.run()
     assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
+
+
+def test_prefetch_is_only_a_hint(lsg):
+    """lsg_sgmv_prefetch on a side stream concurrently with the launch it feeds: same results, bad
+    arguments rejected, slot -1 and empty calls are no-ops."""
+    bounds, _, _ = segments_for(DISTINCT, 64, 60)
+    x, A, B = random_problem(4096, 4096, 16, bounds, 61)
+    p = Problem(lsg, x, A, B, bounds, torch.float16, layers=2, layer=1)
+    base = p.run()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        lsg.sgmv_prefetch(p.pool, p.seg_slot, 1)
+    assert torch.equal(p.run(), base)
+    lsg.sgmv_prefetch(p.pool, torch.tensor([-1, 3], dtype=torch.int32, device="cuda"), 0)
+    lsg.sgmv_prefetch(p.pool, p.seg_slot, 0, num_segments=0)
+    with pytest.raises(lsg._lib.LsgError):
+        lsg.sgmv_prefetch(p.pool, p.seg_slot, 5)
+    torch.cuda.synchronize()
