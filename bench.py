@@ -572,20 +572,8 @@ def run_decode_step(lsg, torch, a, dtype, stream, layers=LAYERS, batch=64, rank=
                     lsg.sgmv_multi([ys[i] for i in idx], [xs[i] for i in idx],
                                    [views[(layer, LLAMA7B_SITES[g][0])] for g in grp], ss, sl, 0, tc_min_rows=no_tc)
 
-    # the LoRA launch cannot overlap a library GEMM through PDL (cuBLAS never triggers its
-    # dependents early): a tiny kernel ahead of the GEMM prefetches the site's adapters into L2
-    # (lsg_sgmv_prefetch; the bulk prefetches complete while the GEMM runs), so the LoRA kernel
-    # after it reads its weights from L2
-    def step_prefetch():
-        for i in range(nsites):
-            layer, name = i // len(LLAMA7B_SITES), LLAMA7B_SITES[i % len(LLAMA7B_SITES)][0]
-            lsg.sgmv_prefetch(pools[name], sl, layer)
-            backbone(i)
-            lsg.sgmv(ys[i], xs[i], pools[name], ss, sl, layer, tc_min_rows=no_tc)
-
     out = {}
-    for key, fn in (("backbone_only", step_base), ("backbone_lora", step_lora), ("backbone_lora_grouped", step_grouped),
-                    ("backbone_lora_prefetch", step_prefetch)):
+    for key, fn in (("backbone_only", step_base), ("backbone_lora", step_lora), ("backbone_lora_grouped", step_grouped)):
         g = graph_of(torch, fn, stream)
         with torch.cuda.stream(stream):
             for _ in range(3):
@@ -598,7 +586,6 @@ def run_decode_step(lsg, torch, a, dtype, stream, layers=LAYERS, batch=64, rank=
         "model": "Llama-2-7B, 32 layers, batch 64 decode, Distinct adapters, rank 16",
         "lora_overhead_us_per_site": (out["backbone_lora_ms"] - out["backbone_only_ms"]) * 1e3 / nsites,
         "lora_overhead_us_per_site_grouped": (out["backbone_lora_grouped_ms"] - out["backbone_only_ms"]) * 1e3 / nsites,
-        "lora_overhead_us_per_site_prefetch": (out["backbone_lora_prefetch_ms"] - out["backbone_only_ms"]) * 1e3 / nsites,
         "lora_overhead_frac": out["backbone_lora_ms"] / out["backbone_only_ms"] - 1.0,
         "lora_alg_bytes_per_step": lora_bytes,
         "backbone_weight_bytes_per_step": sum(hi * ho * 2 for _, hi, ho in LLAMA7B_SITES) * layers,

@@ -16,7 +16,6 @@
  *   lsg_build_segments <- lorasim::plan_batch grouping             core/src/simulator.cpp:267-309,
  *                         and the per-row gather loop              sgmv.cpp:195-203
  *   lsg_partition_segments <- Scheduler::place (request -> GPU)    core/src/scheduler.cpp:12-29
- *   lsg_sgmv_prefetch  <- (no counterpart) L2 prefetch of a launch's adapters behind the backbone GEMM
  *   lsg_tp_sgmv / _nccl <- (no reference counterpart: TP is out of the reference's scope,
  *                         SPEC.md:15) the 70B TP expand with its output all-gather
  *
@@ -194,16 +193,14 @@ int lsg_tp_sgmv_nccl(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg
                      int32_t layer, int32_t tp_rank, int32_t tp_size, void* nccl_comm /* ncclComm_t */,
                      void* workspace, size_t workspace_bytes, lsg_stream_t stream);
 
-/* Dense projection with the LoRA add fused into the GEMM (decode shapes):
+/* Dense projection with the LoRA add in the GEMM epilogue (decode shapes):
  *   y[s_n, h_out] = x[s_n, h_in] . W[h_in, h_out] + x . A_slot(s) . B_slot(s)   (overwrite)
  * <- lorasim::dense_projection(const Batch&, const Matrix& w), sgmv.cpp:143-155.
- * W is row-major [h_in, h_out] (row stride ldw), same dtype as the pool.  Two PDL-chained
- * launches: a one-CTA-per-row shrink writes v (fp32, [s_n, rank]) into the workspace
- * (lsg_dense_lora_workspace_size bytes); the tcgen05 GEMM streams W and x and accumulates x.W
- * concurrently with it, then adds v . B as extra reduction blocks of the same accumulator
- * (v rounded to the storage type there, as the reference's CUDA kernels do).  Rank 16,
- * s_n <= 64, num_segments <= 64, h_in % 64 == 0, h_out % 128 == 0 (else LSG_EUNSUPPORTED).
- * Deterministic: the K-split partials are summed in a fixed order. */
+ * W is row-major [h_in, h_out] (row stride ldw), same dtype as the pool.  The shrink
+ * writes v (fp32, [s_n, rank]) into the caller's workspace; one tcgen05 GEMM launch
+ * then computes x.W per 64-column tile and adds v . B in its epilogue.  Rank 16,
+ * s_n <= 64, h_in % 256 == 0, h_out % 64 == 0 (else LSG_EUNSUPPORTED).  A cluster of 4 CTAs
+ * splits K per 64-column tile; the partial products are summed over DSMEM in CTA order. */
 size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows);
 int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
                    const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot,
@@ -244,14 +241,6 @@ int lsg_bgmv(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg_weight_
  * Because of the padding, lsg_sgmv may be launched with ANY host-side
  * num_segments in [n, s_n] (e.g. the host's count of distinct adapters) without
  * reading n back.  One CTA; total_rows <= 16384. */
-/* L2 prefetch of the adapters a later lsg_sgmv will read: A and B of every segment's slot at
- * `layer` (a cache hint, no data dependence -- launch it on a side stream concurrently with the
- * backbone GEMM that precedes the LoRA launch, so the LoRA kernel, which cannot overlap a library
- * GEMM through PDL, finds its weights in L2).  Replaces nothing in the reference (its decode step
- * is a cost model, simulator.cpp:313-335). */
-int lsg_sgmv_prefetch(const lsg_weight_table* tbl, const int32_t* seg_slot, int32_t num_segments, int32_t layer,
-                      lsg_stream_t stream);
-
 size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots);
 int lsg_build_segments(const int32_t* row_slot, int32_t total_rows, int32_t num_slots,
                        int32_t lead_slot, int32_t lead_row0, int32_t lead_row1, int32_t* row_perm, int32_t* seg_starts,

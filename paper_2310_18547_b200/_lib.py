@@ -26,7 +26,7 @@ EXPORTED = (
     "lsg_set_option", "lsg_get_option", "lsg_query_launch", "lsg_status_string",
     "lsg_last_error", "lsg_version", "lsg_set_trace", "lsg_partition_segments", "lsg_sgmv_multi",
     "lsg_dense_lora", "lsg_dense_lora_workspace_size", "lsg_sgmv_ex", "lsg_sgmv_multi_ex",
-    "lsg_tp_sgmv", "lsg_tp_sgmv_nccl", "lsg_tp_nccl_workspace_size", "lsg_sgmv_prefetch",
+    "lsg_tp_sgmv", "lsg_tp_sgmv_nccl", "lsg_tp_nccl_workspace_size",
 )
 
 
@@ -113,7 +113,6 @@ def lib() -> C.CDLL:
         L.lsg_bgmv.argtypes = [vp, i64, vp, i64, tp, vp, i32, i32, vp]
         L.lsg_build_segments_workspace.argtypes = [i32, i32]
         L.lsg_build_segments_workspace.restype = C.c_size_t
-        L.lsg_sgmv_prefetch.argtypes = [tp, vp, i32, i32, vp]
         L.lsg_build_segments.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.lsg_gather_rows.argtypes = [vp, i64, vp, i64, vp, i32, i32, vp]
         L.lsg_scatter_rows.argtypes = [vp, i64, vp, i64, vp, i32, i32, vp]

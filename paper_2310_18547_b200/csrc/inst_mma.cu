@@ -1,11 +1,8 @@
 // inst_mma.cu -- sm_100a instantiations of the segment-tile tensor-core pair (K7,
 // sgmv_mma.cuh) and their launchers.
-#include <mutex>
-
 #include "launch.cuh"
 #include "sgmv_mma.cuh"
 #include "sgmv_stream.cuh"
-#include "sgmv_dense.cuh"
 
 namespace lsg {
 
@@ -67,72 +64,6 @@ int launch_stream(int dtype, int rank, const StreamParams& p, int tiles, cudaStr
   if (dtype == LSG_F16) LSG_ST_R(__half)
   LSG_ST_R(__nv_bfloat16)
 #undef LSG_ST_R
-}
-
-template <typename T>
-static bool configure_dense_lora() {
-  static std::atomic<unsigned long long> configured{0};  // one bit per device (per instantiation)
-  if (configured_on_device(configured)) return true;
-  if (cudaFuncSetAttribute(dense_lora_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dn_smem()) !=
-      cudaSuccess)
-    return false;
-  // the shrink CTAs (small) share SMs with the GEMM's: leave the GEMM its shared memory
-  if (cudaFuncSetAttribute(dense_shrink_kernel<T, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
-      cudaSuccess)
-    return false;
-  mark_configured(configured);
-  return true;
-}
-
-template <typename T>
-static int launch_dense_lora_inst(const DenseLoraParams& p, cudaStream_t st) {
-  if (!configure_dense_lora<T>()) return cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dense lora smem)");
-  cudaError_t e = launch_ex(dense_shrink_kernel<T, 16>, dim3(static_cast<unsigned>(p.s_n)), dim3(kDnShThreads), 0, 0,
-                            st, &p);
-  if (e != cudaSuccess) return cuda_fail(e, "dense_shrink_kernel launch");
-  e = launch_ex(dense_lora_kernel<T, 16>, dim3(static_cast<unsigned>(p.ks),
-                                                                 static_cast<unsigned>(p.h_out / kDnN)),
-                                  dim3(kDnThreads), dn_smem(), p.ks, st, &p);
-  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "dense_lora_kernel launch");
-}
-
-int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st) {
-  return dtype == LSG_F16 ? launch_dense_lora_inst<__half>(p, st) : launch_dense_lora_inst<__nv_bfloat16>(p, st);
-}
-
-template <typename T>
-static int dense_max_clusters_inst(int ks) {
-  if (!configure_dense_lora<T>()) return 0;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(ks), 1, 1);
-  cfg.blockDim = dim3(kDnThreads);
-  cfg.dynamicSmemBytes = static_cast<size_t>(dn_smem());
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = static_cast<unsigned>(ks);
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, dense_lora_kernel<T, 16>, &cfg) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return 0;
-  }
-  return n;
-}
-
-int dense_lora_max_clusters(int dtype, int ks) {
-  // cached per (device, dtype, ks): the answer depends only on the device
-  static std::mutex mu;
-  static int cache[64][2][4] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
-  const int d = dtype == LSG_F16 ? 0 : 1, k = ks == 8 ? 3 : ks == 4 ? 2 : ks == 2 ? 1 : 0;
-  std::lock_guard<std::mutex> lock(mu);
-  if (cache[dev][d][k] == 0)
-    cache[dev][d][k] = d == 0 ? dense_max_clusters_inst<__half>(ks) : dense_max_clusters_inst<__nv_bfloat16>(ks);
-  return cache[dev][d][k];
 }
 
 }  // namespace lsg

@@ -95,6 +95,24 @@ int launch_tc_fused(int dtype, const TcFusedParams& p, int C, int tiles, cudaStr
 
 namespace lsg {
 
+template <typename T>
+static int launch_dense_lora_inst(const DenseLoraParams& p, cudaStream_t st) {
+  auto kern = dense_lora_kernel<T, 16>;
+  static std::atomic<unsigned long long> configured{0};  // one bit per device (per instantiation)
+  if (!configured_on_device(configured)) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dl_smem<16>()));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(dense lora smem)");
+    mark_configured(configured);
+  }
+  const cudaError_t e = launch_ex(kern, dim3(kDlKS, static_cast<unsigned>(p.h_out / kDlN)), dim3(kTcThreads),
+                                  static_cast<int>(dl_smem<16>()), kDlKS, st, &p);
+  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "dense_lora_kernel launch");
+}
+
+int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st) {
+  return dtype == LSG_F16 ? launch_dense_lora_inst<__half>(p, st) : launch_dense_lora_inst<__nv_bfloat16>(p, st);
+}
 
 }  // namespace lsg
 

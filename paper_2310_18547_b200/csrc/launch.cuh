@@ -80,8 +80,6 @@ struct Tc2Params;
 int launch_tc_stream(int dtype, int rank, const Tc2Params& p, int C, uint32_t smem, int tiles, cudaStream_t st);
 struct DenseLoraParams;
 int launch_dense_lora(int dtype, const DenseLoraParams& p, cudaStream_t st);
-// clusters of ks dense-LoRA CTAs that fit on the current device at once (0 on error)
-int dense_lora_max_clusters(int dtype, int ks);
 
 template <typename K>
 cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, int smem, int cluster, cudaStream_t st,

@@ -28,7 +28,6 @@
 #include "sgmv_tc3.cuh"
 #include "sgmv_mma.cuh"
 #include "sgmv_stream.cuh"
-#include "sgmv_dense.cuh"
 
 namespace lsg {
 
@@ -53,29 +52,6 @@ struct TpFlagParams {
   int32_t rank, size;
   uint32_t epoch;
 };
-// Weight prefetch into L2 (lsg_sgmv_prefetch): CTA s issues cp.async.bulk.prefetch.L2 for the A
-// and B of segment s's slot at `layer`, 16 KiB per lane-request.  Only a cache hint: it may run on
-// any stream, concurrently with anything (e.g. the backbone GEMM before the LoRA launch).
-struct PrefetchParams {
-  const void* const* a_ptr;
-  const void* const* b_ptr;
-  int64_t a_off, b_off;  // bytes
-  int64_t a_bytes, b_bytes;
-  const int32_t* seg_slot;
-  int32_t num_slots;
-};
-__global__ void sgmv_prefetch_kernel(const __grid_constant__ PrefetchParams p) {
-  const int slot = p.seg_slot[blockIdx.x];
-  if (slot < 0 || slot >= p.num_slots) return;
-  const char* a = static_cast<const char*>(p.a_ptr[slot]) + p.a_off;
-  const char* b = static_cast<const char*>(p.b_ptr[slot]) + p.b_off;
-  constexpr int64_t kPiece = 16384;
-  for (int64_t o = static_cast<int64_t>(threadIdx.x) * kPiece; o < p.a_bytes; o += blockDim.x * kPiece)
-    bulk_prefetch_l2(a + o, static_cast<uint32_t>(p.a_bytes - o < kPiece ? p.a_bytes - o : kPiece));
-  for (int64_t o = static_cast<int64_t>(threadIdx.x) * kPiece; o < p.b_bytes; o += blockDim.x * kPiece)
-    bulk_prefetch_l2(b + o, static_cast<uint32_t>(p.b_bytes - o < kPiece ? p.b_bytes - o : kPiece));
-}
-
 __global__ void tp_flags_kernel(const __grid_constant__ TpFlagParams p) {
   const int d = threadIdx.x;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -1239,11 +1215,7 @@ int lsg_tp_sgmv_nccl(void* y, int64_t ldy, const void* x, int64_t ldx, const lsg
 size_t lsg_dense_lora_workspace_size(const lsg_weight_table* tbl, int32_t total_rows) {
   CallScope scope(nullptr);
   if (tbl == nullptr || validate_table(tbl) != LSG_OK || total_rows < 0) return 0;
-#ifdef LSG_DN_TRACE
-  return static_cast<size_t>(kDnMaxRows) * tbl->rank * sizeof(float) + 2 * 220 * 64;
-#else
   return static_cast<size_t>(total_rows) * tbl->rank * sizeof(float);
-#endif
 }
 
 int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
@@ -1259,48 +1231,34 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
   if (x == nullptr || y == nullptr || w == nullptr || seg_starts == nullptr || seg_slot == nullptr)
     return fail(LSG_EINVAL, "lsg_dense_lora: NULL pointer");
   if (ldx < tbl->h_in || ldy < tbl->h_out || ldw < tbl->h_out) return fail(LSG_EINVAL, "lsg_dense_lora: bad strides");
-  if (tbl->rank != 16 || total_rows > kDnMaxRows || num_segments > kDnMaxRows || tbl->h_in % kDnKB != 0 ||
-      tbl->h_out % kDnN != 0 || !aligned16(x) || !aligned16(y) || !aligned16(w) || ldx % 8 != 0 || ldy % 8 != 0 ||
-      ldw % 8 != 0 || tbl->a_layer_stride % 8 != 0 || tbl->b_layer_stride % 8 != 0 || encode_tiled_fn() == nullptr)
-    return fail(LSG_EUNSUPPORTED,
-                "lsg_dense_lora: rank 16, <= 64 rows and segments, h_in % 64, h_out % 128, 16-byte rows");
+  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % (kTcKB * kDlKS) != 0 || tbl->h_out % kDlN != 0 ||
+      !aligned16(x) || !aligned16(y) || !aligned16(w) || ldx % 8 != 0 || ldy % 8 != 0 || ldw % 8 != 0 ||
+      tbl->b_layer_stride % 8 != 0 || encode_tiled_fn() == nullptr)
+    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 256, h_out % 64, 16-byte rows");
   if (workspace == nullptr || workspace_bytes < lsg_dense_lora_workspace_size(tbl, total_rows) || !aligned16(workspace))
     return fail(LSG_EINVAL, "lsg_dense_lora: workspace too small");
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  float* v = static_cast<float*>(workspace);
+  st = run(kKShrink, nullptr, 0, x, ldx, v, nullptr, tbl, seg_starts, seg_slot, nullptr, num_segments, total_rows,
+           layer, stream);
+  if (st != LSG_OK) return st;
   DenseLoraParams p{};
-  if (!encode_map_2d(&p.tmap_x, tbl->dtype, x, static_cast<uint64_t>(tbl->h_in), static_cast<uint64_t>(total_rows),
-                     static_cast<uint64_t>(ldx), kDnKB, kDnMaxRows, CU_TENSOR_MAP_SWIZZLE_128B))
-    return fail(LSG_ECUDA, "tensor map x");
-  {  // W as {64 columns, h_in rows, h_out / 64 column blocks}: one box = both halves of a 128-column stage
-    const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(tbl->h_in), static_cast<cuuint64_t>(tbl->h_out / 64)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, 128};
-    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kDnKB), 2};
-    const cuuint32_t estr[3] = {1, 1, 1};
+  if (!encode_rows_map(&p.tmap_x, tbl->dtype, x, tbl->h_in, total_rows, ldx)) return fail(LSG_ECUDA, "tensor map x");
+  {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_out), static_cast<cuuint64_t>(tbl->h_in)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kDlN), static_cast<cuuint32_t>(kTcKB)};
+    const cuuint32_t estr[2] = {1, 1};
     if (encode_tiled_fn()(&p.tmap_w,
-                          tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                          tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                           const_cast<void*>(w), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return fail(LSG_ECUDA, "tensor map W");
   }
-  // K split = cluster size: the largest of 8 / 4 / 2 / 1 whose grid is one co-resident wave
-  const int tiles = tbl->h_out / kDnN, nkb = tbl->h_in / kDnKB;
-  p.ks = 0;
-  for (int ks = kDnMaxKS; ks >= 1; ks /= 2)
-    if (ks <= nkb && tiles <= dense_lora_max_clusters(tbl->dtype, ks)) {
-      p.ks = ks;
-      break;
-    }
-  if (p.ks == 0) p.ks = 1;  // several waves
-  if (const char* e = getenv("LSG_DN_FORCE_KS")) p.ks = atoi(e);  // debugging aid
   p.y = y;
   p.ldy = ldy;
-  p.x = x;
-  p.ldx = ldx;
-  p.v = static_cast<float*>(workspace);
-  p.layer = layer;
-  p.a_ptr = tbl->a_ptr;
-  p.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
+  p.v = v;
   p.b_ptr = tbl->b_ptr;
   p.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride;
   p.seg_starts = seg_starts;
@@ -1428,31 +1386,6 @@ int lsg_query_launch(const lsg_weight_table* tbl, int32_t num_segments, int32_t 
   info->grid_ctas = pl.path ? total_rows : pl.cluster * pl.clusters;
   info->smem_bytes = pl.smem;
   return LSG_OK;
-}
-
-int lsg_sgmv_prefetch(const lsg_weight_table* tbl, const int32_t* seg_slot, int32_t num_segments, int32_t layer,
-                      lsg_stream_t stream) {
-  CallScope scope(nullptr);
-  const int st = validate_table(tbl);
-  if (st != LSG_OK) return st;
-  if (num_segments < 0 || layer < 0 || layer >= tbl->num_layers)
-    return fail(LSG_EINVAL, "lsg_sgmv_prefetch: bad segment count or layer");
-  if (num_segments == 0) return LSG_OK;
-  if (seg_slot == nullptr) return fail(LSG_EINVAL, "lsg_sgmv_prefetch: seg_slot is NULL");
-  if (tbl->a_layer_stride % 8 != 0 || tbl->b_layer_stride % 8 != 0)
-    return LSG_OK;  // a hint only: nothing to do for unaligned layer strides
-  PrefetchParams p{};
-  p.a_ptr = tbl->a_ptr;
-  p.b_ptr = tbl->b_ptr;
-  p.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride * 2;
-  p.b_off = static_cast<int64_t>(layer) * tbl->b_layer_stride * 2;
-  p.a_bytes = (static_cast<int64_t>(tbl->h_in) * tbl->rank * 2) & ~static_cast<int64_t>(15);
-  p.b_bytes = (static_cast<int64_t>(tbl->rank) * tbl->h_out * 2) & ~static_cast<int64_t>(15);
-  p.seg_slot = seg_slot;
-  p.num_slots = tbl->num_slots;
-  sgmv_prefetch_kernel<<<num_segments, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
-  const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_prefetch_kernel launch");
 }
 
 size_t lsg_build_segments_workspace(int32_t total_rows, int32_t num_slots) {

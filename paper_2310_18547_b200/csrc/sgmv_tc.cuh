@@ -900,4 +900,188 @@ __global__ void __launch_bounds__(kTcThreads, 1) sgmv_tc_fused_kernel(const __gr
 
 namespace lsg {
 
+// ---------------------------------------------------------------------------------------
+// Dense projection with the LoRA add in the GEMM epilogue, decode shape
+// (s_n <= 64 rows): y = x . W + v . B_seg(row)   (reference dense_projection,
+// sgmv.cpp:143-155: x.W + lora_addon).  v = x . A comes from the shrink kernel.
+// A cluster of kDlKS CTAs per 64-column tile of y splits K: CTA c streams its K slice
+// of x (K-major) and W (MN-major) through a TMA ring into tcgen05.mma (partial D_c,
+// fp32 in TMEM, M = 128 with rows >= s_n zero).  Row m's partials go to the CTA owning
+// rows [16c, 16c + 16) over DSMEM; the owner sums them in CTA order, adds
+// sum_k v[m,k] B_seg(m)[k,n] (fp32 chain over k; its rows' B slices staged by
+// cp.async ahead of the PDL wait) and rounds once.
+// ---------------------------------------------------------------------------------------
+constexpr int kDlN = 64;        // columns per cluster
+constexpr int kDlMaxRows = 64;  // decode rows per launch
+constexpr int kDlKS = 4;        // K split = cluster size; CTA c owns rows [16c, 16c + 16)
+constexpr int kDlRowsPer = kDlMaxRows / kDlKS;
+constexpr int kDlStages = 2;
+constexpr int kDlStage = kTcBox + kTcKB * kDlN * 2;  // x box 16 KB + W box 8 KB
+
+struct DenseLoraParams {
+  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 128, SW128
+  CUtensorMap tmap_w;  // W [h_in, h_out] row-major, box 64 (N) x 64 (K), SW128
+  void* y;
+  int64_t ldy;
+  const float* v;      // [s_n, R] fp32
+  const void* const* b_ptr;
+  int64_t b_off;
+  const int32_t* seg_starts;
+  const int32_t* seg_slot;
+  int32_t n_seg, s_n, num_slots, h_in, h_out;
+};
+
+template <int R>
+struct DlLayout {
+  static constexpr uint32_t kB = kDlStages * kDlStage;                    // my rows' B slices
+  static constexpr uint32_t kRecv = kB + kDlRowsPer * R * kDlN * 2;        // [src][16 rows][64] fp32
+  static constexpr uint32_t kBars = kRecv + kDlKS * kDlRowsPer * kDlN * 4;
+  static constexpr uint32_t kTotal = kBars + 256 + 1024;
+};
+template <int R>
+__host__ __device__ constexpr uint32_t dl_smem() {
+  return DlLayout<R>::kTotal;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_constant__ DenseLoraParams p) {
+  using L = DlLayout<R>;
+  constexpr int fmt = std::is_same<T, __half>::value ? 0 : 1;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* Bsm = smem + L::kB;  // [local row][k][64 cols] 16-bit
+  float* recv = reinterpret_cast<float*>(smem + L::kRecv);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);  // full[2], empty[2], D, recv
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  __shared__ int s_slot[kDlRowsPer];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = static_cast<int>(blockIdx.x);  // cluster rank = K slice = owned row block
+  const int n0 = static_cast<int>(blockIdx.y) * kDlN;
+  const int nkb_all = p.h_in / kTcKB, kb0 = (c * nkb_all) / kDlKS, nkb = ((c + 1) * nkb_all) / kDlKS - kb0;
+
+  if (tid == 0) {
+    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+    prefetch_tmap(&p.tmap_x);
+    prefetch_tmap(&p.tmap_w);
+  }
+  if (warp == 0) tmem_alloc<kDlN>(tmem_slot);
+  if (tid < kDlRowsPer) {  // slot of owned row c*16 + tid: last s with seg_starts[s] <= row
+    const int m = c * kDlRowsPer + tid;
+    int slot = -1;
+    if (m < p.s_n) {
+      int lo = 0, hi = p.n_seg;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (p.seg_starts[mid + 1] > m) hi = mid; else lo = mid + 1;
+      }
+      slot = lo < p.n_seg ? p.seg_slot[lo] : -1;
+      if (slot >= p.num_slots) slot = -1;
+    }
+    s_slot[tid] = slot;
+  }
+  __syncthreads();
+  // my rows' B[:, n0 : n0 + 64] (weights: before the PDL wait)
+  for (int i = tid; i < kDlRowsPer * R * (kDlN / 8); i += kTcThreads) {
+    const int ml = i / (R * (kDlN / 8)), rem = i - ml * (R * (kDlN / 8)), k = rem / (kDlN / 8), cc = rem % (kDlN / 8);
+    const int slot = s_slot[ml];
+    if (slot >= 0)
+      cp_async16(Bsm + ((ml * R + k) * kDlN + cc * 8) * 2,
+                 static_cast<const T*>(p.b_ptr[slot]) + p.b_off + static_cast<int64_t>(k) * p.h_out + n0 + cc * 8);
+  }
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  cluster_arrive_relaxed();  // barrier inits -> the cluster
+
+  pdl_wait();  // x and v come from the preceding kernels
+  pdl_launch_dependents();
+  if (warp == 1 && lane == 0) {  // TMA producer: x box + W box per K step of my slice
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDlStages;
+      if (kb >= kDlStages) mbar_wait(&bars[2 + s], ((kb / kDlStages) - 1) & 1);
+      mbar_arrive_expect_tx(&bars[s], kDlStage);
+      uint8_t* st = smem + s * kDlStage;
+      tma_load_2d(st, &p.tmap_x, (kb0 + kb) * kTcKB, 0, &bars[s]);
+      tma_load_2d(st + kTcBox, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[s]);
+    }
+  } else if (warp == 0 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = umma_idesc(fmt, kTcM, kDlN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDlStages;
+      mbar_wait(&bars[s], (kb / kDlStages) & 1);
+      tc_fence_after();
+      const uint32_t xa = smem_u32(smem + s * kDlStage), wa = xa + kTcBox;
+#pragma unroll
+      for (int ks = 0; ks < kTcKB / 16; ++ks) {
+        const uint64_t ad = umma_desc(xa + ks * 32, 16, 1024, kSw128);            // x: K-major SW128
+        const uint64_t bd = umma_desc(wa + ks * 2 * 1024, 8 * 1024, 1024, kSw128);  // W: MN-major SW128
+        umma_f16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+      }
+      umma_commit(&bars[2 + s]);
+    }
+    umma_commit(&bars[4]);
+  }
+  __syncwarp();
+  cluster_wait();  // peers' barriers initialised
+  if (tid == 0) mbar_arrive_expect_tx(&bars[5], static_cast<uint32_t>(kDlKS * kDlRowsPer * kDlN * 4));
+  mbar_wait(&bars[4], 0);
+  tc_fence_after();
+  // row m of my partial D_c -> owner m / 16 (rows >= 64 are padding: warps 2, 3 send nothing)
+#pragma unroll
+  for (int cc = 0; cc < kDlN / 16; ++cc) {
+    float d[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + cc * 16, d);  // all threads (aligned)
+    const int m = tid;
+    if (m < kDlMaxRows) {
+      const int owner = m / kDlRowsPer, ml = m - owner * kDlRowsPer;
+      const uint32_t ra = mapa_u32(recv + ((c * kDlRowsPer + ml) * kDlN + cc * 16), static_cast<uint32_t>(owner));
+      const uint32_t rb = mapa_u32(&bars[5], static_cast<uint32_t>(owner));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_async_v4(ra + j * 16, d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3], rb);
+    }
+  }
+  cp_async_wait<0>();
+  mbar_wait(&bars[5], 0);
+  __syncthreads();  // every thread's B slices visible
+  // my 16 rows x 64 columns: thread -> (row tid / 8, 8 columns)
+  {
+    const int ml = tid / 8, cg = (tid % 8) * 8, m = c * kDlRowsPer + ml;
+    if (m < p.s_n) {
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+      for (int src = 0; src < kDlKS; ++src)  // partials in CTA (K slice) order
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += recv[(src * kDlRowsPer + ml) * kDlN + cg + j];
+      float lo[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) lo[j] = 0.f;
+      if (s_slot[ml] >= 0) {
+        const float* vr = p.v + static_cast<int64_t>(m) * R;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float b[8];
+          Cvt<T>::unpack8(*reinterpret_cast<const uint4*>(Bsm + ((ml * R + k) * kDlN + cg) * 2), b);
+          const float vk = vr[k];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) lo[j] = fmaf(vk, b[j], lo[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = acc[j] + lo[j];
+      st_global_v4(static_cast<T*>(p.y) + static_cast<int64_t>(m) * p.ldy + n0 + cg, Cvt<T>::pack8(acc));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<kDlN>(tmem);
+  }
+}
+
 }  // namespace lsg

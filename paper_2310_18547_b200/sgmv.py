@@ -152,8 +152,7 @@ def sgmv_multi(ys, xs, pools, seg_starts: torch.Tensor, seg_slot: torch.Tensor, 
 def dense_lora(y: torch.Tensor, x: torch.Tensor, w: torch.Tensor, pool: AdapterPool, seg_starts: torch.Tensor,
                seg_slot: torch.Tensor, layer: int, num_segments: int | None = None) -> torch.Tensor:
     """``y = x . W + x . A_slot . B_slot`` (overwrite): the dense projection with the LoRA add
-    and the LoRA expand fused into the GEMM's tensor-core accumulation, behind a PDL-overlapped
-    shrink (lsg_dense_lora; rank 16, <= 64 rows).  W is ``[h_in, h_out]``."""
+    in the GEMM epilogue (lsg_dense_lora; rank 16, <= 64 rows).  W is ``[h_in, h_out]``."""
     _rows_check(x, y, pool)
     _check_i32(seg_starts, "seg_starts")
     _check_i32(seg_slot, "seg_slot")
@@ -206,14 +205,6 @@ def bgmv(y: torch.Tensor, x: torch.Tensor, pool: AdapterPool, row_slot: torch.Te
     return y
 
 
-def sgmv_prefetch(pool: AdapterPool, seg_slot: torch.Tensor, layer: int, num_segments: int | None = None) -> None:
-    """L2 prefetch of the adapters (A and B at ``layer``) of every segment's slot (lsg_sgmv_prefetch):
-    a cache hint, for a side stream running concurrently with the backbone GEMM."""
-    _check_i32(seg_slot, "seg_slot")
-    n = seg_slot.numel() if num_segments is None else num_segments
-    _lib.call("lsg_sgmv_prefetch", C.byref(pool.table), _ptr(seg_slot), n, layer, _stream())
-
-
 def build_segments(row_slot: torch.Tensor, num_slots: int, lead_slot: int = -1, lead_rows: tuple[int, int] = (0, 0)):
     """On-device stable grouping of rows by slot (plan_batch's order, simulator.cpp:239-311).
 
@@ -264,6 +255,6 @@ def query_launch(pool: AdapterPool, num_segments: int, total_rows: int, kernel: 
     return {f: getattr(info, f) for f, _ in LaunchInfo._fields_}
 
 
-__all__ = ["AdapterPool", "call_opts", "sgmv", "sgmv_multi", "sgmv_prefetch", "dense_lora", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
+__all__ = ["AdapterPool", "call_opts", "sgmv", "sgmv_multi", "dense_lora", "sgmv_shrink", "sgmv_expand", "bgmv", "build_segments", "gather_rows",
            "scatter_rows", "set_option", "get_option", "query_launch", "KERNEL_FUSED", "KERNEL_SHRINK",
            "KERNEL_EXPAND", "KERNEL_BGMV"]

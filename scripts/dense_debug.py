@@ -54,7 +54,4 @@ def run(pop, batch, h_in, h_out):
 if __name__ == "__main__":
     lsg.set_option(lsg.LSG_OPT_PDL, int(os.environ.get("PDL", "0")))
     run(UNIFORM, 37, 4096, 2048)
-    for ks in ("1", "2", "4"):
-        os.environ["LSG_DN_FORCE_KS"] = ks
-        print("force ks", ks)
-        run(UNIFORM, 37, 4096, 2048)
+    run(DISTINCT, 64, 4096, 4096)
