@@ -95,6 +95,7 @@ def parse(argv=None):
     ap.add_argument("--no-row-mode", action="store_true", help="segment-major decode for one-row tiles")
     ap.add_argument("--tc-gen", type=int, default=0, help="LSG_OPT_TC_LEGACY (long-segment kernel generation)")
     ap.add_argument("--mma-min-rows", type=int, default=0, help="LSG_OPT_MMA_MIN_ROWS (0 = auto)")
+    ap.add_argument("--mma-fused", type=int, default=0, help="LSG_OPT_MMA_FUSED: 0 / 1 the two-launch pair, 2 one launch")
     ap.add_argument("--tc-min-rows", type=int, default=0,
                     help="per-call tensor-core row threshold (0 = from the step's own segment plan)")
     ap.add_argument("--kernel", choices=["sgmv", "bgmv"], default="sgmv",
@@ -735,6 +736,7 @@ def main():
     lsg.set_option(lsg._lib.LSG_OPT_TC_SPLIT, int(a.tc_split))
     lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, a.tc_gen)
     lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, a.mma_min_rows)
+    lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, a.mma_fused)
     lsg.set_option(lsg._lib.LSG_OPT_NO_ROW_MODE, int(a.no_row_mode))
     h, r, sites = a.hidden, a.rank, a.sites
     # Request partitioning: the partitioner (lsg_partition_segments) hands every rank whole

@@ -306,10 +306,14 @@ typedef enum {
                                    cluster kernel (rank 16); 2 the streamed cluster kernel (ranks 16 / 32);
                                    3 the segment-tile MMA pair; 4 the streaming kernel; 5 the
                                    cluster-free tcgen05 partials + expand pair */
-  LSG_OPT_MMA_MIN_ROWS = 11     /* segments with at least this many rows (and below the long-segment
+  LSG_OPT_MMA_MIN_ROWS = 11,    /* segments with at least this many rows (and below the long-segment
                                    threshold) take the segment-tile MMA pair; 0 (default) = auto: rank 64
                                    calls whose rows share adapters (total_rows > num_segments) send every
                                    segment to it, other ranks keep the CUDA-core kernel */
+  LSG_OPT_MMA_FUSED = 12        /* the segment-tile MMA path as ONE launch (one cluster per tile: shrink,
+                                   DSMEM exchange of the partials, expand): 0 (default) and 1 the
+                                   two-launch pair (faster on B200 at every measured shape), 2 the
+                                   one-launch form whenever a split fits */
 } lsg_option;
 int lsg_set_option(int32_t option, int32_t value);
 int lsg_get_option(int32_t option);

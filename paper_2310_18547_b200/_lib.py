@@ -16,7 +16,7 @@ LSG_OK, LSG_EINVAL, LSG_EUNSUPPORTED, LSG_ECUDA, LSG_ENODEVICE = 0, -1, -2, -3, 
 LSG_F16, LSG_BF16 = 0, 1
 (LSG_OPT_PDL, LSG_OPT_FORCE_CLUSTER, LSG_OPT_FORCE_GENERIC, LSG_OPT_FORCE_TILE_ROWS, LSG_OPT_NO_L2_STAGING,
  LSG_OPT_NO_TENSOR_CORES, LSG_OPT_TC_SPLIT, LSG_OPT_NO_ROW_MODE, LSG_OPT_NO_MULTIROW_TILES,
- LSG_OPT_TC_MIN_ROWS, LSG_OPT_TC_LEGACY, LSG_OPT_MMA_MIN_ROWS) = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11
+ LSG_OPT_TC_MIN_ROWS, LSG_OPT_TC_LEGACY, LSG_OPT_MMA_MIN_ROWS, LSG_OPT_MMA_FUSED) = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12
 KERNEL_FUSED, KERNEL_SHRINK, KERNEL_EXPAND, KERNEL_BGMV = 0, 1, 2, 3
 
 # Every symbol include/lsg_sgmv.h declares (checked by tests/test_abi.py).

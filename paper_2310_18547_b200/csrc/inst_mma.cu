@@ -10,12 +10,20 @@ template <typename T, int R>
 static int launch_mma_inst(const MmaParams& p, int tiles, cudaStream_t st) {
   auto kp = sgmv_mma_part_kernel<T, R>;
   auto ke = sgmv_mma_exp_kernel<T, R>;
+  auto kf = sgmv_mma_fused_kernel<T, R>;
   static std::atomic<unsigned long long> configured{0};  // one bit per device
   if (!configured_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma pair smem)");
     mark_configured(configured);
+  }
+  if (p.fused) {  // one launch: a cluster of pc CTAs per tile
+    const int nst = (p.h_in > p.h_out ? p.h_in : p.h_out) / p.pc / kMmaKC;
+    const cudaError_t e = launch_ex(kf, dim3(static_cast<unsigned>(p.pc), static_cast<unsigned>(tiles), 1),
+                                    dim3(kMmaThreads), static_cast<int>(mma_fused_smem(R, nst, p.pc)), p.pc, st, &p);
+    return e == cudaSuccess ? LSG_OK : cuda_fail(e, "sgmv_mma_fused_kernel launch");
   }
   cudaError_t e = launch_ex(kp, dim3(static_cast<unsigned>(p.kparts), static_cast<unsigned>(tiles), 1),
                             dim3(32 * kMmaPW), static_cast<int>(mma_part_smem(R, p.h_in / p.kparts / kMmaKC, p.pc)),

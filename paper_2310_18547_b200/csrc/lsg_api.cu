@@ -87,6 +87,7 @@ std::atomic<int> g_opt_no_rank64_tiles{0};
 std::atomic<int> g_opt_tc_min_rows{0};  // rows from which a segment takes the tensor-core path (0 = default)
 std::atomic<int> g_opt_tc_legacy{0};    // long-segment kernel generation (LSG_OPT_TC_LEGACY)
 std::atomic<int> g_opt_mma_min_rows{0};  // rows from which a segment takes the segment-tile MMA pair (0 = auto)
+std::atomic<int> g_opt_mma_fused{0};     // K7 as one launch: 0 auto, 1 never (the pair), 2 whenever it fits
 
 struct Opts {
   int pdl, force_cluster, force_generic, force_tile_rows, no_alias, no_tile_scan, no_tc, tc_split, no_row_mode,
@@ -352,6 +353,23 @@ bool prepare_mma(MmaParams& mp, int& tiles, const RowRanges& rr, void* y, int64_
   if (!mma_splits(tbl, tiles, mp.kparts, mp.pc, mp.ncol)) return false;
   mp.ws = static_cast<float*>(ws);
   const size_t pctas = mma_part_ctas(tbl, tiles);
+  // One launch (clusters of c CTAs per tile, K and columns split c ways), only on request
+  // (LSG_OPT_MMA_FUSED = 2): measured slower than the pair at every preset (c3: 8.1 vs 6.5 us
+  // -- one CTA per SM runs its shrink and expand back to back, the pair overlaps 360 CTAs)
+  mp.fused = 0;
+  const int fmode = g_opt_mma_fused.load();
+  if (fmode == 2) {
+    for (int c = kMmaMaxPc; c >= 2; --c) {
+      if (tbl->h_in % (c * kMmaKC) != 0 || tbl->h_out % (c * kMmaKC) != 0) continue;
+      const int nst = std::max(tbl->h_in, tbl->h_out) / (c * kMmaKC);
+      if (nst > kMmaMaxStagesDecl || mma_fused_smem(R, nst, c) > static_cast<uint32_t>(kSmemBudget)) continue;
+      const size_t ctas = static_cast<size_t>(tiles) * c;
+      if (ctas > pctas || ctas > mma_exp_ctas(tbl, tiles)) continue;
+      mp.fused = 1;
+      mp.kparts = mp.pc = mp.ncol = c;
+      break;
+    }
+  }
   mp.maps_p = static_cast<uint8_t*>(ws) + pctas * kMmaM * R * sizeof(float);
   mp.maps_e = mp.maps_p + pctas * 128;
   mp.n_seg = n_seg;
@@ -1332,6 +1350,10 @@ int lsg_set_option(int32_t option, int32_t value) {
       if (value < 0) return fail(LSG_EINVAL, "lsg: MMA row threshold must be >= 0");
       g_opt_mma_min_rows = value;
       return LSG_OK;
+    case LSG_OPT_MMA_FUSED:
+      if (value < 0 || value > 2) return fail(LSG_EINVAL, "lsg: MMA fused mode must be 0 .. 2");
+      g_opt_mma_fused = value;
+      return LSG_OK;
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }
@@ -1350,6 +1372,7 @@ int lsg_get_option(int32_t option) {
     case LSG_OPT_TC_MIN_ROWS: return g_opt_tc_min_rows.load();
     case LSG_OPT_TC_LEGACY: return g_opt_tc_legacy.load();
     case LSG_OPT_MMA_MIN_ROWS: return g_opt_mma_min_rows.load();
+    case LSG_OPT_MMA_FUSED: return g_opt_mma_fused.load();
   }
   return fail(LSG_EINVAL, "lsg: unknown option");
 }

@@ -81,6 +81,7 @@ struct MmaParams {
   int32_t ncol;      // column slices (gridDim.x of the expand kernel)
   int32_t min_rows;  // segments with min_rows <= len < max_rows take this path
   int32_t max_rows;
+  int32_t fused;     // 1: one launch (sgmv_mma_fused_kernel, clusters of pc = kparts = ncol CTAs)
   unsigned long long* trace;  // phase stamps (instrumented builds only, LSG_TC_TRACE layout)
   int32_t trace_ctas;
 };
@@ -519,6 +520,248 @@ __global__ void __launch_bounds__(kMmaThreads) sgmv_mma_exp_kernel(const __grid_
     }
   }
   LSG_TC_TRACE(1, 5);
+}
+
+// ---- one-launch variant ---------------------------------------------------------------------
+// sgmv_mma_fused_kernel: grid (C, tile bound), clusters of C CTAs per tile (C = kparts = pc =
+// ncol).  CTA c computes the tile's partial over K slice c exactly like the partials kernel,
+// sends it to every CTA of the cluster (DSMEM), sums the C partials in rank order (so every CTA
+// holds the same v, with the pair's arithmetic) and expands its column slice c exactly like the
+// expand kernel.  One buffer set serves both phases: a stage's B slice and y_old are requested
+// into it as soon as the warp that owns the stage has run its shrink MMAs (stages beyond the
+// shrink's count at once: B before the PDL wait, y_old after it).
+__host__ __device__ constexpr uint32_t mma_fused_smem(int R, int stages, int C) {
+  return 1024 + stages * mma_part_stage_bytes(R) + (4 + C) * kMmaM * R * 4 + 2 * kMmaM * R * 2 + 256 +
+         8 * (2 * kMmaMaxStagesDecl + 2);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kMmaThreads) sgmv_mma_fused_kernel(const __grid_constant__ MmaParams p) {
+  static_assert(R == 16 || R == 32 || R == 64, "tensor-core ranks");
+  constexpr int ROWB = R * 2;                    // bytes per A row (= its TMA swizzle span) and per v row
+  constexpr uint32_t kXB = kMmaM * kMmaKC * 2;   // x / y stage bytes
+  constexpr uint32_t kBB = R * kMmaKC * 2;       // A / B stage bytes
+  constexpr uint32_t kSB = mma_part_stage_bytes(R);
+  static_assert(mma_part_stage_bytes(R) == mma_exp_stage_bytes(R), "one buffer per stage for both phases");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int C = p.pc, crank = static_cast<int>(blockIdx.x);  // cluster dims (C, 1, 1), grid.x == C
+  const int KS = p.h_in / C, nk = KS / kMmaKC, NC = p.h_out / C, nn = NC / kMmaKC, nst = nk > nn ? nk : nn;
+  float* red = reinterpret_cast<float*>(smem + nst * kSB);  // [4][16][R]
+  float* recv = red + 4 * kMmaM * R;                        // [C][16][R]
+  uint8_t* vhi = reinterpret_cast<uint8_t*>(recv + C * kMmaM * R);
+  uint8_t* vlo = vhi + kMmaM * R * 2;
+  uint8_t* smap_a = vlo + kMmaM * R * 2;
+  uint8_t* smap_b = smap_a + 128;
+  uint64_t* fullk = reinterpret_cast<uint64_t*>(smap_b + 128);  // [nk] shrink stages
+  uint64_t* fulln = fullk + kMmaMaxStagesDecl;                   // [nn] expand stages
+  uint64_t* rbar = fulln + kMmaMaxStagesDecl;                    // the peers' partials
+
+  __shared__ int s_seg, s_tile;
+  if (warp == 0) {
+    int seg, tin;
+    mma_tile_of(p.seg_starts, p.n_seg, blockIdx.y, lane, p.min_rows, p.max_rows, seg, tin);
+    if (lane == 0) {
+      s_seg = seg;
+      s_tile = tin;
+    }
+  }
+  if (tid == 32) {
+    for (int i = 0; i < nk; ++i) mbar_init(&fullk[i], 1);
+    for (int i = 0; i < nn; ++i) mbar_init(&fulln[i], 1);
+    mbar_init(rbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int slot = s_seg >= 0 ? p.seg_slot[s_seg] : -1;
+  if (s_seg < 0 || slot < 0 || slot >= p.num_slots) {  // the whole cluster (one tile) leaves
+    if (blockIdx.y == 0) {
+      pdl_wait();
+      pdl_launch_dependents();
+    }
+    return;
+  }
+  cluster_arrive_relaxed();  // this CTA's barriers are initialised
+  const int r0 = p.seg_starts[s_seg] + s_tile * kMmaM;
+  const int rows = min(kMmaM, p.seg_starts[s_seg + 1] - r0);
+  const int k0 = crank * KS, n0 = crank * NC;
+  const int64_t cta = static_cast<int64_t>(blockIdx.y) * C + crank;
+  uint8_t* gmap_a = p.maps_p + cta * 128;
+  uint8_t* gmap_b = p.maps_e + cta * 128;
+  const CUtensorMap* amap = reinterpret_cast<const CUtensorMap*>(gmap_a);
+  const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap_b);
+  T* Yg = static_cast<T*>(p.y) + static_cast<int64_t>(r0) * p.ldy + n0;
+  // weights first (before the PDL wait): the A stages, and the B stages that have a buffer of
+  // their own (s >= nk)
+  if (warp == 0) {
+    make_slot_tmap(&p.tmap_a, smap_a, gmap_a, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
+    if (lane == 0)
+      for (int s = 0; s < nk; ++s) {
+        mbar_arrive_expect_tx(&fullk[s], kSB);
+        tma_load_2d(smem + s * kSB + kXB, amap, 0, k0 + s * kMmaKC, &fullk[s]);
+      }
+  } else if (warp == 1) {
+    make_slot_tmap(&p.tmap_b, smap_b, gmap_b, static_cast<const T*>(p.b_ptr[slot]) + p.b_off, lane);
+    if (lane == 0)
+      for (int s = nk; s < nn; ++s) {
+        mbar_arrive_expect_tx(&fulln[s], kSB);
+        tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &fulln[s]);
+      }
+  } else if (warp == 2 && lane < rows) {
+    bulk_prefetch_l2(static_cast<const T*>(p.x) + static_cast<int64_t>(r0 + lane) * p.ldx + k0,
+                     static_cast<uint32_t>(KS * 2));
+  }
+  pdl_wait();  // x and y_old may come from the preceding kernel
+  pdl_launch_dependents();
+  __syncthreads();  // warp 1's B descriptor is published
+  if (lane == 0) asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(gmap_b) : "memory");
+  if (tid == 0) {
+    for (int s = 0; s < nk; ++s) tma_load_2d(smem + s * kSB, &p.tmap_x, k0 + s * kMmaKC, r0, &fullk[s]);
+    for (int s = nk; s < nn; ++s) tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &fulln[s]);
+  }
+
+  // ---- shrink: P^T[R][rows] = A^T . x^T over my K slice (the partials kernel's arithmetic) ---
+  constexpr int MT = R / 16;
+  const bool two = rows > 8;
+  {
+    float acc[MT][2][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0.f;
+    const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;
+    const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;
+    for (int s = warp; s < nk; s += 4) {
+      mbar_wait(&fullk[s], 0);
+      const uint32_t xs = smem_u32(smem + s * kSB), as = xs + kXB;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t b[4];
+        {
+          const int c = 2 * kk + xc;
+          ldsm_x4(xs + xr * 128 + ((c ^ (xr & 7)) << 4), b[0], b[1], b[2], b[3]);
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int k = 16 * kk + ak, c = 2 * i + ac;
+          uint32_t a[4];
+          ldsm_x4_t(as + k * ROWB + ((c ^ swz<ROWB>(k)) << 4), a[0], a[1], a[2], a[3]);
+          mma16816<T>(acc[i][0], a, b[0], b[1]);
+          if (two) mma16816<T>(acc[i][1], a, b[2], b[3]);
+        }
+      }
+      // this warp is done with the buffer: the expand stage s (B, y_old) goes into it
+      __syncwarp();
+      if (s < nn && lane == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&fulln[s], kSB);
+        tma_load_2d(smem + s * kSB, bmap, n0 + s * kMmaKC, 0, &fulln[s]);
+        tma_load_2d(smem + s * kSB + kBB, &p.tmap_y, n0 + s * kMmaKC, r0, &fulln[s]);
+      }
+    }
+    const int g = lane >> 2, t = lane & 3;
+    float* rw = red + warp * kMmaM * R;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m0 = 8 * j + 2 * t, r = 16 * i + g;
+        rw[m0 * R + r] = acc[i][j][0];
+        rw[(m0 + 1) * R + r] = acc[i][j][1];
+        rw[m0 * R + r + 8] = acc[i][j][2];
+        rw[(m0 + 1) * R + r + 8] = acc[i][j][3];
+      }
+  }
+  __syncthreads();
+  // ---- my partial (warp order) -> every CTA of the cluster; v = the C partials in rank order --
+  if (tid == 0) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((C - 1) * kMmaM * R * 4));
+  cluster_wait();  // the peers' barriers are initialised
+  for (int i = tid * 4; i < kMmaM * R; i += kMmaThreads * 4) {
+    float4 s4 = *reinterpret_cast<const float4*>(red + i);
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      const float4 o = *reinterpret_cast<const float4*>(red + w * kMmaM * R + i);
+      s4.x += o.x, s4.y += o.y, s4.z += o.z, s4.w += o.w;
+    }
+    float* mine = recv + crank * kMmaM * R + i;
+    *reinterpret_cast<float4*>(mine) = s4;
+    for (int c = 0; c < C; ++c)
+      if (c != crank) st_async_v4(mapa_u32(mine, static_cast<uint32_t>(c)), s4.x, s4.y, s4.z, s4.w,
+                                  mapa_u32(rbar, static_cast<uint32_t>(c)));
+  }
+  mbar_wait(rbar, 0);
+  __syncthreads();
+  for (int i = tid * 8; i < kMmaM * R; i += kMmaThreads * 8) {  // -> 16-bit hi + lo, swizzled rows
+    float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < C; ++c) {
+      const float4 u0 = *reinterpret_cast<const float4*>(recv + c * kMmaM * R + i);
+      const float4 u1 = *reinterpret_cast<const float4*>(recv + c * kMmaM * R + i + 4);
+      f[0] += u0.x, f[1] += u0.y, f[2] += u0.z, f[3] += u0.w, f[4] += u1.x, f[5] += u1.y, f[6] += u1.z, f[7] += u1.w;
+    }
+    float hf[8], lo[8];
+    const uint4 hi = Cvt<T>::pack8(f);
+    Cvt<T>::unpack8(hi, hf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) lo[e] = f[e] - hf[e];
+    const int m = i / R, c = (i - m * R) >> 3;
+    const uint32_t off = m * ROWB + ((c ^ swz<ROWB>(m)) << 4);
+    *reinterpret_cast<uint4*>(vhi + off) = hi;
+    *reinterpret_cast<uint4*>(vlo + off) = Cvt<T>::pack8(lo);
+  }
+  __syncthreads();
+  // ---- expand my column slice: y^T = B^T . v^T (hi and lo), + y_old, one rounding ----------
+  const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;
+  const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;
+  uint32_t vh[R / 16][4], vl[R / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < R / 16; ++kk) {
+    const int c = 2 * kk + xc;
+    const uint32_t off = xr * ROWB + ((c ^ swz<ROWB>(xr)) << 4);
+    ldsm_x4(smem_u32(vhi + off), vh[kk][0], vh[kk][1], vh[kk][2], vh[kk][3]);
+    ldsm_x4(smem_u32(vlo + off), vl[kk][0], vl[kk][1], vl[kk][2], vl[kk][3]);
+  }
+  const int g = lane >> 2, t = lane & 3;
+  for (int s = warp; s < nn; s += 4) {
+    mbar_wait(&fulln[s], 0);
+    uint8_t* bs = smem + s * kSB;
+    uint8_t* ys = bs + kBB;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float dh[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      float dl[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < R / 16; ++kk) {
+        const int k = 16 * kk + ak, c = 2 * i + ac;
+        uint32_t a[4];
+        ldsm_x4_t(smem_u32(bs + k * 128 + ((c ^ (k & 7)) << 4)), a[0], a[1], a[2], a[3]);
+        mma16816<T>(dh[0], a, vh[kk][0], vh[kk][1]);
+        mma16816<T>(dl[0], a, vl[kk][0], vl[kk][1]);
+        if (two) {
+          mma16816<T>(dh[1], a, vh[kk][2], vh[kk][3]);
+          mma16816<T>(dl[1], a, vl[kk][2], vl[kk][3]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j == 1 && !two) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int m = 8 * j + 2 * t + (e & 1), col = 16 * i + g + (e >> 1) * 8;
+          T* q = reinterpret_cast<T*>(ys + m * 128 + (((col >> 3) ^ (m & 7)) << 4) + (col & 7) * 2);
+          *q = Cvt<T>::from_f(dh[j][e] + dl[j][e] + Cvt<T>::to_f(*q));
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int m = it * 4 + (lane >> 3), c = lane & 7;
+      if (m < rows)
+        st_global_v4(Yg + static_cast<int64_t>(m) * p.ldy + s * kMmaKC + c * 8,
+                     *reinterpret_cast<const uint4*>(ys + m * 128 + ((c ^ (m & 7)) << 4)));
+    }
+  }
 }
 
 }  // namespace lsg

@@ -153,11 +153,13 @@ def mma_cases():
             bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
             pool, x, ss, sl, ref = problem(512, 256, r, bounds, 50 + r)
             for pdl in (0, 1):
-                lsg.set_option(lsg.LSG_OPT_PDL, pdl)
-                y = torch.zeros(int(bounds[-1]), 256, dtype=torch.float16, device=dev)
-                lsg.sgmv(y, x, pool, ss, sl, 0)
-                check(f"mma pair r{r} lens{lens} pdl{pdl}", y, ref)
-    for opt in (lsg._lib.LSG_OPT_MMA_MIN_ROWS, lsg._lib.LSG_OPT_TC_LEGACY, lsg.LSG_OPT_PDL):
+                for fused in (1, 2):  # the two-launch pair, the one-launch form
+                    lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+                    lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, fused)
+                    y = torch.zeros(int(bounds[-1]), 256, dtype=torch.float16, device=dev)
+                    lsg.sgmv(y, x, pool, ss, sl, 0)
+                    check(f"mma {'pair' if fused == 1 else 'one-launch'} r{r} lens{lens} pdl{pdl}", y, ref)
+    for opt in (lsg._lib.LSG_OPT_MMA_MIN_ROWS, lsg._lib.LSG_OPT_TC_LEGACY, lsg.LSG_OPT_PDL, lsg._lib.LSG_OPT_MMA_FUSED):
         lsg.set_option(opt, 0)
 
 

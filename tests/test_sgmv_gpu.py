@@ -37,7 +37,8 @@ def _reset_options(lsg):
     yield
     for opt in (lsg.LSG_OPT_FORCE_CLUSTER, lsg.LSG_OPT_FORCE_GENERIC, lsg.LSG_OPT_FORCE_TILE_ROWS, lsg.LSG_OPT_PDL,
                 lsg.LSG_OPT_NO_TENSOR_CORES, lsg._lib.LSG_OPT_TC_SPLIT, lsg._lib.LSG_OPT_NO_ROW_MODE,
-                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES, lsg._lib.LSG_OPT_TC_LEGACY, lsg._lib.LSG_OPT_MMA_MIN_ROWS):
+                lsg._lib.LSG_OPT_TC_MIN_ROWS, lsg._lib.LSG_OPT_NO_MULTIROW_TILES, lsg._lib.LSG_OPT_TC_LEGACY, lsg._lib.LSG_OPT_MMA_MIN_ROWS,
+                lsg._lib.LSG_OPT_MMA_FUSED):
         lsg.set_option(opt, 0)
 
 
@@ -938,9 +939,16 @@ def test_mma_pair_shared_adapters_match_oracle(lsg, dtype, shape, pop):
     y = p.run()
     assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(dtype)
     assert torch.equal(p.run(), y)
-    if r == 64:  # the automatic choice is the same pair
+    if r == 64:  # the automatic choice is the same path
         lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, 0)
         assert torch.equal(p.run(), y)
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, 1)
+    # the one-launch form (a cluster per tile) and the two-launch pair: both within tolerance
+    for mode in (1, 2):
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, mode)
+        ym = p.run()
+        assert row_norm_err(ym.double().cpu().numpy(), p.reference()) <= tol(dtype), mode
+        assert torch.equal(p.run(), ym), mode
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -957,8 +965,10 @@ def test_mma_pair_long_segments_match_oracle(lsg, dtype, r, lens, gen):
     lsg.set_option(lsg._lib.LSG_OPT_TC_LEGACY, gen)
     for lo in (1, 2):
         lsg.set_option(lsg._lib.LSG_OPT_MMA_MIN_ROWS, lo)
-        y = p.run()
-        assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(dtype), lo
+        for mode in (1, 2):  # the two-launch pair, the one-launch form
+            lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, mode)
+            y = p.run()
+            assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(dtype), (lo, mode)
 
 
 def test_mma_pair_no_adapter_segments_untouched_and_scattered_slots(lsg):
@@ -970,12 +980,14 @@ def test_mma_pair_no_adapter_segments_untouched_and_scattered_slots(lsg):
     x, A, B = random_problem(5120, 5120, 64, bounds, 610)
     y0 = oracle().rng(611).fill_pm1(sum(lens) * 5120).reshape(sum(lens), 5120)
     p = Problem(lsg, x, A, B, bounds, torch.float16, slots=slots, num_slots=12, layers=3, layer=2, y0=y0)
-    y = p.run()
     ref = p.reference()
-    assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(torch.float16)
-    for s in (1, 4):
-        a, b = int(bounds[s]), int(bounds[s + 1])
-        assert torch.equal(y[a:b], p.y0[a:b]), s
+    for mode in (1, 2):  # the two-launch pair, the one-launch form
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, mode)
+        y = p.run()
+        assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(torch.float16), mode
+        for s in (1, 4):
+            a, b = int(bounds[s]), int(bounds[s + 1])
+            assert torch.equal(y[a:b], p.y0[a:b]), (mode, s)
 
 
 def test_mma_pair_many_tiles_and_workspace_bound(lsg):
@@ -985,5 +997,7 @@ def test_mma_pair_many_tiles_and_workspace_bound(lsg):
     bounds = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
     x, A, B = random_problem(1024, 2048, 64, bounds, 620)
     p = Problem(lsg, x, A, B, bounds, torch.bfloat16)
-    y = p.run()
-    assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16)
+    for mode in (1, 2):  # the two-launch pair, the one-launch form
+        lsg.set_option(lsg._lib.LSG_OPT_MMA_FUSED, mode)
+        y = p.run()
+        assert row_norm_err(y.double().cpu().numpy(), p.reference()) <= tol(torch.bfloat16), mode
