@@ -1261,7 +1261,9 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
            layer, stream);
   if (st != LSG_OK) return st;
   DenseLoraParams p{};
-  if (!encode_rows_map(&p.tmap_x, tbl->dtype, x, tbl->h_in, total_rows, ldx)) return fail(LSG_ECUDA, "tensor map x");
+  if (!encode_map_2d(&p.tmap_x, tbl->dtype, x, static_cast<uint64_t>(tbl->h_in), static_cast<uint64_t>(total_rows),
+                     static_cast<uint64_t>(ldx), kTcKB, kDlMaxRows, CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(LSG_ECUDA, "tensor map x");
   {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_out), static_cast<cuuint64_t>(tbl->h_in)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw) * 2};

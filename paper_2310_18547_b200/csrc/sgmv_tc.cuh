@@ -915,11 +915,17 @@ constexpr int kDlN = 64;        // columns per cluster
 constexpr int kDlMaxRows = 64;  // decode rows per launch
 constexpr int kDlKS = 4;        // K split = cluster size; CTA c owns rows [16c, 16c + 16)
 constexpr int kDlRowsPer = kDlMaxRows / kDlKS;
-constexpr int kDlStages = 2;
-constexpr int kDlStage = kTcBox + kTcKB * kDlN * 2;  // x box 16 KB + W box 8 KB
+#ifndef LSG_DL_STAGES
+#define LSG_DL_STAGES 3
+#endif
+constexpr int kDlStages = LSG_DL_STAGES;
+// x box of the 64 decode rows (8 KB) + W box (8 KB).  The MMA's M is 128: its A rows 64..127
+// read the stage's W box -- garbage rows of D that nobody reads (rows >= 64 are padding).
+constexpr int kDlXB = kDlMaxRows * kTcKB * 2;
+constexpr int kDlStage = kDlXB + kTcKB * kDlN * 2;
 
 struct DenseLoraParams {
-  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 x 128, SW128
+  CUtensorMap tmap_x;  // x [s_n, h_in], box 64 (k) x 64 rows, SW128
   CUtensorMap tmap_w;  // W [h_in, h_out] row-major, box 64 (N) x 64 (K), SW128
   void* y;
   int64_t ldy;
@@ -933,9 +939,16 @@ struct DenseLoraParams {
 
 template <int R>
 struct DlLayout {
-  static constexpr uint32_t kB = kDlStages * kDlStage;                    // my rows' B slices
-  static constexpr uint32_t kRecv = kB + kDlRowsPer * R * kDlN * 2;        // [src][16 rows][64] fp32
+  static constexpr uint32_t kB = kDlStages * kDlStage;  // my rows' B slices
+#ifdef LSG_DL_ALIAS
+  // the partials' receive buffer reuses the ring once every CTA of the cluster is done with it
+  static constexpr uint32_t kRecv = 0;
+  static constexpr uint32_t kBars = kB + kDlRowsPer * R * kDlN * 2;
+  static_assert(kDlKS * kDlRowsPer * kDlN * 4 <= kDlStages * kDlStage, "receive buffer fits the ring");
+#else
+  static constexpr uint32_t kRecv = kB + kDlRowsPer * R * kDlN * 2;  // [src][16 rows][64] fp32
   static constexpr uint32_t kBars = kRecv + kDlKS * kDlRowsPer * kDlN * 4;
+#endif
   static constexpr uint32_t kTotal = kBars + 256 + 1024;
 };
 template <int R>
@@ -951,8 +964,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
   uint8_t* smem = align1024(smem_raw);
   uint8_t* Bsm = smem + L::kB;  // [local row][k][64 cols] 16-bit
   float* recv = reinterpret_cast<float*>(smem + L::kRecv);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);  // full[2], empty[2], D, recv
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  constexpr int S = kDlStages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);  // full[S], empty[S], D, recv
+  uint64_t* const bar_d = bars + 2 * S;
+  uint64_t* const bar_recv = bars + 2 * S + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2);
   __shared__ int s_slot[kDlRowsPer];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = static_cast<int>(blockIdx.x);  // cluster rank = K slice = owned row block
@@ -960,7 +976,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
   const int nkb_all = p.h_in / kTcKB, kb0 = (c * nkb_all) / kDlKS, nkb = ((c + 1) * nkb_all) / kDlKS - kb0;
 
   if (tid == 0) {
-    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 2 * S + 2; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
     prefetch_tmap(&p.tmap_x);
     prefetch_tmap(&p.tmap_w);
@@ -996,39 +1012,50 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
   cluster_arrive_relaxed();  // barrier inits -> the cluster
 
+  // TMA producer: the first ring's W boxes before the PDL wait (W is a weight), then x
+  const int pre = nkb < S ? nkb : S;
+  if (warp == 1 && lane == 0)
+    for (int kb = 0; kb < pre; ++kb) {
+      mbar_arrive_expect_tx(&bars[kb], kDlStage);
+      tma_load_2d(smem + kb * kDlStage + kDlXB, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[kb]);
+    }
   pdl_wait();  // x and v come from the preceding kernels
   pdl_launch_dependents();
-  if (warp == 1 && lane == 0) {  // TMA producer: x box + W box per K step of my slice
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kDlStages;
-      if (kb >= kDlStages) mbar_wait(&bars[2 + s], ((kb / kDlStages) - 1) & 1);
+  if (warp == 1 && lane == 0) {  // x box + W box per K step of my slice
+    for (int kb = 0; kb < pre; ++kb) tma_load_2d(smem + kb * kDlStage, &p.tmap_x, (kb0 + kb) * kTcKB, 0, &bars[kb]);
+    for (int kb = pre; kb < nkb; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&bars[S + s], ((kb / S) - 1) & 1);
       mbar_arrive_expect_tx(&bars[s], kDlStage);
       uint8_t* st = smem + s * kDlStage;
       tma_load_2d(st, &p.tmap_x, (kb0 + kb) * kTcKB, 0, &bars[s]);
-      tma_load_2d(st + kTcBox, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[s]);
+      tma_load_2d(st + kDlXB, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[s]);
     }
   } else if (warp == 0 && lane == 0) {  // MMA issuer
     const uint32_t idesc = umma_idesc(fmt, kTcM, kDlN);
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kDlStages;
-      mbar_wait(&bars[s], (kb / kDlStages) & 1);
+      const int s = kb % S;
+      mbar_wait(&bars[s], (kb / S) & 1);
       tc_fence_after();
-      const uint32_t xa = smem_u32(smem + s * kDlStage), wa = xa + kTcBox;
+      const uint32_t xa = smem_u32(smem + s * kDlStage), wa = xa + kDlXB;
 #pragma unroll
       for (int ks = 0; ks < kTcKB / 16; ++ks) {
         const uint64_t ad = umma_desc(xa + ks * 32, 16, 1024, kSw128);            // x: K-major SW128
         const uint64_t bd = umma_desc(wa + ks * 2 * 1024, 8 * 1024, 1024, kSw128);  // W: MN-major SW128
         umma_f16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
       }
-      umma_commit(&bars[2 + s]);
+      umma_commit(&bars[S + s]);
     }
-    umma_commit(&bars[4]);
+    umma_commit(bar_d);
   }
   __syncwarp();
   cluster_wait();  // peers' barriers initialised
-  if (tid == 0) mbar_arrive_expect_tx(&bars[5], static_cast<uint32_t>(kDlKS * kDlRowsPer * kDlN * 4));
-  mbar_wait(&bars[4], 0);
+  if (tid == 0) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(kDlKS * kDlRowsPer * kDlN * 4));
+  mbar_wait(bar_d, 0);
   tc_fence_after();
+#ifdef LSG_DL_ALIAS
+  cluster_sync();  // every CTA's MMAs are done: the rings may take the partials
+#endif
   // row m of my partial D_c -> owner m / 16 (rows >= 64 are padding: warps 2, 3 send nothing)
 #pragma unroll
   for (int cc = 0; cc < kDlN / 16; ++cc) {
@@ -1038,13 +1065,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
     if (m < kDlMaxRows) {
       const int owner = m / kDlRowsPer, ml = m - owner * kDlRowsPer;
       const uint32_t ra = mapa_u32(recv + ((c * kDlRowsPer + ml) * kDlN + cc * 16), static_cast<uint32_t>(owner));
-      const uint32_t rb = mapa_u32(&bars[5], static_cast<uint32_t>(owner));
+      const uint32_t rb = mapa_u32(bar_recv, static_cast<uint32_t>(owner));
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_async_v4(ra + j * 16, d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3], rb);
     }
   }
   cp_async_wait<0>();
-  mbar_wait(&bars[5], 0);
+  mbar_wait(bar_recv, 0);
   __syncthreads();  // every thread's B slices visible
   // my 16 rows x 64 columns: thread -> (row tid / 8, 8 columns)
   {
