@@ -613,6 +613,31 @@ def test_dense_lora_no_adapter_and_empty_segments(lsg):
     assert row_norm_err(y.double().cpu().numpy(), ref) <= tol(dtype)
 
 
+def test_dense_lora_pdl_chain_reads_fresh_x(lsg):
+    """With PDL on, the dense projection's GEMM streams x before its own wait (its shrink releases it
+    only after the shrink's wait): x produced by the kernel right before (an SGMV launch writing
+    it) must be seen complete.  Repeated chains, compared with the PDL-off result."""
+    dtype, h, r = torch.float16, 4096, 16
+    bounds, _, _ = segments_for(DISTINCT, 64, 70)
+    x, A, B = random_problem(h, h, r, bounds, 71)
+    p = Problem(lsg, x, A, B, bounds, dtype)
+    W = torch.tensor(oracle().rng(72).fill_pm1(h * h).reshape(h, h) * 0.05, dtype=torch.float64).to(dtype).cuda()
+    outs = []
+    for pdl in (0, 1):
+        lsg.set_option(lsg.LSG_OPT_PDL, pdl)
+        res = []
+        for it in range(3):
+            xin = torch.zeros_like(p.x)  # x of this layer = an SGMV launch's output
+            lsg.sgmv(xin, p.x, p.pool, p.seg_starts, p.seg_slot, 0)
+            y = torch.full_like(p.x, float("nan"))
+            lsg.dense_lora(y, xin, W, p.pool, p.seg_starts, p.seg_slot, 0)
+            res.append(y)
+        torch.cuda.synchronize()
+        outs.append(res)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+
+
 def test_dense_lora_rejects_unsupported(lsg):
     pool = lsg.AdapterPool(2, 1, 4096, 4096, 32, torch.float16)
     x = torch.zeros(4, 4096, dtype=torch.float16, device="cuda")
