@@ -512,6 +512,19 @@ bool encode_b_blocks(CUtensorMap* m, int dtype, const void* base, int h_out, int
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// activations [rows][cols] (leading dimension ld) as 3-D {64 columns, rows, cols / 64 blocks}
+// (strides ld * 2, 128 bytes), box {64, 16 rows, blocks}, SW128: one copy lands a 16-row tile's
+// `blocks` column blocks as [block][16 rows][64] (K9's activation stages)
+bool encode_rows_blocks(CUtensorMap* m, int dtype, const void* base, int cols, int rows, int64_t ld, int blocks) {
+  const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, 128};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kMmaM), static_cast<cuuint32_t>(blocks)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode_tiled_fn()(m, dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, int64_t ldx,
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
@@ -526,7 +539,9 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     const int abox = R == 16 ? stream_a_box_rows(16) : R == 32 ? stream_a_box_rows(32) : stream_a_box_rows(64);
     if (!encode_map_2d(&q.tmap_a, tbl->dtype, x, 64, static_cast<uint64_t>(tbl->h_in) * R / 64, 64, 64, abox,
                        CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_b_blocks(&q.tmap_b, tbl->dtype, x, tbl->h_out, R, stream_kc(R) / 64))
+        !encode_b_blocks(&q.tmap_b, tbl->dtype, x, tbl->h_out, R, stream_kc(R) / 64) ||
+        !encode_rows_blocks(&q.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx, stream_kc(R) / 64) ||
+        !encode_rows_blocks(&q.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy, stream_kc(R) / 64))
       return false;
     q.x = x;
     q.y = y;

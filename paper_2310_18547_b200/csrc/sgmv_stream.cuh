@@ -57,6 +57,15 @@ __device__ __forceinline__ void named_barrier_sync(int id, int threads) {
 __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_local_cnt(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tmap, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // phase stamp from any one thread (the producer warp's lane 0 included)
 #define LSG_STREAM_TRACE(i)                                                                        \
   do {                                                                                             \
@@ -76,6 +85,12 @@ constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
 #ifndef LSG_STREAM_SMEM
 #define LSG_STREAM_SMEM (220 * 1024)
 #endif
+// 1: a stage's 16 activation rows (x or y_old) move as ONE 3-D TMA box {64 columns, 16 rows,
+// KC / 64 column blocks} (SW128), and a full tile's y as one 3-D box store; 0: one 1-D bulk
+// copy per row (padded rows)
+#ifndef LSG_STREAM_ABOX
+#define LSG_STREAM_ABOX 1
+#endif
 #ifndef LSG_STREAM_KC16
 #define LSG_STREAM_KC16 1024
 #endif
@@ -89,7 +104,7 @@ __host__ __device__ constexpr int stream_kc(int R) { return R == 16 ? LSG_STREAM
 // rows of A's 128-byte view per stage, and per TMA box (<= 256)
 __host__ __device__ constexpr int stream_a_view_rows(int R) { return stream_kc(R) * R / 64; }
 __host__ __device__ constexpr int stream_a_box_rows(int R) { return stream_a_view_rows(R) < 256 ? stream_a_view_rows(R) : 256; }
-__host__ __device__ constexpr uint32_t stream_pitch(int R) { return stream_kc(R) * 2 + 16; }
+__host__ __device__ constexpr uint32_t stream_pitch(int R) { return stream_kc(R) * 2 + (LSG_STREAM_ABOX ? 0 : 16); }
 __host__ __device__ constexpr uint32_t stream_wbytes(int R) { return stream_kc(R) * R * 2; }
 __host__ __device__ constexpr uint32_t stream_slot_bytes(int R) {
   return (stream_wbytes(R) + kMmaM * stream_pitch(R) + 1023u) & ~1023u;
@@ -107,6 +122,8 @@ struct StreamParams {
                        // (strides h_out * 2, 128 bytes), box 64 x R x KC/64, SW128: ONE copy per
                        // stage lands the stage's [column block][R][64] layout (the per-stage copy
                        // count, not the bytes, is what L2 weight traffic costs: tma_probe.cu)
+  CUtensorMap tmap_x;  // x as 3-D {64 columns, s_n rows, h_in / 64 blocks}, box {64, 16, KC / 64}, SW128
+  CUtensorMap tmap_y;  // y likewise over h_out (loads of y_old, stores of full tiles)
   const void* x;
   void* y;
   int64_t ldx;
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       const CUtensorMap* bmap = reinterpret_cast<const CUtensorMap*>(gmap + 128);
       const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx;
       const T* Y = static_cast<const T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
-      const uint32_t bytes = kWB + static_cast<uint32_t>(rows) * KC * 2;
+      const uint32_t bytes = kWB + static_cast<uint32_t>(LSG_STREAM_ABOX ? kMmaM : rows) * KC * 2;
       auto weights = [&](int i) {
         uint8_t* sb = smem + (i % S) * kSB;
         if (kALin && i < nk) {  // A rows [i*KC, (i+1)*KC): one contiguous copy
@@ -222,6 +239,11 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       };
       auto acts = [&](int i) {  // x (shrink) or y_old (expand): one bulk copy per row of the tile
         uint8_t* sb = smem + (i % S) * kSB + kWB;
+#if LSG_STREAM_ABOX  // one box of 16 rows (rows past the segment are loaded, never stored; past s_n: zeros)
+        if (i < nk) tma_load_3d(sb, &p.tmap_x, 0, r0, i * (KC / 64), &full[i % S]);
+        else tma_load_3d(sb, &p.tmap_y, 0, r0, (i - nk) * (KC / 64), &full[i % S]);
+        return;
+#endif
         const T* src = i < nk ? X + i * KC : Y + (i - nk) * KC;
         const int64_t ld = i < nk ? p.ldx : p.ldy;
         for (int m = 0; m < rows; ++m) bulk_g2s(sb + m * PITCH, src + m * ld, KC * 2, &full[i % S]);
@@ -272,7 +294,14 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
     for (int q = 0; q < KPW; ++q) {
       const int kk = warp * KPW + q;
       uint32_t b[4];  // x^T: {b0, b1} rows 0..7, {b2, b3} rows 8..15 (padded rows)
+#if LSG_STREAM_ABOX  // [block][16 rows][64 columns], SW128: chunk q of row xr
+      {
+        const int q16 = 2 * kk + xc;
+        ldsm_x4(xs + (q16 >> 3) * (kMmaM * 128) + xr * 128 + (((q16 & 7) ^ (xr & 7)) << 4), b[0], b[1], b[2], b[3]);
+      }
+#else
       ldsm_x4(xs + xr * PITCH + (2 * kk + xc) * 16, b[0], b[1], b[2], b[3]);
+#endif
 #pragma unroll
       for (int i = 0; i < MT; ++i) {  // A^T block (rank 16i.., k 16kk..) from the 128-byte view rows
         uint32_t a[4];
@@ -372,12 +401,45 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int m = g + 8 * h;
+#if LSG_STREAM_ABOX
+            uint32_t* q = reinterpret_cast<uint32_t*>(ys + bq * (kMmaM * 128) + m * 128 +
+                                                      (((2 * jp + jj) ^ (m & 7)) << 4) + 4 * t);
+            (void)col;
+#else
             uint32_t* q = reinterpret_cast<uint32_t*>(ys + m * PITCH + col * 2);
+#endif
             *q = add2_round<T>(*q, d[jj][2 * h] + e2[jj][2 * h], d[jj][2 * h + 1] + e2[jj][2 * h + 1]);
           }
         }
       }
     }
+#if LSG_STREAM_ABOX
+    if (rows == kMmaM) {                      // full tile: ONE 3-D box store of the stage
+      fence_proxy_async_smem();               // epilogue writes -> the TMA store
+      named_barrier_sync(1, 32 * kStreamCW);  // the stage's y tile is complete
+      if (tid == 0) {
+        tma_store_3d(&p.tmap_y, ys, 0, r0, j * (KC / 64));
+        bulk_commit_group();
+        bulk_wait_group_read<1>();            // the previous stage's store has read its slot
+        if (j > 0) mbar_arrive_local_cnt(&empty[(s - 1) % S], kStreamCW);
+      }
+    } else {                                  // last tile of a segment: its rows, de-swizzled
+      named_barrier_sync(1, 32 * kStreamCW);
+      for (int i = tid; i < rows * (KC / 8); i += 32 * kStreamCW) {
+        const int m = i / (KC / 8), q16 = i - m * (KC / 8);
+        st_global_v4(Yg + static_cast<int64_t>(m) * p.ldy + j * KC + q16 * 8,
+                     *reinterpret_cast<const uint4*>(ys + (q16 >> 3) * (kMmaM * 128) + m * 128 +
+                                                     (((q16 & 7) ^ (m & 7)) << 4)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[s % S]);
+    }
+  }
+  if (rows == kMmaM && tid == 0) {  // the last stage's store
+    bulk_wait_group_read<0>();
+    mbar_arrive_local_cnt(&empty[(nst - 1) % S], kStreamCW);
+  }
+#else
     fence_proxy_async_smem();                 // epilogue writes -> the bulk stores
     named_barrier_sync(1, 32 * kStreamCW);    // the stage's y tile is complete
     if (lane == 0) {                          // warp w stores rows 2w, 2w + 1 (the segment's rows only)
@@ -393,6 +455,7 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
     bulk_wait_group_read<0>();
     mbar_arrive_local(&empty[(nst - 1) % S]);
   }
+#endif
   if (tid == 0) LSG_STREAM_TRACE(5);
 }
 

@@ -45,7 +45,8 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, i
       : "memory");
 }
 
-__global__ void probe(const __grid_constant__ CUtensorMap map, const __half* x, int cols, int mode, int depth,
+__global__ void probe(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap m3s,
+                      const __grid_constant__ CUtensorMap m3n, const __half* x, int cols, int mode, int depth,
                       unsigned long long* out, int KC, int RT, int smem_bytes) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + smem_bytes - 256);
@@ -66,6 +67,10 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const __half* x, 
     mb_expect(b, stage);
     if (mode == 0) {
       for (int q = 0; q < KC / 64; ++q) tma2d(dst + q * 2048, &map, s * KC + q * 64, r0, b);  // RT = 16 only
+    } else if (mode == 2) {  // ONE 3-D box per stage: {64 cols, RT rows, KC/64 blocks}, SW128
+      tma3d(dst, &m3s, 0, r0, s * KC / 64, b);
+    } else if (mode == 3) {  // ONE 3-D box per stage: {256 cols, RT rows, KC/256 blocks}, no swizzle
+      tma3d(dst, &m3n, 0, r0, s * KC / 256, b);
     } else {
       for (int m = 0; m < RT; ++m) bulk(dst + m * KC * 2, x + static_cast<int64_t>(r0 + m) * cols + s * KC, KC * 2, b);
     }
@@ -140,13 +145,25 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
   auto enc = reinterpret_cast<decltype(&cuTensorMapEncodeTiled)>(fn);
-  std::vector<CUtensorMap> maps(nbuf);
+  std::vector<CUtensorMap> maps(nbuf), m3s(nbuf), m3n(nbuf);
   for (int i = 0; i < nbuf; ++i) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     cuuint64_t str[1] = {static_cast<cuuint64_t>(cols) * 2};
     cuuint32_t box[2] = {64, 16}, es[2] = {1, 1};
     enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, xs[i], dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint64_t d3[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+    cuuint64_t s3[2] = {static_cast<cuuint64_t>(cols) * 2, 128};
+    cuuint32_t b3[3] = {64, 16, 16}, e3[3] = {1, 1, 1};
+    if (enc(&m3s[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, xs[i], d3, s3, b3, e3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      printf("m3s encode failed\n");
+    cuuint64_t d4[3] = {256, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 256)};
+    cuuint64_t s4[2] = {static_cast<cuuint64_t>(cols) * 2, 512};
+    cuuint32_t b4[3] = {256, 16, 4};
+    if (enc(&m3n[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, xs[i], d4, s4, b4, e3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      printf("m3n encode failed\n");
   }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -154,17 +171,18 @@ int main() {
   struct Cfg { int mode, RT, KC, depth, ctas_per_sm; };
   const Cfg cfgs[] = {{0, 16, 256, 8, 1},  {1, 16, 1024, 4, 1}, {1, 16, 2048, 3, 1}, {1, 16, 4096, 1, 1},
                       {1, 8, 1024, 4, 2},  {1, 8, 2048, 3, 2},  {1, 8, 4096, 1, 2},  {1, 16, 1024, 2, 2},
-                      {1, 4, 4096, 2, 3},  {1, 4, 2048, 4, 3}};
+                      {1, 4, 4096, 2, 3},  {1, 4, 2048, 4, 3}, {1, 16, 1024, 3, 1}, {2, 16, 1024, 3, 1},
+                      {3, 16, 1024, 3, 1}, {2, 16, 1024, 6, 1}, {3, 16, 1024, 6, 1}};
   for (const Cfg& c : cfgs) {
     const int smem = c.ctas_per_sm == 1 ? 210 * 1024 : c.ctas_per_sm == 2 ? 110 * 1024 : 72 * 1024;
     if (c.depth * c.RT * c.KC * 2 + 256 > smem) continue;
     const int ctas = rows / c.RT;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int w = 0; w < 3; ++w) probe<<<ctas, 32, smem>>>(maps[w], xs[w], cols, c.mode, c.depth, out, c.KC, c.RT, smem);
+    for (int w = 0; w < 3; ++w) probe<<<ctas, 32, smem>>>(maps[w], m3s[w], m3n[w], xs[w], cols, c.mode, c.depth, out, c.KC, c.RT, smem);
     cudaEventRecord(a);
     const int iters = 32;
     for (int it = 0; it < iters; ++it)
-      probe<<<ctas, 32, smem>>>(maps[it % nbuf], xs[it % nbuf], cols, c.mode, c.depth, out, c.KC, c.RT, smem);
+      probe<<<ctas, 32, smem>>>(maps[it % nbuf], m3s[it % nbuf], m3n[it % nbuf], xs[it % nbuf], cols, c.mode, c.depth, out, c.KC, c.RT, smem);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;
