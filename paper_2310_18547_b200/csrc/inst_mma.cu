@@ -54,6 +54,10 @@ static int launch_stream_inst(const StreamParams& p, int tiles, cudaStream_t st)
   if (!configured_on_device(configured)) {
     const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stream smem)");
+    // the largest shared-memory carveout, so the short-segment kernel's CTAs of the same call
+    // can share an SM with a streaming CTA when its ring leaves room
+    const cudaError_t e2 = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFuncSetAttribute(stream carveout)");
     mark_configured(configured);
   }
   const cudaError_t e = launch_ex(k, dim3(static_cast<unsigned>(tiles)), dim3(kStreamThreads),

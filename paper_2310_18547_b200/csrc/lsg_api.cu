@@ -563,7 +563,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     const uint32_t fixed = R == 16 ? stream_fixed(16) : R == 32 ? stream_fixed(32) : stream_fixed(64);
     const uint32_t slotb = R == 16 ? stream_slot_bytes(16) : R == 32 ? stream_slot_bytes(32) : stream_slot_bytes(64);
     // >= 2 slots: the expand releases a slot only after the NEXT stage's stores are issued
-    q.stages = std::min({nst, kStreamMaxStages, static_cast<int>((kStreamSmem - fixed) / slotb)});
+    q.stages = std::min({nst, kStreamMaxStages, static_cast<int>((stream_smem_budget(R) - fixed) / slotb)});
     if (q.stages < 2 || nst < 2) return false;
     lp.stream9 = 1;
     lp.tiles = tiles;
@@ -840,7 +840,11 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     if (span % cand != 0 && cand != c_cap && cand != c_min) continue;
     if (smem_for(cand) > kSmemBudget) continue;
     if (c_small == 0) c_small = cand;
-    const int64_t limit = (pl.tile_scan || cand <= 4) ? 256 : 148;
+    // behind the rank-16 streaming kernel (K9) the short-segment CTAs share SMs with its CTAs
+    // (one each): at most ~128 CTAs (c4: C = 8 -> 4, 14.8 -> 14.1 us)
+    const int64_t limit = (long_on_tc && t->rank == 16 && stream_ok(t, s_n)) ? 128
+                          : (pl.tile_scan || cand <= 4)                       ? 256
+                                                                              : 148;
     if (est_clusters * cand <= limit) c = cand;
   }
   if (c == 0) c = c_small;

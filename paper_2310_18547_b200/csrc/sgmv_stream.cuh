@@ -91,10 +91,17 @@ constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
 #ifndef LSG_STREAM_ABOX
 #define LSG_STREAM_ABOX 1
 #endif
+// Rank 16: KC = 512 in a 140 KB ring (four 32 KB slots): the short-segment kernel of the same
+// call (70 KB CTAs) then shares the SMs instead of waiting for streaming CTAs to exit
+// (c4: 16.2 -> 14.8 us; KC 1024 in 220 KB: three 64 KB slots, one CTA per SM)
 #ifndef LSG_STREAM_KC16
-#define LSG_STREAM_KC16 1024
+#define LSG_STREAM_KC16 512
+#endif
+#ifndef LSG_STREAM_SMEM16
+#define LSG_STREAM_SMEM16 (140 * 1024)
 #endif
 constexpr int kStreamSmem = LSG_STREAM_SMEM;
+__host__ __device__ constexpr int stream_smem_budget(int R) { return R == 16 ? LSG_STREAM_SMEM16 : LSG_STREAM_SMEM; }
 
 // Stage geometry per rank: KC columns per stage (x / y_old rows move as one 1-D bulk copy
 // of KC * 2 bytes each -- >= 1 KiB pieces keep HBM streaming at full rate, 128-byte
