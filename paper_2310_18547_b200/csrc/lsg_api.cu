@@ -158,17 +158,21 @@ int tc_nq(const lsg_weight_table* t) {
 
 int tc_fused_c(const lsg_weight_table* t, int* compact);
 
-int tc_min_rows();
+int tc_min_rows(const lsg_weight_table* t = nullptr);
 // Upper bound on the 128-row tiles of the segments with >= tc_min_rows() rows:
 // sum ceil(len / 128) <= s_n / 128 + (number of such segments).
 int tc_tile_bound(int s_n, int n_seg) {
   return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows()));
 }
 
-// Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default).
-int tc_min_rows() {
+// Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default:
+// 384 at rank 16, else 128).  Measured crossover at rank 16, h = 4096 (one prefill segment +
+// decodes, µs per site, CUDA-core row mode vs tensor cores): 128 rows 5.7 vs 10.8, 256 rows
+// 10.6 vs 11.2, 512 rows 17.7 vs 11.7.  Without a table: the smallest default (tile bounds).
+int tc_min_rows(const lsg_weight_table* t) {
   const int x = cur().tc_min_rows;
-  return x > 0 ? x : kTcMinRows;
+  if (x > 0) return x;
+  return t != nullptr && t->rank == 16 ? kTcMinRows16 : kTcMinRows;
 }
 
 bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
@@ -208,15 +212,15 @@ size_t tc3_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg) {
   return static_cast<size_t>(tc_tile_bound(s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
 }
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
-  if (tc_nq(t) == 0 || s_n < tc_min_rows()) return 0;
+  if (tc_nq(t) == 0 || s_n < tc_min_rows(t)) return 0;
   if (stream_ok(t, s_n)) return static_cast<size_t>(stream_tiles(s_n, s_n)) * 256;
-  if (tc3_ok(t, s_n)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows());
+  if (tc3_ok(t, s_n)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows(t));
   if (!cur().tc_split && tc_gen(t, s_n) == 3) return 0;  // the MMA pair's own region (row_ranges)
   // the fused kernels keep v on chip
   if (!cur().tc_split && ((cur().tc_legacy == 2 && tc2_choose(t, nullptr)) ||
                            (cur().tc_legacy == 1 && tc_fused_c(t, nullptr) > 0)))
     return 0;
-  return tc_nq(t) > 0 && s_n >= tc_min_rows() ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
+  return tc_nq(t) > 0 && s_n >= tc_min_rows(t) ? static_cast<size_t>(s_n) * t->rank * sizeof(float) : 0;
 }
 
 // ---- segment-tile MMA pair (K7, sgmv_mma.cuh) ---------------------------------------
@@ -237,13 +241,13 @@ struct RowRanges {
 RowRanges row_ranges(const lsg_weight_table* t, int n_seg, int s_n) {
   RowRanges rr;
   if (cur().no_tc) return rr;
-  const bool tc = tc_nq(t) > 0 && s_n >= tc_min_rows();
+  const bool tc = tc_nq(t) > 0 && s_n >= tc_min_rows(t);
   const bool gen3 = !cur().tc_split && tc_gen(t, s_n) == 3 && mma_shape_ok(t);
-  if (tc && !gen3) rr.tc_lo = tc_min_rows();
+  if (tc && !gen3) rr.tc_lo = tc_min_rows(t);
   int lo = cur().mma_min_rows;
   if (lo <= 0) lo = (t->rank == 64 && s_n > n_seg) ? 1 : 0;
   if (!mma_shape_ok(t)) lo = 0;
-  if (gen3 && tc) lo = lo > 0 ? std::min(lo, tc_min_rows()) : tc_min_rows();
+  if (gen3 && tc) lo = lo > 0 ? std::min(lo, tc_min_rows(t)) : tc_min_rows(t);
   const int hi = rr.tc_lo > 0 ? rr.tc_lo : kRowsInf;
   if (lo > 0 && lo < hi && s_n >= lo) {
     rr.mma_lo = lo;
@@ -390,7 +394,7 @@ size_t align256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
 size_t call_ws_bound(const lsg_weight_table* t, int s_n) {
   const RowRanges rr = row_ranges(t, std::max(0, s_n - 1), s_n);
   size_t b = rr.mma_lo > 0 ? align256(mma_ws_bytes(t, s_n, s_n, rr.mma_lo)) : 0;
-  if (tc_nq(t) > 0 && s_n >= tc_min_rows()) b += tc_workspace_bytes(t, s_n);
+  if (tc_nq(t) > 0 && s_n >= tc_min_rows(t)) b += tc_workspace_bytes(t, s_n);
   return b;
 }
 
@@ -529,7 +533,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
   const int nq = tc_nq(tbl);
-  if (nq == 0 || s_n < tc_min_rows() || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
+  if (nq == 0 || s_n < tc_min_rows(tbl) || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
   if (stream_ok(tbl, s_n)) {
     const int tiles = stream_tiles(s_n, n_seg), R = tbl->rank;
@@ -567,7 +571,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     if (q.stages < 2 || nst < 2) return false;
     lp.stream9 = 1;
     lp.tiles = tiles;
-    q.min_rows = tc_min_rows();
+    q.min_rows = tc_min_rows(tbl);
     q.trace = g_trace;
     q.trace_ctas = g_trace_ctas;
     return true;
@@ -593,7 +597,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     pp.num_slots = tbl->num_slots;
     pp.h_in = tbl->h_in;
     pp.kparts = tc3_kparts(tbl->h_in);
-    pp.min_rows = tc_min_rows();
+    pp.min_rows = tc_min_rows(tbl);
     pp.trace = g_trace;
     pp.trace_ctas = g_trace_ctas;
     xp.y = y;
@@ -639,7 +643,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     tp.kbs_max = ch.kbs;
     tp.chs_max = ch.chs;
     tp.stages = ch.stages;
-    tp.min_rows = tc_min_rows();
+    tp.min_rows = tc_min_rows(tbl);
     tp.tiles = lp.tiles;
     tp.trace = g_trace;
     tp.trace_ctas = g_trace_ctas;
@@ -670,7 +674,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
     fp.h_out = tbl->h_out;
     fp.kcs_max = ((tbl->h_in / kTcKB + fc - 1) / fc) * kTcKB;
     fp.compact = compact;
-    fp.min_rows = tc_min_rows();
+    fp.min_rows = tc_min_rows(tbl);
     fp.trace = g_trace;
     fp.trace_ctas = g_trace_ctas;
     return true;
@@ -697,7 +701,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   sp.num_slots = tbl->num_slots;
   sp.h_in = tbl->h_in;
   sp.kcs = tbl->h_in / nq;
-  sp.min_rows = tc_min_rows();
+  sp.min_rows = tc_min_rows(tbl);
   sp.trace = g_trace;
   sp.trace_ctas = g_trace_ctas;
   ep.y = y;
@@ -711,7 +715,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
   ep.s_n = s_n;
   ep.num_slots = tbl->num_slots;
   ep.h_out = tbl->h_out;
-  ep.min_rows = tc_min_rows();
+  ep.min_rows = tc_min_rows(tbl);
   ep.trace = g_trace;
   ep.trace_ctas = g_trace_ctas;
   return true;
@@ -1135,7 +1139,7 @@ int lsg_sgmv_multi_ex(const lsg_sgmv_site* sites, int32_t num_sites, const int32
                  !cur().force_generic && !cur().no_row_mode &&
                  static_cast<int64_t>(num_sites) * total_rows <= kMaxGridY &&
                  make_plan(t0, kKFused, num_segments, total_rows, true).mt == 1 &&
-                 (cur().no_tc || total_rows < tc_min_rows() || tc_nq(t0) == 0);
+                 (cur().no_tc || total_rows < tc_min_rows(t0) || tc_nq(t0) == 0);
   for (int i = 0; grouped && i < num_sites; ++i)
     grouped = sites[i].x != nullptr && sites[i].y != nullptr && aligned16(sites[i].x) && aligned16(sites[i].y) &&
               sites[i].ldx % 8 == 0 && sites[i].ldy % 8 == 0 && sites[i].ldx >= t0->h_in &&
