@@ -161,8 +161,8 @@ int tc_fused_c(const lsg_weight_table* t, int* compact);
 int tc_min_rows(const lsg_weight_table* t = nullptr);
 // Upper bound on the 128-row tiles of the segments with >= tc_min_rows() rows:
 // sum ceil(len / 128) <= s_n / 128 + (number of such segments).
-int tc_tile_bound(int s_n, int n_seg) {
-  return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows()));
+int tc_tile_bound(const lsg_weight_table* t, int s_n, int n_seg) {
+  return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows(t)));
 }
 
 // Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default:
@@ -194,7 +194,9 @@ constexpr int kStreamMinRows = 1024;
 int tc_gen(const lsg_weight_table* t, int s_n) {
   const int g = cur().tc_legacy;
   if (g != 0) return g;
-  if (s_n >= kStreamMinRows && stream_shape_ok(t)) return 4;
+  // rank 16: the streaming kernel for every tensor-core call (>= 384 rows; measured 512-row
+  // prefill + decodes 10.9 us vs 11.7 on the tcgen05 pair, 768 rows 11.3)
+  if ((s_n >= kStreamMinRows || t->rank == 16) && stream_shape_ok(t)) return 4;
   if (tc_nq(t) > 0 && t->h_out % kTcNT == 0) return 5;  // measured: c4-128 10.8 us vs 12.3 on K7
   if (mma_shape_ok(t)) return 3;
   return 5;
@@ -205,15 +207,15 @@ bool tc3_ok(const lsg_weight_table* t, int s_n) {
 bool stream_ok(const lsg_weight_table* t, int s_n) {
   return !cur().tc_split && tc_gen(t, s_n) == 4 && stream_shape_ok(t);
 }
-int stream_tiles(int s_n, int n_seg) {  // 16-row tiles of the segments with >= tc_min_rows rows
-  return std::max(1, s_n / 16 + std::min(n_seg, s_n / tc_min_rows()));
+int stream_tiles(const lsg_weight_table* t, int s_n, int n_seg) {  // 16-row tiles of the segments with >= tc_min_rows rows
+  return std::max(1, s_n / 16 + std::min(n_seg, s_n / tc_min_rows(t)));
 }
 size_t tc3_ws_bytes(const lsg_weight_table* t, int s_n, int n_seg) {
-  return static_cast<size_t>(tc_tile_bound(s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
+  return static_cast<size_t>(tc_tile_bound(t, s_n, n_seg)) * tc3_kparts(t->h_in) * kTcM * t->rank * sizeof(float);
 }
 size_t tc_workspace_bytes(const lsg_weight_table* t, int s_n) {
   if (tc_nq(t) == 0 || s_n < tc_min_rows(t)) return 0;
-  if (stream_ok(t, s_n)) return static_cast<size_t>(stream_tiles(s_n, s_n)) * 256;
+  if (stream_ok(t, s_n)) return static_cast<size_t>(stream_tiles(t, s_n, s_n)) * 256;
   if (tc3_ok(t, s_n)) return tc3_ws_bytes(t, s_n, s_n / tc_min_rows(t));
   if (!cur().tc_split && tc_gen(t, s_n) == 3) return 0;  // the MMA pair's own region (row_ranges)
   // the fused kernels keep v on chip
@@ -533,10 +535,10 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
                            const lsg_weight_table* tbl, const int32_t* seg_starts, const int32_t* seg_slot, int n_seg,
                            int s_n, int layer, void* ws, size_t ws_bytes) {
   const int nq = tc_nq(tbl);
-  if (nq == 0 || s_n < tc_min_rows(tbl) || tc_tile_bound(s_n, n_seg) > kMaxGridY) return false;
+  if (nq == 0 || s_n < tc_min_rows(tbl) || tc_tile_bound(tbl, s_n, n_seg) > kMaxGridY) return false;
   if (!aligned16(x) || !aligned16(y) || ldx % 8 != 0 || ldy % 8 != 0 || encode_tiled_fn() == nullptr) return false;
   if (stream_ok(tbl, s_n)) {
-    const int tiles = stream_tiles(s_n, n_seg), R = tbl->rank;
+    const int tiles = stream_tiles(tbl, s_n, n_seg), R = tbl->rank;
     if (ws == nullptr || !aligned16(ws) || ws_bytes < static_cast<size_t>(tiles) * 256) return false;
     StreamParams& q = lp.sp9;
     q = StreamParams{};
@@ -586,7 +588,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
         !encode_rows_map(&xp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
       return false;
     lp.tc3 = 1;
-    lp.tiles = tc_tile_bound(s_n, n_seg);
+    lp.tiles = tc_tile_bound(tbl, s_n, n_seg);
     pp.ws = static_cast<float*>(ws);
     pp.a_ptr = tbl->a_ptr;
     pp.a_off = static_cast<int64_t>(layer) * tbl->a_layer_stride;
@@ -626,7 +628,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
       return false;
     lp.stream_c = ch.C;
     lp.stream_smem = ch.smem;
-    lp.tiles = tc_tile_bound(s_n, n_seg);
+    lp.tiles = tc_tile_bound(tbl, s_n, n_seg);
     tp.y = y;
     tp.ldy = ldy;
     tp.a_ptr = tbl->a_ptr;
@@ -658,7 +660,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
         !encode_rows_map(&fp.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
       return false;
     lp.fused_c = fc;
-    lp.tiles = tc_tile_bound(s_n, n_seg);
+    lp.tiles = tc_tile_bound(tbl, s_n, n_seg);
     fp.y = y;
     fp.ldy = ldy;
     fp.a_ptr = tbl->a_ptr;
@@ -688,7 +690,7 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
       !encode_rows_map(&ep.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy))
     return false;
   // tiles of long segments: sum ceil(len/128) over len >= 128 is at most s_n/64
-  const int tiles = tc_tile_bound(s_n, n_seg);
+  const int tiles = tc_tile_bound(tbl, s_n, n_seg);
   lp.nq = nq;
   lp.tiles = tiles;
   sp.v = static_cast<float*>(ws);
