@@ -301,9 +301,9 @@ typedef enum {
                                    at 128-256 decode rows: an engine that knows a step has no prefill
                                    segment sets it above the batch size for that step. */
   LSG_OPT_TC_LEGACY = 10,       /* long-segment kernel generation: 0 (default) auto -- the one-pass
-                                   streaming kernel (a CTA per 16-row tile) for calls of >= 1024 rows,
-                                   else the cluster-free tcgen05 pair (the segment-tile MMA pair where
-                                   that does not apply); A/B measurements: 1 the first fused
+                                   streaming kernel (a CTA per 16-row tile) at ranks 16 / 32 and for calls
+                                   of >= 1024 rows, the segment-tile MMA pair at rank 64 below that,
+                                   else the cluster-free tcgen05 pair; A/B measurements: 1 the first fused
                                    cluster kernel (rank 16); 2 the streamed cluster kernel (ranks 16 / 32);
                                    3 the segment-tile MMA pair; 4 the streaming kernel; 5 the
                                    cluster-free tcgen05 partials + expand pair */

@@ -186,17 +186,20 @@ bool stream_shape_ok(const lsg_weight_table* t) {
          t->a_layer_stride % 8 == 0 && t->b_layer_stride % 8 == 0;
 }
 // Long-segment kernel generation of a call (LSG_OPT_TC_LEGACY): 0 = auto -- the one-pass
-// streaming kernel (K9, sgmv_stream.cuh) for calls of >= 1024 rows (enough 16-row tiles to
-// fill the GPU), else the cluster-free tcgen05 pair (sgmv_tc3.cuh; the MMA pair K7 where it
-// does not apply); explicit 1 / 2 = the cluster kernels,
+// streaming kernel (K9, sgmv_stream.cuh) at ranks 16 / 32 and for calls of >= 1024 rows, the
+// segment-tile MMA pair K7 at rank 64 below that, else the cluster-free tcgen05 pair
+// (sgmv_tc3.cuh); explicit 1 / 2 = the cluster kernels,
 // 3 = the MMA pair, 4 = the streaming kernel, 5 = the cluster-free tcgen05 pair (sgmv_tc3.cuh).
 constexpr int kStreamMinRows = 1024;
 int tc_gen(const lsg_weight_table* t, int s_n) {
   const int g = cur().tc_legacy;
   if (g != 0) return g;
-  // rank 16: the streaming kernel for every tensor-core call (>= 384 rows; measured 512-row
-  // prefill + decodes 10.9 us vs 11.7 on the tcgen05 pair, 768 rows 11.3)
-  if ((s_n >= kStreamMinRows || t->rank == 16) && stream_shape_ok(t)) return 4;
+  // ranks 16 / 32: the streaming kernel for every tensor-core call (measured 512-row prefill +
+  // decodes: rank 16 10.9 us vs 17.6 on the tcgen05 pair, rank 32 13.6 vs 16.9); rank 64 below
+  // 1024 rows takes the segment-tile MMA pair K7 (128-row prefill + decodes 21.7 us vs 36.7 on
+  // the tcgen05 pair, 40.9 on K9; 512 rows 31.9 vs 38.3 / 41.2)
+  if ((s_n >= kStreamMinRows || t->rank <= 32) && stream_shape_ok(t)) return 4;
+  if (t->rank == 64 && mma_shape_ok(t)) return 3;
   if (tc_nq(t) > 0 && t->h_out % kTcNT == 0) return 5;  // measured: c4-128 10.8 us vs 12.3 on K7
   if (mma_shape_ok(t)) return 3;
   return 5;
