@@ -21,7 +21,7 @@ if [[ $what == *san* ]]; then
   CS=/usr/local/cuda/bin/compute-sanitizer
   F="--kernel-name kns=sgmv --kernel-name kns=dense --kernel-name kns=build_segments --kernel-name kns=permute"
   for tool in memcheck racecheck synccheck; do
-    SAN_MAX_CLUSTER=${SAN_MAX_CLUSTER:-16} timeout 1200 $CS --tool $tool $F --print-limit 100 python scripts/sanitize.py > $o/san/$tool.log 2>&1
+    SAN_MAX_CLUSTER=${SAN_MAX_CLUSTER:-16} timeout 1200 $CS --tool $tool $F --print-limit 100 python scripts/sanitize.py ${SAN_WHICH:-} > $o/san/$tool.log 2>&1
     echo "$tool=$?" >> $st
   done
 fi
@@ -38,7 +38,7 @@ if [[ $what == *ncu* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:sgmv -c 60 --csv \
     --log-file $o/launches_c4.csv python bench.py --preset c4 --profile --warmup 2 --sites 8 > /dev/null 2>&1
   echo "ncu_c4_list=$?" >> $st
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_tc -s 4 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_stream -s 4 -c 1 \
     -o $o/prof_c4 -f python bench.py --preset c4 --profile --warmup 2 --sites 8 > $o/ncu_c4.log 2>&1
   echo "ncu_c4=$?" >> $st
 fi
