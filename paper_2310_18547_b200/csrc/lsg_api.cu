@@ -275,7 +275,13 @@ int mma_split(int nstages, int tiles, int max_st, int target) {
   }
   return best;
 }
-constexpr int kMmaPartTarget = 160, kMmaExpTarget = 320;  // CTAs per kernel
+#ifndef LSG_MMA_PART_TARGET
+#define LSG_MMA_PART_TARGET 160
+#endif
+#ifndef LSG_MMA_EXP_TARGET
+#define LSG_MMA_EXP_TARGET 320
+#endif
+constexpr int kMmaPartTarget = LSG_MMA_PART_TARGET, kMmaExpTarget = LSG_MMA_EXP_TARGET;  // CTAs per kernel
 constexpr uint32_t kMmaPartSmemTarget = 150 * 1024;       // one partials CTA + one expand CTA per SM
 constexpr uint32_t kMmaSmemTarget = 110 * 1024;           // expand: two CTAs per SM
 // resident stages per CTA within the shared-memory target
@@ -851,7 +857,10 @@ Plan make_plan(const lsg_weight_table* t, int kernel, int n_seg, int s_n, bool f
     if (c_small == 0) c_small = cand;
     // behind the rank-16 streaming kernel (K9) the short-segment CTAs share SMs with its CTAs
     // (one each): at most ~128 CTAs (c4: C = 8 -> 4, 14.8 -> 14.1 us)
-    const int64_t limit = (long_on_tc && t->rank == 16 && stream_ok(t, s_n)) ? 128
+#ifndef LSG_DECODE_CAP_MAX_RANK
+#define LSG_DECODE_CAP_MAX_RANK 16
+#endif
+    const int64_t limit = (long_on_tc && t->rank <= LSG_DECODE_CAP_MAX_RANK && stream_ok(t, s_n)) ? 128
                           : (pl.tile_scan || cand <= 4)                       ? 256
                                                                               : 148;
     if (est_clusters * cand <= limit) c = cand;
