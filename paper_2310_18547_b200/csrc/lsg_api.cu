@@ -1286,10 +1286,10 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
   if (x == nullptr || y == nullptr || w == nullptr || seg_starts == nullptr || seg_slot == nullptr)
     return fail(LSG_EINVAL, "lsg_dense_lora: NULL pointer");
   if (ldx < tbl->h_in || ldy < tbl->h_out || ldw < tbl->h_out) return fail(LSG_EINVAL, "lsg_dense_lora: bad strides");
-  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % (kTcKB * kDlKS) != 0 || tbl->h_out % kDlN != 0 ||
+  if (tbl->rank != 16 || total_rows > kDlMaxRows || tbl->h_in % (kTcKB * kDlKS) != 0 || tbl->h_out % kDlN != 0 || tbl->h_out % 64 != 0 ||
       !aligned16(x) || !aligned16(y) || !aligned16(w) || ldx % 8 != 0 || ldy % 8 != 0 || ldw % 8 != 0 ||
       tbl->b_layer_stride % 8 != 0 || encode_tiled_fn() == nullptr)
-    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 256, h_out % 64, 16-byte rows");
+    return fail(LSG_EUNSUPPORTED, "lsg_dense_lora: rank 16, <= 64 rows, h_in % 256, h_out a multiple of the column tile, 16-byte rows");
   if (workspace == nullptr || workspace_bytes < lsg_dense_lora_workspace_size(tbl, total_rows) || !aligned16(workspace))
     return fail(LSG_EINVAL, "lsg_dense_lora: workspace too small");
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
@@ -1301,13 +1301,14 @@ int lsg_dense_lora(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
   if (!encode_map_2d(&p.tmap_x, tbl->dtype, x, static_cast<uint64_t>(tbl->h_in), static_cast<uint64_t>(total_rows),
                      static_cast<uint64_t>(ldx), kTcKB, kDlMaxRows, CU_TENSOR_MAP_SWIZZLE_128B))
     return fail(LSG_ECUDA, "tensor map x");
-  {
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(tbl->h_out), static_cast<cuuint64_t>(tbl->h_in)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kDlN), static_cast<cuuint32_t>(kTcKB)};
-    const cuuint32_t estr[2] = {1, 1};
+  {  // W [h_in][h_out] as 3-D {64 columns, h_in rows, h_out / 64 column blocks}: one box = kDlN / 64
+     // stacked [64 k][64 n] MN-major atoms
+    const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(tbl->h_in), static_cast<cuuint64_t>(tbl->h_out / 64)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, 128};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kTcKB), static_cast<cuuint32_t>(kDlN / 64)};
+    const cuuint32_t estr[3] = {1, 1, 1};
     if (encode_tiled_fn()(&p.tmap_w,
-                          tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          tbl->dtype == LSG_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                           const_cast<void*>(w), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)

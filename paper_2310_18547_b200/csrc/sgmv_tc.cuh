@@ -147,6 +147,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tmap, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
@@ -912,7 +920,10 @@ namespace lsg {
 // sum_k v[m,k] B_seg(m)[k,n] (fp32 chain over k; its rows' B slices staged by
 // cp.async ahead of the PDL wait) and rounds once.
 // ---------------------------------------------------------------------------------------
-constexpr int kDlN = 64;        // columns per cluster
+#ifndef LSG_DL_N
+#define LSG_DL_N 64
+#endif
+constexpr int kDlN = LSG_DL_N;  // columns per cluster (64 or 128: W as kDlN / 64 stacked 64-column boxes)
 constexpr int kDlMaxRows = 64;  // decode rows per launch
 constexpr int kDlKS = 4;        // K split = cluster size; CTA c owns rows [16c, 16c + 16)
 constexpr int kDlRowsPer = kDlMaxRows / kDlKS;
@@ -927,7 +938,7 @@ constexpr int kDlStage = kDlXB + kTcKB * kDlN * 2;
 
 struct DenseLoraParams {
   CUtensorMap tmap_x;  // x [s_n, h_in], box 64 (k) x 64 rows, SW128
-  CUtensorMap tmap_w;  // W [h_in, h_out] row-major, box 64 (N) x 64 (K), SW128
+  CUtensorMap tmap_w;  // W [h_in, h_out] row-major as 3-D {64 (N), h_in (K), h_out / 64}, box {64, 64, kDlN / 64}, SW128
   void* y;
   int64_t ldy;
   const float* v;      // [s_n, R] fp32
@@ -1018,7 +1029,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
   if (warp == 1 && lane == 0)
     for (int kb = 0; kb < pre; ++kb) {
       mbar_arrive_expect_tx(&bars[kb], kDlStage);
-      tma_load_2d(smem + kb * kDlStage + kDlXB, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[kb]);
+      tma_load_3d(smem + kb * kDlStage + kDlXB, &p.tmap_w, 0, (kb0 + kb) * kTcKB, n0 / 64, &bars[kb]);
     }
   pdl_wait();  // x and v come from the preceding kernels
   pdl_launch_dependents();
@@ -1030,7 +1041,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
       mbar_arrive_expect_tx(&bars[s], kDlStage);
       uint8_t* st = smem + s * kDlStage;
       tma_load_2d(st, &p.tmap_x, (kb0 + kb) * kTcKB, 0, &bars[s]);
-      tma_load_2d(st + kDlXB, &p.tmap_w, n0, (kb0 + kb) * kTcKB, &bars[s]);
+      tma_load_3d(st + kDlXB, &p.tmap_w, 0, (kb0 + kb) * kTcKB, n0 / 64, &bars[s]);
     }
   } else if (warp == 0 && lane == 0) {  // MMA issuer
     const uint32_t idesc = umma_idesc(fmt, kTcM, kDlN);
@@ -1075,8 +1086,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense_lora_kernel(const __grid_
   mbar_wait(bar_recv, 0);
   __syncthreads();  // every thread's B slices visible
   // my 16 rows x 64 columns: thread -> (row tid / 8, 8 columns)
-  {
-    const int ml = tid / 8, cg = (tid % 8) * 8, m = c * kDlRowsPer + ml;
+#pragma unroll
+  for (int half = 0; half < kDlN / 64; ++half) {
+    const int ml = tid / 8, cg = half * 64 + (tid % 8) * 8, m = c * kDlRowsPer + ml;
     if (m < p.s_n) {
       float acc[8];
 #pragma unroll
