@@ -556,7 +556,8 @@ bool prepare_long_segments(LongPlan& lp, void* y, int64_t ldy, const void* x, in
                        CU_TENSOR_MAP_SWIZZLE_128B) ||
         !encode_b_blocks(&q.tmap_b, tbl->dtype, x, tbl->h_out, R, stream_kc(R) / 64) ||
         !encode_rows_blocks(&q.tmap_x, tbl->dtype, x, tbl->h_in, s_n, ldx, stream_kc(R) / 64) ||
-        !encode_rows_blocks(&q.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy, stream_kc(R) / 64))
+        !encode_rows_blocks(&q.tmap_y, tbl->dtype, y, tbl->h_out, s_n, ldy, stream_kc(R) / 64) ||
+        !encode_rows_blocks(&q.tmap_y1, tbl->dtype, y, tbl->h_out, s_n, ldy, 1))
       return false;
     q.x = x;
     q.y = y;

@@ -83,6 +83,19 @@ constexpr int kStreamMaxStages = 16;  // ring slots (barriers reserved)
 #ifndef LSG_STREAM_ABOX
 #define LSG_STREAM_ABOX 1
 #endif
+// L2 prefetch of the tile's activation rows: 0 none; 1 x at entry, y_old too when the grid has
+// fewer than kStreamPfYMaxTiles tiles (measured: with y_old c4 14.1 us, 2048-row rank-32 21.6,
+// 512-row rank-16 10.7; without it 13.5 / 20.6 / 11.8 -- the extra early traffic pays only while
+// the grid leaves SMs idle); 2 x and y_old at entry; 3 y_old once v is ready (c4 14.4); 4 y_old
+// after the PDL wait (c4 14.6)
+#ifndef LSG_STREAM_PF
+#define LSG_STREAM_PF 1
+#endif
+constexpr unsigned kStreamPfYMaxTiles = 96;
+// 1: each consumer warp stores its own 64-column boxes of a full tile (no block barrier per stage)
+#ifndef LSG_STREAM_WARP_STORE
+#define LSG_STREAM_WARP_STORE 0
+#endif
 // Rank 16: KC = 512 in a 140 KB ring (four 32 KB slots): the short-segment kernel of the same
 // call (70 KB CTAs) then shares the SMs instead of waiting for streaming CTAs to exit
 // (c4: 16.2 -> 14.8 us; KC 1024 in 220 KB: three 64 KB slots, one CTA per SM)
@@ -123,6 +136,7 @@ struct StreamParams {
                        // count, not the bytes, is what L2 weight traffic costs: tma_probe.cu)
   CUtensorMap tmap_x;  // x as 3-D {64 columns, s_n rows, h_in / 64 blocks}, box {64, 16, KC / 64}, SW128
   CUtensorMap tmap_y;  // y likewise over h_out (loads of y_old, stores of full tiles)
+  CUtensorMap tmap_y1; // y with a one-block box {64, 16, 1} (per-warp stores, LSG_STREAM_WARP_STORE)
   const void* x;
   void* y;
   int64_t ldx;
@@ -206,8 +220,10 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   } else if (warp == 1) {
     const T* X = static_cast<const T*>(p.x) + static_cast<int64_t>(r0) * p.ldx;
     const T* Y = static_cast<const T*>(p.y) + static_cast<int64_t>(r0) * p.ldy;
-    if (lane < rows) bulk_prefetch_l2(X + lane * p.ldx, static_cast<uint32_t>(p.h_in * 2));
-    else if (lane >= 16 && lane - 16 < rows) bulk_prefetch_l2(Y + (lane - 16) * p.ldy, static_cast<uint32_t>(p.h_out * 2));
+    if (LSG_STREAM_PF >= 1 && lane < rows) bulk_prefetch_l2(X + lane * p.ldx, static_cast<uint32_t>(p.h_in * 2));
+    else if ((LSG_STREAM_PF == 2 || (LSG_STREAM_PF == 1 && gridDim.x < kStreamPfYMaxTiles)) && lane >= 16 &&
+             lane - 16 < rows)
+      bulk_prefetch_l2(Y + (lane - 16) * p.ldy, static_cast<uint32_t>(p.h_out * 2));
   }
   if (warp == kStreamCW) {  // --------------------------------------------------------- producer
     if constexpr (!kALin) make_slot_tmap(&p.tmap_a, smap, gmap, static_cast<const T*>(p.a_ptr[slot]) + p.a_off, lane);
@@ -275,6 +291,8 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   // ------------------------------------------------------------------------------ consumers
   pdl_wait();  // (returns at once by the time any y is written)
   pdl_launch_dependents();
+  if (LSG_STREAM_PF == 4 && warp == 1 && lane < rows)
+    bulk_prefetch_l2(static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + lane) * p.ldy, static_cast<uint32_t>(p.h_out * 2));
   const bool two = rows > 8;  // second n8 tile of the shrink (rows 8..15)
   const int xr = (lane & 7) + ((lane >> 4) << 3), xc = (lane >> 3) & 1;  // row-major 16 x 16 blocks
   const int ak = (lane & 7) + ((lane >> 4) << 3), ac = (lane >> 3) & 1;  // .trans blocks of [k][n] rows
@@ -336,6 +354,8 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
   }
   named_barrier_sync(1, 32 * kStreamCW);
   if (tid == 0) LSG_STREAM_TRACE(4);
+  if (LSG_STREAM_PF == 3 && warp == 1 && lane < rows)
+    bulk_prefetch_l2(static_cast<const T*>(p.y) + static_cast<int64_t>(r0 + lane) * p.ldy, static_cast<uint32_t>(p.h_out * 2));
   for (int i = tid * 8; i < kMmaM * R; i += 32 * kStreamCW * 8) {
     float f[8];
 #pragma unroll
@@ -413,6 +433,19 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       }
     }
 #if LSG_STREAM_ABOX
+#if LSG_STREAM_WARP_STORE
+    if (rows == kMmaM) {  // full tile: every warp stores its own 64-column boxes (no block barrier)
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int bi = 0; bi < BPW; ++bi)
+          tma_store_3d(&p.tmap_y1, ys + (warp * BPW + bi) * (kMmaM * 128), 0, r0, j * (KC / 64) + warp * BPW + bi);
+        bulk_commit_group();
+        bulk_wait_group_read<1>();
+        if (j > 0) mbar_arrive_local(&empty[(s - 1) % S]);
+      }
+    } else
+#endif
     if (rows == kMmaM) {                      // full tile: ONE 3-D box store of the stage
       fence_proxy_async_smem();               // epilogue writes -> the TMA store
       named_barrier_sync(1, 32 * kStreamCW);  // the stage's y tile is complete
@@ -434,10 +467,17 @@ __global__ void __launch_bounds__(kStreamThreads) sgmv_stream_kernel(const __gri
       if (lane == 0) mbar_arrive_local(&empty[s % S]);
     }
   }
+#if LSG_STREAM_WARP_STORE
+  if (rows == kMmaM && lane == 0) {  // this warp's last stores
+    bulk_wait_group_read<0>();
+    mbar_arrive_local(&empty[(nst - 1) % S]);
+  }
+#else
   if (rows == kMmaM && tid == 0) {  // the last stage's store
     bulk_wait_group_read<0>();
     mbar_arrive_local_cnt(&empty[(nst - 1) % S], kStreamCW);
   }
+#endif
 #else
     fence_proxy_async_smem();                 // epilogue writes -> the bulk stores
     named_barrier_sync(1, 32 * kStreamCW);    // the stage's y tile is complete
