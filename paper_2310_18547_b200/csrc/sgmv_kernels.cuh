@@ -28,6 +28,11 @@
 
 #include "sgmv_device.cuh"
 
+// 1: the first tile's y_old rows are L2-prefetched with x ahead of the PDL wait (A/B knob)
+#ifndef LSG_FAST_PF_Y
+#define LSG_FAST_PF_Y 1
+#endif
+
 namespace lsg {
 
 namespace cg = cooperative_groups;
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, MT == 1 ? LSG_MIN_BLOCKS : 1)
       if (kSh && lane < rows && nqc > 0)
         bulk_prefetch_l2(static_cast<const T*>(s_x) + static_cast<int64_t>(r0 + lane) * s_ldx + q0 * KW,
                          static_cast<uint32_t>(ndl * sizeof(T)));
-      if (kEx && lane >= 16 && lane - 16 < rows && ncv > 0)
+      if (LSG_FAST_PF_Y && kEx && lane >= 16 && lane - 16 < rows && ncv > 0)
         bulk_prefetch_l2(static_cast<const T*>(s_y) + static_cast<int64_t>(r0 + lane - 16) * s_ldy + cv0 * 8,
                          static_cast<uint32_t>(ncv * 16));
     }
