@@ -399,9 +399,13 @@ class Workload:
         self.seg_slot = self.slots.cuda()
         self.row_slot = torch.repeat_interleave(self.slots, torch.tensor(np.diff(self.bounds), dtype=torch.int64)).to(
             torch.int32).cuda()
-        # The serving engine knows its step's segment lengths: a decode-only step (no segment
-        # of >= 128 rows) skips the tensor-core pass -- a per-call option (lsg_call_opts).
-        self.tc_min_rows = self.rows + 1 if max(np.diff(self.bounds), default=0) < 128 else None
+        # The serving engine knows its step's segment lengths and passes them as a per-call
+        # option (lsg_call_opts): a step with no segment of >= 128 rows (256 at rank 16, the
+        # measured crossover, one prefill + decodes: 128 rows 5.7 us on the CUDA-core row mode
+        # vs 10.3 on the tensor cores, 192 rows 9.9 vs 10.2, 256 rows 10.7 vs 10.4) skips the
+        # tensor-core pass.
+        crossover = 256 if r == 16 else 128
+        self.tc_min_rows = self.rows + 1 if max(np.diff(self.bounds), default=0) < crossover else None
         if a.tc_min_rows > 0:
             self.tc_min_rows = a.tc_min_rows
         self.bytes = alg_bytes(self.rows, self.nseg, h, r)

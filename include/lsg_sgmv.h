@@ -293,9 +293,11 @@ typedef enum {
   LSG_OPT_NO_ROW_MODE = 7,     /* 1: one-row tiles use the segment-major decode (row split / tile scan)
                                   instead of one cluster per row with a segment search */
   LSG_OPT_NO_MULTIROW_TILES = 8, /* 1: rank 64 keeps one-row tiles even when rows share adapters */
-  LSG_OPT_TC_MIN_ROWS = 9,      /* 0 (default 384 at rank 16, 128 otherwise -- the measured
-                                   crossover): segments with at least this many rows take the
-                                   tensor-core path.  A call with >= this many rows launches the
+  LSG_OPT_TC_MIN_ROWS = 9,      /* 0 (default 128): segments with at least this many rows take the
+                                   tensor-core path (rank 16 measured crossover ~256 rows: an engine
+                                   whose step has no segment that long passes a threshold above the
+                                   batch size per call,
+                                   see lsg_api.cu tc_min_rows).  A call with >= this many rows launches the
                                    tensor-core kernel even when no segment turns out that long (the
                                    host does not read segment lengths), which costs ~1 us per launch
                                    at 128-256 decode rows: an engine that knows a step has no prefill

@@ -165,14 +165,18 @@ int tc_tile_bound(const lsg_weight_table* t, int s_n, int n_seg) {
   return std::max(1, s_n / kTcM + std::min(n_seg, s_n / tc_min_rows(t)));
 }
 
-// Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default:
-// 384 at rank 16, else 128).  Measured crossover at rank 16, h = 4096 (one prefill segment +
-// decodes, µs per site, CUDA-core row mode vs tensor cores): 128 rows 5.7 vs 10.8, 256 rows
-// 10.6 vs 11.2, 512 rows 17.7 vs 11.7.  Without a table: the smallest default (tile bounds).
+// Rows from which a segment takes the tensor-core path (LSG_OPT_TC_MIN_ROWS, 0 = default 128).
+// The measured crossover at rank 16 is higher (h = 4096, one prefill segment + decodes, µs per
+// site, CUDA-core row mode vs tensor cores: 128 rows 5.7 vs 10.3, 192 rows 9.9 vs 10.2, 256
+// rows 10.7 vs 10.4, 512 rows 17.7 vs 10.8), but a higher default starves calls whose short
+// segments are long-ish: with a tensor-core pass in the call the short-segment kernel runs
+// tile-scan on a grid sized by the segment count (threshold 384, two 300-row segments: 1117 us
+// per site).  So the library keeps 128, and an engine that knows its step has no segment of
+// >= 256 rows passes a threshold above the batch size per call (lsg_call_opts; bench.py does).
 int tc_min_rows(const lsg_weight_table* t) {
+  (void)t;
   const int x = cur().tc_min_rows;
-  if (x > 0) return x;
-  return t != nullptr && t->rank == 16 ? kTcMinRows16 : kTcMinRows;
+  return x > 0 ? x : kTcMinRows;
 }
 
 bool tc2_choose(const lsg_weight_table* t, struct Tc2Choice* out);
@@ -1013,7 +1017,11 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   // With the long segments on the tensor cores, the short ones have at most n_seg
   // segments' worth of work items in practice: size the tile-scan grid by that
   // (clusters loop over further tiles) instead of by s_n.
-  if (skip_long && pl.tile_scan) pl.clusters = std::min(pl.clusters, std::max(1, n_seg));
+#ifndef LSG_SKIP_LONG_MIN_CTAS
+#define LSG_SKIP_LONG_MIN_CTAS 0
+#endif
+  if (skip_long && pl.tile_scan)
+    pl.clusters = std::min(pl.clusters, std::max({1, n_seg, LSG_SKIP_LONG_MIN_CTAS / std::max(1, pl.cluster)}));
 
   FastParams p{};
   p.y = y;

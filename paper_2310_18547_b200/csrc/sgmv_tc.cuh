@@ -32,7 +32,6 @@
 namespace lsg {
 
 constexpr int kTcMinRows = 128;  // segments at least this long use the tensor-core path
-constexpr int kTcMinRows16 = 384;  // rank 16 (measured crossover, lsg_api.cu tc_min_rows)
 constexpr int kTcM = 128;        // rows per tile (UMMA M)
 constexpr int kTcKB = 64;        // K per x box (128 bytes of 16-bit)
 constexpr int kTcBox = kTcM * kTcKB * 2;  // 16 KB per 64 x 128 box

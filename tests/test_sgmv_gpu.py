@@ -679,14 +679,13 @@ def test_pdl_chain_of_dependent_launches(lsg, lens):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("r,prefill,on_tc", [(16, 128, False), (16, 300, False), (16, 512, True), (32, 128, True),
+@pytest.mark.parametrize("r,prefill,on_tc", [(16, 128, True), (16, 300, True), (16, 512, True), (32, 128, True),
                                              (64, 128, True)])
 def test_default_long_segment_dispatch_by_rank(lsg, r, prefill, on_tc):
-    """The automatic dispatch: a rank-16 prefill below 384 rows stays on the
-    CUDA-core kernel (bitwise the no-tensor-core run), longer ones and rank 32 / 64 prefills of 128
-    rows run on the tensor cores (K9 / K7: not bitwise the CUDA-core result) -- the call must not
-    fall back silently, e.g. on a workspace bound computed with another threshold.  Both forms
-    stay within the oracle tolerance."""
+    """The automatic dispatch: prefills of >= 128 rows run on the tensor
+    cores (K9 at ranks 16 / 32, K7 at rank 64 below 1024 rows: not bitwise the CUDA-core result)
+    -- the call must not fall back silently, e.g. on a workspace bound computed with another
+    threshold.  Both forms stay within the oracle tolerance."""
     bounds = np.concatenate([[0, prefill], prefill + np.arange(1, 32)]).astype(np.uint64)
     x, A, B = random_problem(4096, 4096, r, bounds, 321 + r)
     p = Problem(lsg, x, A, B, bounds, torch.float16)
