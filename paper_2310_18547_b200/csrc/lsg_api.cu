@@ -1017,8 +1017,12 @@ int run(int kernel, void* y, int64_t ldy, const void* x, int64_t ldx, float* v_o
   // With the long segments on the tensor cores, the short ones have at most n_seg
   // segments' worth of work items in practice: size the tile-scan grid by that
   // (clusters loop over further tiles) instead of by s_n.
+// ... but at least ~256 CTAs: the host does not know how many rows the short segments hold, and
+// a grid of n_seg clusters starves calls with few, long-ish short segments (four 100-row
+// segments in a call with a tensor-core pass: 4 clusters).  Measured: c4 13.5 -> 13.4 us,
+// 1024-row prefill + decodes 11.6 -> 10.8, two 300-row segments under a 384 threshold 1117 -> 156.
 #ifndef LSG_SKIP_LONG_MIN_CTAS
-#define LSG_SKIP_LONG_MIN_CTAS 0
+#define LSG_SKIP_LONG_MIN_CTAS 256
 #endif
   if (skip_long && pl.tile_scan)
     pl.clusters = std::min(pl.clusters, std::max({1, n_seg, LSG_SKIP_LONG_MIN_CTAS / std::max(1, pl.cluster)}));
